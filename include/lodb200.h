@@ -1,0 +1,160 @@
+/*
+ * lodb200 -- C ABI of the B200-native LOD-construction path.
+ *
+ * Drop-in boundary for the reference's two-stage Python API
+ *   partition(cloud, config) -> Octree        pkg/src/lodforge/partition.py:300-302
+ *     (+ forced world bounds: Partitioner(cloud, config, bounds), partition.py:82,87)
+ *   build_lod(tree, strategy, seed) -> Octree  pkg/src/lodforge/sampling.py:165-176
+ * and of the north-star fused form build_lod(points, colors, T, grid, mode).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Point buffers are DEVICE pointers to packed records
+ *    (see lod_point_format); the library never frees caller memory.
+ *  - Calls are synchronous with respect to the given CUDA stream (passed as void*,
+ *    NULL = legacy default stream) and return a status code; lod_last_error() gives the
+ *    message of the last failure on the calling thread.
+ *  - A lod_tree owns its device buffers (leaf points, voxels, node table, scratch) and
+ *    reuses them across builds (grow-only), so repeated builds do not allocate.
+ *  - Not reentrant per lod_tree; distinct trees may be used from distinct threads.
+ *
+ * Status codes map to the reference's exceptions at the Python boundary:
+ *   LOD_EVALUE        -> ValueError        (empty cloud, non-finite bounds, bad config,
+ *                                            unknown strategy; model.py:118-124,202-205,
+ *                                            partition.py:83-84, sampling.py:169-170)
+ *   LOD_ECONSISTENCY  -> ConsistencyError  (2^20 random limit sampling.py:73-75, internal
+ *                                            invariants partition.py:170,191,224,239,260,269,286)
+ *   LOD_ECUDA         -> RuntimeError      (CUDA / NCCL failure)
+ *   LOD_EUNSUPPORTED  -> NotImplementedError (first-come / weighted strategies, configs
+ *                                            outside the supported envelope)
+ */
+#ifndef LODB200_H
+#define LODB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOD_OK 0
+#define LOD_EVALUE 1
+#define LOD_ECONSISTENCY 2
+#define LOD_ECUDA 3
+#define LOD_EUNSUPPORTED 4
+
+/* Point record layouts (device). */
+enum lod_point_format {
+  LOD_POINTS_F32 = 0, /* 16 B: float x, y, z; uint8 r, g, b, pad */
+  LOD_POINTS_F64 = 1  /* 32 B: double x, y, z; uint8 r, g, b, pad[5] */
+};
+
+/* Voxel sampling strategies (model.py:127 STRATEGIES, restricted to the GPU path). */
+enum lod_mode {
+  LOD_MODE_RANDOM = 0,  /* sampling.py:69-85 */
+  LOD_MODE_AVERAGE = 1  /* sampling.py:88-97 ("color_filter") */
+};
+
+/* BuildConfig (model.py:108-124). grid_size is not a field: the reference never reads it. */
+typedef struct lod_config {
+  uint32_t T;              /* max points per non-oversized leaf, >= 1 */
+  int32_t initial_depth;   /* main counting grid depth (8 -> 256^3), 0..10 */
+  int32_t extension_depth; /* levels per extension round, 1..5 */
+  int32_t max_depth;       /* initial_depth..16 */
+} lod_config;
+
+/* Summary of a built tree. */
+typedef struct lod_tree_info {
+  uint64_t n_points;
+  uint64_t n_voxels;       /* sum of inner-node voxels after lod_voxelize, else 0 */
+  uint32_t n_nodes;
+  uint32_t n_leaves;
+  uint32_t n_inner;
+  uint32_t depth;          /* deepest node depth */
+  int32_t point_format;
+  int32_t voxel_mode;      /* -1 until lod_voxelize succeeded */
+  double world_min[3];
+  double world_size;
+  uint32_t n_ext_grids;    /* extension pyramids created (partition.py:109-151) */
+  uint32_t radix_passes;   /* stable-distribute passes used */
+} lod_tree_info;
+
+/* One node of the exported node table (DFS-independent order: main pyramid levels
+ * coarse->fine, then extension pyramids).  Node 0 is the root. */
+typedef struct lod_node {
+  double min[3];           /* bounds_at(world, path) min, sequential fp64 adds (model.py:62-81) */
+  double size;
+  uint64_t first;          /* leaf: first point in the leaf buffer; inner: first voxel */
+  uint32_t count;          /* leaf: points; inner: voxels (0 before lod_voxelize) */
+  int32_t parent;          /* -1 for the root */
+  uint16_t cell[3];        /* absolute cell coordinates at `depth`; path digits are its bits */
+  uint8_t depth;
+  uint8_t flags;           /* bit0 leaf, bit1 oversized (partition.py:222) */
+  int32_t child[8];        /* node ids by octant, -1 if absent */
+} lod_node;
+
+typedef struct lod_tree lod_tree;
+
+/* Handle lifecycle.  `device` is the CUDA ordinal the tree's buffers live on. */
+lod_tree* lod_tree_create(int device);
+void lod_tree_destroy(lod_tree* tree);
+
+/* partition(): split n points (device records of `format`) into leaves of <= T points.
+ * bounds_or_null: NULL -> cubic world bounds of the points (model.py:199-209); else
+ * {min_x, min_y, min_z, size} forced bounds (points outside -> LOD_ECONSISTENCY). */
+int lod_split(lod_tree* tree, const void* d_points, uint64_t n, int format,
+              const double* bounds_or_null, const lod_config* config, void* stream);
+
+/* build_lod(tree, strategy, seed): fill every inner node with voxels, deepest first. */
+int lod_voxelize(lod_tree* tree, int mode, uint64_t seed, void* stream);
+
+/* north-star fused build: lod_split (world bounds) + lod_voxelize. */
+int lod_build(lod_tree* tree, const void* d_points, uint64_t n, int format,
+              const lod_config* config, int mode, uint64_t seed, void* stream);
+
+int lod_tree_get_info(const lod_tree* tree, lod_tree_info* out);
+
+/* Copy the node table to host memory (n_nodes entries). */
+int lod_tree_copy_nodes(const lod_tree* tree, lod_node* host_nodes, void* stream);
+
+/* Device pointers of the outputs (valid until the next build on this tree):
+ * leaf points: n_points records of the input format, grouped by leaf, input order within
+ *              a leaf (partition.py:262 stable order);
+ * voxels: n_voxels x {uint32 key = (x*128 + y)*128 + z, uint32 rgb = r | g<<8 | b<<16},
+ *         per inner node ascending key (sampling.py:83-85, 97). */
+int lod_tree_leaf_points(const lod_tree* tree, const void** d_ptr);
+int lod_tree_voxels(const lod_tree* tree, const void** d_ptr);
+
+/* Host copies of the outputs (sizes from lod_tree_get_info). */
+int lod_tree_copy_leaf_points(const lod_tree* tree, void* host, void* stream);
+int lod_tree_copy_voxels(const lod_tree* tree, void* host, void* stream);
+
+/* Device memory currently held by the tree, bytes. */
+uint64_t lod_tree_device_bytes(const lod_tree* tree);
+
+/* Per-stage device times of the last build in milliseconds (CUDA events), for profiling:
+ * out[0] bounds+count, [1] extension, [2] merge+nodes+targets, [3] distribute, [4] voxelize.
+ * Timing is recorded only when enabled (small overhead from event records). */
+int lod_set_timing(lod_tree* tree, int enabled);
+int lod_tree_stage_ms(const lod_tree* tree, float* out5);
+
+/* Number of kernel launches issued by the last lod_split + lod_voxelize. */
+uint64_t lod_tree_launches(const lod_tree* tree);
+
+/* Deterministic synthetic generators on the device, rows
+ * [start, start+n) of cloud `kind` ("sphere", "terrain", "scene", "cluster", "surface")
+ * written as LOD_POINTS_F32 records.  `table`: scene object table from the host
+ * generator (65 x {kind, 7 params, cdf}) or NULL for the other kinds. */
+int lod_generate(const char* kind, uint64_t seed, uint64_t start, uint64_t n, void* d_out,
+                 const double* table_or_null, void* stream);
+
+/* Message of the last failure on the calling thread. */
+const char* lod_last_error(void);
+
+/* Library version string. */
+const char* lod_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LODB200_H */

@@ -1,0 +1,684 @@
+// C ABI + host orchestration of one LOD build (include/lodb200.h).
+//
+// The host side only sequences launches and reads a handful of scalars back; all
+// per-point and per-cell work is on the device.  Synchronisation points per build:
+//   1. after counting (+1 per extension round)   -> extension grids to create
+//   2. after node enumeration                    -> node-table size
+//   3. after leaf numbering                      -> leaf count, per-depth inner lists
+//   4. end of distribute / end of voxelize       -> error flags
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace lod {
+
+static thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int fail_cuda(cudaError_t e, const char* what) {
+  return fail(LOD_ECUDA, "CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+static size_t round_up(size_t b) { return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1); }
+
+// grow-only; keep_bytes of the old contents are preserved when growing
+static cudaError_t ensure(DevBuf& b, size_t bytes, size_t keep_bytes = 0, cudaStream_t s = 0) {
+  if (bytes <= b.cap) return cudaSuccess;
+  void* np = nullptr;
+  size_t cap = round_up(bytes);
+  cudaError_t e = cudaMalloc(&np, cap);
+  if (e != cudaSuccess) return e;
+  if (b.p) {
+    if (keep_bytes) {
+      e = cudaMemcpyAsync(np, b.p, keep_bytes, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return e;
+      cudaStreamSynchronize(s);
+    }
+    cudaFree(b.p);
+  }
+  b.p = np;
+  b.cap = cap;
+  return cudaSuccess;
+}
+
+struct Round {
+  uint32_t first, count;
+  int ext, base;
+  uint64_t pyr_base, tgt_base;
+};
+
+}  // namespace lod
+
+using namespace lod;
+
+struct lod_tree {
+  int device = 0;
+  int fmt = LOD_POINTS_F32;
+  uint64_t n = 0;
+  lod_config cfg{};
+  bool split_done = false;
+  int voxel_mode = -1;
+  uint64_t n_voxels = 0;
+  uint64_t launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[6] = {};
+  float stage_ms[5] = {};
+
+  DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
+  DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
+  DevBuf leaf_node, leaf_first, depth_count, depth_off, depth_cursor, depth_lists;
+  DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf;
+  DevBuf vox, scratch, export_buf;
+  DevState* host_state = nullptr;  // pinned mirror
+
+  uint32_t n_nodes = 0, n_leaves = 0, n_ext = 0, max_depth_used = 0;
+  uint32_t inner_per_depth[kMaxDepth + 1] = {};
+  uint32_t inner_off[kMaxDepth + 1] = {};
+  std::vector<Round> rounds;
+  uint64_t total_slots = 0;
+  double world[4] = {};
+  RadixPlan plan{};
+  uint32_t epoch = 1;
+};
+
+namespace {
+
+int read_state(lod_tree* t, cudaStream_t s) {
+  LOD_CUDA_CHECK(cudaMemcpyAsync(t->host_state, t->state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  LOD_CUDA_CHECK(cudaStreamSynchronize(s));
+  return LOD_OK;
+}
+
+std::string path_of(uint64_t cell) {
+  uint32_t cx = (uint32_t)cell & 0xFFFF, cy = (uint32_t)(cell >> 16) & 0xFFFF, cz = (uint32_t)(cell >> 32) & 0xFFFF;
+  int depth = (int)(cell >> 48) & 0xFF;
+  std::string p = "(";
+  for (int b = depth - 1; b >= 0; --b) {
+    int o = ((cx >> b) & 1) | (((cy >> b) & 1) << 1) | (((cz >> b) & 1) << 2);
+    p += std::to_string(o);
+    if (b > 0 || depth == 1) p += depth == 1 ? "," : ", ";
+  }
+  return p + ")";
+}
+
+// Map device error bits to the reference's exceptions (messages as in the reference).
+int check_errors(lod_tree* t, cudaStream_t s) {
+  const DevState& h = *t->host_state;
+  uint32_t e = h.err;
+  if (!e) return LOD_OK;
+  auto node_path = [&](uint32_t k) -> std::string {
+    uint64_t cell = 0;
+    if (t->n_cell.p && k < t->n_nodes)
+      cudaMemcpy(&cell, t->n_cell.as<uint64_t>() + k, 8, cudaMemcpyDeviceToHost);
+    return path_of(cell);
+  };
+  (void)s;
+  if (e & ERR_NONFINITE) return fail(LOD_EVALUE, "point coordinates must be finite");
+  if (e & ERR_OUTSIDE) return fail(LOD_ECONSISTENCY, "point outside bounds during grid projection");
+  if (e & ERR_EXT_ROOT) return fail(LOD_ECONSISTENCY, "extended pyramid root must be unmergeable");
+  if (e & ERR_OVERSIZED) return fail(LOD_ECONSISTENCY, "oversized leaf away from max depth");
+  if (e & ERR_NO_ROOT) return fail(LOD_ECONSISTENCY, "partition produced no root node");
+  if (e & ERR_NO_PARENT)
+    return fail(LOD_ECONSISTENCY, "node %s has no inner parent", node_path(h.err_detail).c_str());
+  if (e & ERR_UNRESOLVED) return fail(LOD_ECONSISTENCY, "point did not resolve to a leaf node");
+  if (e & ERR_COUNT) return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
+  if (e & ERR_RANDOM_LIMIT) {
+    // The reference raises at the first offending node in (depth desc, DFS preorder) order
+    // (sampling.py:171-173); levels run deepest first, so the first raise fixed the depth.
+    // Pick the DFS-first offender at that depth from the node table.
+    std::vector<uint64_t> cell(t->n_nodes);
+    std::vector<uint32_t> val(t->n_nodes), cnt(t->n_nodes);
+    std::vector<int32_t> child(8ull * t->n_nodes);
+    cudaMemcpy(cell.data(), t->n_cell.p, 8ull * t->n_nodes, cudaMemcpyDeviceToHost);
+    cudaMemcpy(val.data(), t->n_val.p, 4ull * t->n_nodes, cudaMemcpyDeviceToHost);
+    cudaMemcpy(cnt.data(), t->n_count.p, 4ull * t->n_nodes, cudaMemcpyDeviceToHost);
+    cudaMemcpy(child.data(), t->n_child.p, 32ull * t->n_nodes, cudaMemcpyDeviceToHost);
+    int d0 = (int)(cell[h.err_detail] >> 48) & 0xFF;
+    uint64_t best_code = ~0ull, best_s = h.err_value;
+    for (uint32_t k = 0; k < t->n_nodes; ++k) {
+      if (val[k] != UNMERGEABLE || (int)((cell[k] >> 48) & 0xFF) != d0) continue;
+      uint64_t S = 0;
+      for (int o = 0; o < 8; ++o)
+        if (child[8ull * k + o] >= 0) S += cnt[child[8ull * k + o]];
+      if (S < (uint64_t)kRandomLimit) continue;
+      uint32_t cx = (uint32_t)cell[k] & 0xFFFF, cy = (uint32_t)(cell[k] >> 16) & 0xFFFF,
+               cz = (uint32_t)(cell[k] >> 32) & 0xFFFF;
+      uint64_t code = 0;
+      for (int b = d0 - 1; b >= 0; --b)
+        code = code * 8 + (((cx >> b) & 1) | (((cy >> b) & 1) << 1) | (((cz >> b) & 1) << 2));
+      if (code < best_code) best_code = code, best_s = S;
+    }
+    return fail(LOD_ECONSISTENCY, "%llu samples exceed the 20-bit index limit of random sampling",
+                (unsigned long long)best_s);
+  }
+  if (e & ERR_EMPTY_CHILD) return fail(LOD_ECONSISTENCY, "child of node %s has no samples",
+                                       node_path(h.err_detail).c_str());
+  return fail(LOD_ECONSISTENCY, "device error 0x%x", e);
+}
+
+SplitView make_view(lod_tree* t, const void* pts) {
+  SplitView v{};
+  v.st = t->state.as<DevState>();
+  v.pts = pts;
+  v.n = t->n;
+  v.D = t->cfg.initial_depth;
+  v.max_depth = t->cfg.max_depth;
+  v.T = t->cfg.T;
+  v.pyr = t->pyr.as<uint32_t>();
+  v.main_cells = level_off(v.D + 1);
+  v.node_idx = t->node_idx.as<int32_t>();
+  v.t8 = t->t8.as<int32_t>();
+  v.te = t->te.as<int32_t>();
+  v.meta = t->meta.as<ExtMeta>();
+  v.n_ext = t->n_ext;
+  v.n_cell = t->n_cell.as<uint64_t>();
+  v.n_val = t->n_val.as<uint32_t>();
+  v.n_parent = t->n_parent.as<int32_t>();
+  v.n_child = t->n_child.as<int32_t>();
+  v.n_slot = t->n_slot.as<uint64_t>();
+  v.n_extid = t->n_extid.as<int32_t>();
+  v.n_lvl = t->n_lvl.as<uint8_t>();
+  v.n_leaf = t->n_leaf.as<int32_t>();
+  v.n_box = t->n_box.as<double4>();
+  v.n_first = t->n_first.as<uint64_t>();
+  v.n_count = t->n_count.as<uint32_t>();
+  v.n_nodes = t->n_nodes;
+  v.leaf_node = t->leaf_node.as<uint32_t>();
+  v.leaf_first = t->leaf_first.as<uint64_t>();
+  v.n_leaves = t->n_leaves;
+  return v;
+}
+
+int ceil_log2(uint64_t x) {
+  int b = 0;
+  while ((1ull << b) < x) ++b;
+  return b;
+}
+
+#define CK(expr) LOD_CUDA_CHECK(expr)
+#define RUN(expr)            \
+  do {                       \
+    int _r = (expr);         \
+    if (_r < 0) return fail(LOD_ECUDA, "internal scratch too small: %s", #expr); \
+    t->launches += _r;       \
+  } while (0)
+
+void mark(lod_tree* t, int i, cudaStream_t s) {
+  if (t->timing) cudaEventRecord(t->ev[i], s);
+}
+
+int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub, const lod_config* cfg,
+             cudaStream_t s) {
+  if (!t) return fail(LOD_EVALUE, "null tree");
+  if (!cfg) return fail(LOD_EVALUE, "null config");
+  if (n == 0) return fail(LOD_EVALUE, "cannot partition an empty point cloud");
+  if (cfg->T < 1) return fail(LOD_EVALUE, "T must be >= 1");
+  if (cfg->max_depth < cfg->initial_depth) return fail(LOD_EVALUE, "max_depth must be >= initial_depth");
+  if (cfg->max_depth > kMaxDepth) return fail(LOD_EVALUE, "max_depth must be <= %d", kMaxDepth);
+  if (cfg->initial_depth < 0 || cfg->initial_depth > 10)
+    return fail(LOD_EUNSUPPORTED, "initial_depth must be in [0, 10] on the GPU path");
+  if (cfg->extension_depth < 1 || cfg->extension_depth > 5)
+    return fail(LOD_EUNSUPPORTED, "extension_depth must be in [1, 5] on the GPU path");
+  if (fmt != LOD_POINTS_F32 && fmt != LOD_POINTS_F64) return fail(LOD_EVALUE, "unknown point format %d", fmt);
+  if (n >= 0xFFFFFFFFull) return fail(LOD_EUNSUPPORTED, "at most 2^32 - 2 points per GPU build");
+  if (ub && !(ub[3] > 0)) return fail(LOD_EVALUE, "AABB size must be positive");
+  CK(cudaSetDevice(t->device));
+
+  t->split_done = false;
+  t->voxel_mode = -1;
+  t->n_voxels = 0;
+  t->launches = 0;
+  t->n = n;
+  t->fmt = fmt;
+  t->cfg = *cfg;
+  t->n_ext = 0;
+  t->n_nodes = t->n_leaves = 0;
+  t->rounds.clear();
+  const int D = cfg->initial_depth;
+  const uint64_t main_cells = level_off(D + 1);
+  const uint64_t fine_cells = 1ull << (3 * D);
+  const size_t rec = fmt == LOD_POINTS_F32 ? 16 : 32;
+
+  mark(t, 0, s);
+  // device state
+  DevState init{};
+  for (int a = 0; a < 3; ++a) init.lo_key[a] = ~0ull, init.hi_key[a] = 0;
+  *t->host_state = init;
+  CK(ensure(t->state, sizeof(DevState)));
+  CK(cudaMemcpyAsync(t->state.p, t->host_state, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  CK(ensure(t->pyr, main_cells * 4));
+  CK(cudaMemsetAsync(t->pyr.p, 0, main_cells * 4, s));
+  CK(ensure(t->t8, fine_cells * 4));
+  CK(cudaMemsetAsync(t->t8.p, 0xFF, fine_cells * 4, s));
+  uint64_t scan_blocks = (std::max<uint64_t>(main_cells, n) + kScanTile - 1) / kScanTile + 2;
+  CK(ensure(t->scan, scan_blocks * 8));
+  ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+
+  SplitView v = make_view(t, pts);
+  RUN(launch_bounds(fmt, pts, n, v.st, ub, s));
+  RUN(launch_count(fmt, v, s));
+  mark(t, 1, s);
+
+  // ---- extension rounds (partition.py:109-151) ----
+  uint64_t ext_pyr_used = 0, ext_tgt_used = 0;
+  if (cfg->max_depth > D) {
+    uint64_t max_anchor = std::min<uint64_t>(fine_cells, n / ((uint64_t)cfg->T + 1) + 1);
+    CK(ensure(t->list, max_anchor * 8 + 8));
+    RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s));
+    int r = read_state(t, s);
+    if (r) return r;
+    if ((r = check_errors(t, s))) return r;
+    uint32_t cur = (uint32_t)t->host_state->count_a;
+    int base = D;
+    uint32_t first = 0, parent_first = 0;
+    int round = 0;
+    while (cur > 0) {
+      int ext = std::min(cfg->extension_depth, cfg->max_depth - base);
+      uint64_t psz = level_off(ext + 1), tsz = 1ull << (3 * ext);
+      uint64_t pyr_base = main_cells + ext_pyr_used, tgt_base = ext_tgt_used;
+      uint64_t new_pyr = (uint64_t)cur * psz, new_tgt = (uint64_t)cur * tsz;
+      CK(ensure(t->pyr, (pyr_base + new_pyr) * 4, pyr_base * 4, s));
+      CK(ensure(t->te, (tgt_base + new_tgt) * 4, tgt_base * 4, s));
+      CK(ensure(t->meta, (size_t)(first + cur) * sizeof(ExtMeta), (size_t)first * sizeof(ExtMeta), s));
+      CK(cudaMemsetAsync(t->pyr.as<uint32_t>() + pyr_base, 0, new_pyr * 4, s));
+      CK(cudaMemsetAsync(t->te.as<int32_t>() + tgt_base, 0xFF, new_tgt * 4, s));
+      v = make_view(t, pts);
+      RUN(launch_ext_create(v, round, first, cur, t->list.as<uint64_t>(), parent_first, pyr_base, tgt_base, base,
+                            ext, s));
+      t->n_ext = first + cur;
+      v = make_view(t, pts);
+      RUN(launch_ext_count(fmt, v, first, s));
+      t->rounds.push_back(Round{first, cur, ext, base, pyr_base, tgt_base});
+      ext_pyr_used += new_pyr;
+      ext_tgt_used += new_tgt;
+      uint32_t next = 0;
+      if (base + ext < cfg->max_depth) {
+        uint64_t cap_needed = std::min<uint64_t>((uint64_t)cur * tsz, n / ((uint64_t)cfg->T + 1) + 1);
+        CK(ensure(t->list, cap_needed * 8 + 8));
+        uint64_t sb = ((uint64_t)cur * tsz + kScanTile - 1) / kScanTile + 2;
+        CK(ensure(t->scan, sb * 8));
+        scr = ScanScratch{t->scan.as<uint64_t>(), t->scan.cap / 8};
+        v = make_view(t, pts);
+        RUN(launch_find_subanchors(v, first, cur, ext, t->list.as<uint64_t>(), scr, s));
+        if ((r = read_state(t, s))) return r;
+        next = (uint32_t)t->host_state->count_a;
+      }
+      parent_first = first;
+      first += cur;
+      base += ext;
+      cur = next;
+      ++round;
+    }
+  }
+  mark(t, 2, s);
+
+  // ---- merge (partition.py:155-170) ----
+  {
+    std::vector<uint32_t> rf, rc;
+    std::vector<int> re;
+    std::vector<uint64_t> rb;
+    for (auto& rd : t->rounds) rf.push_back(rd.first), rc.push_back(rd.count), re.push_back(rd.ext),
+        rb.push_back(rd.pyr_base);
+    v = make_view(t, pts);
+    RUN(launch_merge_all(v, rf.data(), rc.data(), re.data(), rb.data(), (int)t->rounds.size(), s));
+  }
+
+  // ---- node enumeration (partition.py:201-231) ----
+  t->total_slots = main_cells + ext_pyr_used;
+  uint64_t slot_cap = std::min<uint64_t>(t->total_slots, n * (uint64_t)(cfg->max_depth + 1) + 1);
+  CK(ensure(t->slots, slot_cap * 8));
+  CK(ensure(t->node_idx, t->total_slots * 4));
+  {
+    uint64_t sb = (t->total_slots + kScanTile - 1) / kScanTile + 2;
+    CK(ensure(t->scan, sb * 8));
+    scr = ScanScratch{t->scan.as<uint64_t>(), t->scan.cap / 8};
+  }
+  RUN(launch_count_nodes(v, t->total_slots, t->slots.as<uint64_t>(), scr, s));
+  int r = read_state(t, s);
+  if (r) return r;
+  if ((r = check_errors(t, s))) return r;
+  t->n_nodes = (uint32_t)t->host_state->count_b;
+  if (t->n_nodes == 0) return fail(LOD_ECONSISTENCY, "partition produced no root node");
+  const uint64_t nn = t->n_nodes;
+  CK(ensure(t->n_cell, nn * 8));
+  CK(ensure(t->n_val, nn * 4));
+  CK(ensure(t->n_parent, nn * 4));
+  CK(ensure(t->n_child, nn * 32));
+  CK(ensure(t->n_slot, nn * 8));
+  CK(ensure(t->n_extid, nn * 4));
+  CK(ensure(t->n_lvl, nn));
+  CK(ensure(t->n_leaf, nn * 4));
+  CK(ensure(t->n_box, nn * 32));
+  CK(ensure(t->n_first, nn * 8));
+  CK(ensure(t->n_count, nn * 4));
+  CK(ensure(t->leaf_node, nn * 4));
+  CK(ensure(t->leaf_first, nn * 8));
+  CK(ensure(t->depth_count, 64 * 4));
+  CK(cudaMemsetAsync(t->depth_count.p, 0, 64 * 4, s));
+  v = make_view(t, pts);
+  RUN(launch_build_nodes(v, t->slots.as<uint64_t>(), s));
+  RUN(launch_number_leaves(v, scr, s));
+  RUN(launch_depth_lists(v, t->depth_count.as<uint32_t>(), s));
+  CK(cudaMemcpyAsync(t->inner_per_depth, t->depth_count.p, sizeof(t->inner_per_depth), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&t->max_depth_used, t->depth_count.as<uint32_t>() + kMaxDepth + 1, 4, cudaMemcpyDeviceToHost,
+                     s));
+  if ((r = read_state(t, s))) return r;
+  if ((r = check_errors(t, s))) return r;
+  t->n_leaves = (uint32_t)t->host_state->count_a;
+  v = make_view(t, pts);
+  RUN(launch_leaf_offsets(v, scr, s));
+  RUN(launch_targets(v, s));
+  for (auto& rd : t->rounds) RUN(launch_targets_ext(v, rd.first, rd.count, rd.ext, s));
+  // per-depth inner-node lists for the voxelizer
+  uint32_t off = 0;
+  for (int d = 0; d <= kMaxDepth; ++d) t->inner_off[d] = off, off += t->inner_per_depth[d];
+  CK(ensure(t->depth_lists, (size_t)std::max<uint32_t>(off, 1) * 4));
+  CK(ensure(t->depth_off, 64 * 4));
+  CK(ensure(t->depth_cursor, 64 * 4));
+  CK(cudaMemcpyAsync(t->depth_off.p, t->inner_off, sizeof(t->inner_off), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(t->depth_cursor.p, 0, 64 * 4, s));
+  RUN(launch_depth_scatter(v, t->depth_off.as<uint32_t>(), t->depth_cursor.as<uint32_t>(),
+                           t->depth_lists.as<uint32_t>(), s));
+  mark(t, 3, s);
+
+  // ---- distribute (partition.py:244-271) ----
+  CK(ensure(t->leaf_pts, n * rec));
+  RadixPlan& p = t->plan;
+  int bits = ceil_log2(t->n_leaves);
+  if (bits > 2 * kRadixMaxBits)
+    return fail(LOD_EUNSUPPORTED, "%u leaves exceed the 2-pass distribute limit", t->n_leaves);
+  p.passes = bits == 0 ? 0 : (bits <= kRadixMaxBits ? 1 : 2);
+  p.bits[0] = p.passes == 2 ? bits / 2 : bits;
+  p.bits[1] = p.passes == 2 ? bits - bits / 2 : 0;
+  p.tiles = (uint32_t)((n + kRadixTile - 1) / kRadixTile);
+  if (p.passes) {
+    int maxb = std::max(p.bits[0], p.bits[1]);
+    uint64_t words = (uint64_t)p.tiles << maxb;
+    size_t old = t->status.cap;
+    CK(ensure(t->status, words * 8));
+    if (t->status.cap != old) {  // fresh memory: clear once, epochs keep it valid afterwards
+      CK(cudaMemsetAsync(t->status.p, 0, t->status.cap, s));
+      t->epoch = 1;
+    }
+    if (t->epoch + 4 > 0xFFFF) {
+      CK(cudaMemsetAsync(t->status.p, 0, t->status.cap, s));
+      t->epoch = 1;
+    }
+    CK(ensure(t->digit_base, (size_t)(2 << kRadixMaxBits) * 8 * 2));
+    CK(ensure(t->ticket, 64));
+    if (p.passes == 2) {
+      CK(ensure(t->tmp_rec, n * rec));
+      CK(ensure(t->tmp_leaf, n * 4));
+    }
+    p.status = t->status.as<uint64_t>();
+    p.status_cap = t->status.cap / 8;
+    p.digit_base = t->digit_base.as<uint64_t>();
+    p.tile_ticket = t->ticket.as<uint32_t>();
+    p.tmp_rec = t->tmp_rec.p;
+    p.tmp_leaf = t->tmp_leaf.as<uint32_t>();
+    p.epoch = t->epoch;
+  }
+  v = make_view(t, pts);
+  RUN(launch_distribute(fmt, v, p, t->leaf_pts.p, s));
+  if (p.passes) t->epoch = p.epoch;
+  mark(t, 4, s);
+  if ((r = read_state(t, s))) return r;
+  if ((r = check_errors(t, s))) return r;
+  if (t->host_state->count_b != n) return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
+  for (int a = 0; a < 3; ++a) t->world[a] = t->host_state->lo[a];
+  t->world[3] = t->host_state->size;
+  CK(cudaGetLastError());
+  t->split_done = true;
+  return LOD_OK;
+}
+
+int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "lod_voxelize before a successful lod_split");
+  if (mode != LOD_MODE_RANDOM && mode != LOD_MODE_AVERAGE)
+    return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
+  CK(cudaSetDevice(t->device));
+  t->voxel_mode = -1;
+  t->n_voxels = 0;
+  uint32_t inner_total = 0, widest = 0;
+  for (int d = 0; d <= kMaxDepth; ++d) inner_total += t->inner_per_depth[d], widest = std::max(widest, t->inner_per_depth[d]);
+  mark(t, 4, s);
+  if (inner_total == 0) {  // single-leaf root: nothing to voxelize (test_sampling.py:163-166)
+    t->voxel_mode = mode;
+    mark(t, 5, s);
+    return LOD_OK;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
+  const int n_clusters = (int)std::max<uint32_t>(1, std::min<uint32_t>(widest, (uint32_t)(sms / 2)));
+  const uint64_t slot_words = 2ull << 21;  // 2 u64 accumulators x up to 128^3 voxels
+  CK(ensure(t->scratch, (size_t)n_clusters * slot_words * 8));
+  uint64_t cap = std::max<uint64_t>(t->n + t->n / 2, 1ull << 21);
+  if (t->vox.cap / 8 > cap) cap = t->vox.cap / 8;
+  for (int attempt = 0; attempt < 6; ++attempt) {
+    CK(ensure(t->vox, cap * 8));
+    cap = t->vox.cap / 8;
+    CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
+                       sizeof(DevState) - offsetof(DevState, err), s));
+    VoxView vv{};
+    vv.st = t->state.as<DevState>();
+    vv.fmt = t->fmt;
+    vv.leaf_pts = t->leaf_pts.p;
+    vv.n_cell = t->n_cell.as<uint64_t>();
+    vv.n_child = t->n_child.as<int32_t>();
+    vv.n_box = t->n_box.as<double4>();
+    vv.n_leaf = t->n_leaf.as<int32_t>();
+    vv.n_first = t->n_first.as<uint64_t>();
+    vv.n_count = t->n_count.as<uint32_t>();
+    vv.vox = t->vox.as<uint2>();
+    vv.vox_cap = cap;
+    vv.scratch = t->scratch.as<uint64_t>();
+    vv.scratch_per_slot = slot_words;
+    vv.mode = mode;
+    vv.seed = seed;
+    for (int d = kMaxDepth; d >= 0; --d) {  // deepest first (sampling.py:171)
+      if (!t->inner_per_depth[d]) continue;
+      vv.depth = d;
+      vv.list = t->depth_lists.as<uint32_t>() + t->inner_off[d];
+      vv.list_n = t->inner_per_depth[d];
+      int nc = (int)std::min<uint32_t>(vv.list_n, (uint32_t)n_clusters);
+      RUN(launch_voxelize_level(vv, nc, s));
+    }
+    int r = read_state(t, s);
+    if (r) return r;
+    CK(cudaGetLastError());
+    if ((t->host_state->err & ERR_ARENA) && !(t->host_state->err & ERR_RANDOM_LIMIT)) {
+      cap = std::max<uint64_t>(cap * 2, t->host_state->vox_cursor + (t->host_state->vox_cursor >> 2));
+      continue;
+    }
+    if ((r = check_errors(t, s))) return r;
+    t->n_voxels = t->host_state->vox_cursor;
+    t->voxel_mode = mode;
+    mark(t, 5, s);
+    return LOD_OK;
+  }
+  return fail(LOD_ECUDA, "voxel arena could not be sized");
+}
+
+}  // namespace
+
+extern "C" {
+
+lod_tree* lod_tree_create(int device) {
+  lod_tree* t = new lod_tree();
+  t->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaMallocHost(&t->host_state, sizeof(DevState)) != cudaSuccess) {
+    fail(LOD_ECUDA, "cannot initialise CUDA device %d", device);
+    delete t;
+    return nullptr;
+  }
+  for (auto& e : t->ev) cudaEventCreate(&e);
+  return t;
+}
+
+void lod_tree_destroy(lod_tree* t) {
+  if (!t) return;
+  cudaSetDevice(t->device);
+  DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan, &t->slots,
+                   &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid, &t->n_lvl,
+                   &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node, &t->leaf_first,
+                   &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
+                   &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf};
+  for (DevBuf* b : all)
+    if (b->p) cudaFree(b->p);
+  for (auto& e : t->ev)
+    if (e) cudaEventDestroy(e);
+  if (t->host_state) cudaFreeHost(t->host_state);
+  delete t;
+}
+
+int lod_split(lod_tree* t, const void* d_points, uint64_t n, int format, const double* bounds_or_null,
+              const lod_config* config, void* stream) {
+  return do_split(t, d_points, n, format, bounds_or_null, config, (cudaStream_t)stream);
+}
+
+int lod_voxelize(lod_tree* t, int mode, uint64_t seed, void* stream) {
+  return do_voxelize(t, mode, seed, (cudaStream_t)stream);
+}
+
+int lod_build(lod_tree* t, const void* d_points, uint64_t n, int format, const lod_config* config, int mode,
+              uint64_t seed, void* stream) {
+  if (mode != LOD_MODE_RANDOM && mode != LOD_MODE_AVERAGE)
+    return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
+  int r = do_split(t, d_points, n, format, nullptr, config, (cudaStream_t)stream);
+  if (r) return r;
+  return do_voxelize(t, mode, seed, (cudaStream_t)stream);
+}
+
+int lod_tree_get_info(const lod_tree* t, lod_tree_info* o) {
+  if (!t || !o) return fail(LOD_EVALUE, "null argument");
+  memset(o, 0, sizeof(*o));
+  o->n_points = t->n;
+  o->n_voxels = t->n_voxels;
+  o->n_nodes = t->n_nodes;
+  o->n_leaves = t->n_leaves;
+  o->n_inner = t->n_nodes - t->n_leaves;
+  o->depth = t->max_depth_used;
+  o->point_format = t->fmt;
+  o->voxel_mode = t->voxel_mode;
+  for (int a = 0; a < 3; ++a) o->world_min[a] = t->world[a];
+  o->world_size = t->world[3];
+  o->n_ext_grids = t->n_ext;
+  o->radix_passes = (uint32_t)t->plan.passes;
+  return LOD_OK;
+}
+
+int lod_tree_copy_nodes(const lod_tree* tc, lod_node* host, void* stream) {
+  lod_tree* t = const_cast<lod_tree*>(tc);
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(t->device));
+  CK(ensure(t->export_buf, (size_t)t->n_nodes * sizeof(lod_node)));
+  SplitView v = make_view(t, nullptr);
+  launch_export_nodes(v, t->export_buf.as<lod_node>(), s);
+  CK(cudaMemcpyAsync(host, t->export_buf.p, (size_t)t->n_nodes * sizeof(lod_node), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return LOD_OK;
+}
+
+int lod_tree_leaf_points(const lod_tree* t, const void** p) {
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
+  *p = t->leaf_pts.p;
+  return LOD_OK;
+}
+
+int lod_tree_voxels(const lod_tree* t, const void** p) {
+  if (!t || t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
+  *p = t->vox.p;
+  return LOD_OK;
+}
+
+int lod_tree_copy_leaf_points(const lod_tree* t, void* host, void* stream) {
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
+  size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
+  CK(cudaSetDevice(t->device));
+  CK(cudaMemcpyAsync(host, t->leaf_pts.p, t->n * rec, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return LOD_OK;
+}
+
+int lod_tree_copy_voxels(const lod_tree* t, void* host, void* stream) {
+  if (!t || t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
+  CK(cudaSetDevice(t->device));
+  if (t->n_voxels)
+    CK(cudaMemcpyAsync(host, t->vox.p, t->n_voxels * 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return LOD_OK;
+}
+
+uint64_t lod_tree_device_bytes(const lod_tree* t) {
+  if (!t) return 0;
+  const DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan,
+                         &t->slots, &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid,
+                         &t->n_lvl, &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node,
+                         &t->leaf_first, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists,
+                         &t->leaf_pts, &t->status, &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf,
+                         &t->vox, &t->scratch, &t->export_buf};
+  uint64_t b = 0;
+  for (const DevBuf* x : all) b += x->cap;
+  return b;
+}
+
+int lod_set_timing(lod_tree* t, int enabled) {
+  if (!t) return fail(LOD_EVALUE, "null tree");
+  t->timing = enabled != 0;
+  return LOD_OK;
+}
+
+int lod_tree_stage_ms(const lod_tree* tc, float* out) {
+  lod_tree* t = const_cast<lod_tree*>(tc);
+  if (!t || !t->timing) return fail(LOD_EVALUE, "timing not enabled");
+  for (int i = 0; i < 5; ++i) {
+    out[i] = 0;
+    if (cudaEventElapsedTime(&out[i], t->ev[i], t->ev[i + 1]) != cudaSuccess) out[i] = -1;
+  }
+  cudaGetLastError();
+  return LOD_OK;
+}
+
+uint64_t lod_tree_launches(const lod_tree* t) { return t ? t->launches : 0; }
+
+int lod_generate(const char* kind, uint64_t seed, uint64_t start, uint64_t n, void* d_out, const double* table,
+                 void* stream) {
+  static const char* kinds[] = {"sphere", "terrain", "scene", "cluster", "surface"};
+  int k = -1;
+  for (int i = 0; i < 5; ++i)
+    if (kind && strcmp(kind, kinds[i]) == 0) k = i;
+  if (k < 0) return fail(LOD_EVALUE, "unknown synthetic kind: %s", kind ? kind : "(null)");
+  if (k == 2 && !table) return fail(LOD_EVALUE, "scene generator needs the object table");
+  launch_generate(k, seed, start, n, d_out, table, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return LOD_OK;
+}
+
+const char* lod_last_error(void) { return g_err.c_str(); }
+
+const char* lod_version(void) { return "lodb200 0.1.0 sm_100a"; }
+
+}  // extern "C"

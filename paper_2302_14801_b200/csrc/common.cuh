@@ -1,0 +1,199 @@
+// Shared device helpers for the LOD-construction path (sm_100a).
+//
+// Point records (device layout, one per input point):
+//   LOD_POINTS_F32: 16 B {f32 x, y, z; u8 r, g, b, pad}   -- the north-star record,
+//                   one 128-bit load per point
+//   LOD_POINTS_F64: 32 B {f64 x, y, z; u8 r, g, b, pad[5]} -- exact path for clouds whose
+//                   coordinates are not float32-representable (reference PointCloud is f64)
+//
+// Geometry is the reference's fp64 projection (model.py:84-98, partition.py:130-135):
+//   q = RN(RN(p - lo) / size);  cell_L = min(floor(q * 2^L), 2^L - 1)
+// Because q * 2^L is exact, every level's cell is a right shift of the depth-16 cell
+// c16 = min(floor(q * 65536), 65535), so each point is projected once per pass.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/lodb200.h"
+
+namespace lod {
+
+constexpr uint32_t UNMERGEABLE = 0xFFFFFFFFu;  // partition.py:20
+constexpr int kGrid = 128;                      // model.py:18
+constexpr int kMaxDepth = 16;                   // model.py:19
+constexpr int kRandomLimit = 1 << 20;           // sampling.py:18
+
+// device error bits (first error wins the detail fields)
+enum : uint32_t {
+  ERR_NONFINITE = 1u << 0,     // model.py:204-205 -> ValueError
+  ERR_OUTSIDE = 1u << 1,       // model.py:94-95 -> ConsistencyError
+  ERR_EXT_ROOT = 1u << 2,      // partition.py:169-170
+  ERR_OVERSIZED = 1u << 3,     // partition.py:223-224
+  ERR_NO_PARENT = 1u << 4,     // partition.py:238-239
+  ERR_UNRESOLVED = 1u << 5,    // partition.py:259-260, 285-286
+  ERR_RANDOM_LIMIT = 1u << 6,  // sampling.py:73-75
+  ERR_ARENA = 1u << 7,         // internal: voxel arena too small, host grows and re-runs
+  ERR_EMPTY_CHILD = 1u << 8,   // sampling.py:34-35
+  ERR_COUNT = 1u << 9,         // partition.py:268-269
+  ERR_NO_ROOT = 1u << 10,      // partition.py:189-191
+};
+
+// Device-resident scalars of one build; read back with a single small D2H copy.
+struct DevState {
+  unsigned long long lo_key[3];   // order-preserving encodings of per-axis min / max
+  unsigned long long hi_key[3];
+  double lo[3];                   // world cube (model.py:199-209 or caller bounds)
+  double size;
+  uint32_t err;
+  uint32_t err_detail;            // node id for voxelize errors
+  unsigned long long err_value;   // e.g. the sample count of the 2^20 violation
+  uint64_t count_a;               // compaction outputs
+  uint64_t count_b;
+  unsigned long long vox_cursor;  // voxel arena bump pointer
+  uint32_t work[kMaxDepth + 1];   // per-depth node tickets for the voxelizer
+  uint32_t pad;
+};
+
+__device__ __forceinline__ void raise_err(DevState* st, uint32_t bit, uint32_t detail = 0,
+                                          unsigned long long value = 0) {
+  uint32_t old = atomicOr(&st->err, bit);
+  if (old == 0) {
+    st->err_detail = detail;
+    st->err_value = value;
+  }
+}
+
+// order-preserving u64 key of a double (for atomicMin / atomicMax)
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dunkey(unsigned long long k) {
+  unsigned long long u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+// ---------------------------------------------------------------------------
+// point records
+// ---------------------------------------------------------------------------
+template <int FMT>
+struct Rec;
+
+template <>
+struct Rec<LOD_POINTS_F32> {
+  static constexpr int kVec = 1;  // 16-byte words per record
+  struct Raw { uint4 a; };
+  __device__ __forceinline__ static Raw load(const void* base, uint64_t i) {
+    return Raw{__ldg(reinterpret_cast<const uint4*>(base) + i)};
+  }
+  __device__ __forceinline__ static Raw load_cg(const void* base, uint64_t i) {
+    return Raw{__ldcg(reinterpret_cast<const uint4*>(base) + i)};
+  }
+  __device__ __forceinline__ static void store(void* base, uint64_t i, const Raw& r) {
+    reinterpret_cast<uint4*>(base)[i] = r.a;
+  }
+  __device__ __forceinline__ static double x(const Raw& r) { return (double)__uint_as_float(r.a.x); }
+  __device__ __forceinline__ static double y(const Raw& r) { return (double)__uint_as_float(r.a.y); }
+  __device__ __forceinline__ static double z(const Raw& r) { return (double)__uint_as_float(r.a.z); }
+  __device__ __forceinline__ static uint32_t rgb(const Raw& r) { return r.a.w & 0xFFFFFFu; }
+};
+
+template <>
+struct Rec<LOD_POINTS_F64> {
+  static constexpr int kVec = 2;
+  struct Raw { uint4 a, b; };
+  __device__ __forceinline__ static Raw load(const void* base, uint64_t i) {
+    const uint4* p = reinterpret_cast<const uint4*>(base) + 2 * i;
+    return Raw{__ldg(p), __ldg(p + 1)};
+  }
+  __device__ __forceinline__ static Raw load_cg(const void* base, uint64_t i) {
+    const uint4* p = reinterpret_cast<const uint4*>(base) + 2 * i;
+    return Raw{__ldcg(p), __ldcg(p + 1)};
+  }
+  __device__ __forceinline__ static void store(void* base, uint64_t i, const Raw& r) {
+    uint4* p = reinterpret_cast<uint4*>(base) + 2 * i;
+    p[0] = r.a;
+    p[1] = r.b;
+  }
+  __device__ __forceinline__ static double x(const Raw& r) {
+    return __hiloint2double((int)r.a.y, (int)r.a.x);
+  }
+  __device__ __forceinline__ static double y(const Raw& r) {
+    return __hiloint2double((int)r.a.w, (int)r.a.z);
+  }
+  __device__ __forceinline__ static double z(const Raw& r) {
+    return __hiloint2double((int)r.b.y, (int)r.b.x);
+  }
+  __device__ __forceinline__ static uint32_t rgb(const Raw& r) { return r.b.z & 0xFFFFFFu; }
+};
+
+// ---------------------------------------------------------------------------
+// projection (reference model.py:84-98; hazard H1: correctly rounded fp64)
+// ---------------------------------------------------------------------------
+
+// One axis of the depth-16 cell; sets *bad if p lies outside [lo, lo + size].
+__device__ __forceinline__ uint32_t quant16(double p, double lo, double size, bool& bad) {
+  double rel = __dsub_rn(p, lo);
+  bad |= !(rel >= 0.0) || (rel > size);
+  double q = __ddiv_rn(rel, size);
+  double f = floor(__dmul_rn(q, 65536.0));
+  f = fmin(fmax(f, 0.0), 65535.0);
+  return (uint32_t)f;
+}
+
+struct Cell16 {
+  uint32_t x, y, z;
+};
+
+template <int FMT>
+__device__ __forceinline__ Cell16 cell16(const typename Rec<FMT>::Raw& r, const DevState& st, bool& bad) {
+  Cell16 c;
+  c.x = quant16(Rec<FMT>::x(r), st.lo[0], st.size, bad);
+  c.y = quant16(Rec<FMT>::y(r), st.lo[1], st.size, bad);
+  c.z = quant16(Rec<FMT>::z(r), st.lo[2], st.size, bad);
+  return c;
+}
+
+// linear x-major key of the cell at `depth` (partition.py:23-24)
+__device__ __forceinline__ uint64_t level_key(const Cell16& c, int depth) {
+  int s = kMaxDepth - depth;
+  return ((uint64_t)(c.x >> s) << (2 * depth)) | ((uint64_t)(c.y >> s) << depth) | (uint64_t)(c.z >> s);
+}
+
+// first cell index of pyramid level l inside a pyramid buffer: (8^l - 1) / 7
+__host__ __device__ __forceinline__ uint64_t level_off(int l) { return ((1ull << (3 * l)) - 1) / 7; }
+
+// ---------------------------------------------------------------------------
+// extension pyramids (partition.py:64-76)
+// ---------------------------------------------------------------------------
+struct ExtMeta {
+  uint64_t pyr_off;      // first slot of this pyramid in the unified pyramid buffer
+  uint64_t tgt_off;      // first entry of its finest-level target table
+  uint64_t anchor_slot;  // slot of the anchor cell (main finest level or parent ext finest level)
+  uint16_t ax, ay, az;   // anchor cell, absolute coordinates at depth `base`
+  uint8_t base;          // depth of the anchor cell
+  uint8_t ext;           // levels below the anchor (finest grid 2^ext per axis)
+};
+
+// Packed node cell: x | y << 16 | z << 32 | depth << 48 | flags << 56
+enum : uint32_t { NODE_LEAF = 1u, NODE_OVERSIZED = 2u };
+__device__ __forceinline__ uint64_t pack_cell(uint32_t x, uint32_t y, uint32_t z, uint32_t depth,
+                                              uint32_t flags) {
+  return (uint64_t)x | ((uint64_t)y << 16) | ((uint64_t)z << 32) | ((uint64_t)depth << 48) |
+         ((uint64_t)flags << 56);
+}
+
+__host__ __device__ __forceinline__ uint32_t ceil_div_u32(uint64_t a, uint64_t b) {
+  return (uint32_t)((a + b - 1) / b);
+}
+
+#define LOD_CUDA_CHECK(expr)                                  \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return ::lod::fail_cuda(_e, #expr); \
+  } while (0)
+
+int fail_cuda(cudaError_t e, const char* what);
+int fail(int code, const char* fmt, ...);
+
+}  // namespace lod

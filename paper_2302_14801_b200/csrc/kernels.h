@@ -1,0 +1,151 @@
+// Host-callable launch wrappers of the split / distribute / voxelize kernels.
+// Every wrapper enqueues on `st` and returns the number of kernels it launched.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace lod {
+
+// Unified device view of a tree's split state, passed by value to kernels.
+struct SplitView {
+  DevState* st;
+  const void* pts;        // input records
+  uint64_t n;
+  int D;                  // initial_depth
+  int max_depth;
+  uint32_t T;
+  uint32_t* pyr;          // unified pyramid buffer: main pyramid at 0, ext pyramids after
+  uint64_t main_cells;    // cells of the main pyramid = level_off(D + 1)
+  int32_t* node_idx;      // slot -> node id (valid at non-zero slots)
+  int32_t* t8;            // main finest level: leaf id, -(ext+2), or -1
+  int32_t* te;            // ext finest levels: same encoding
+  ExtMeta* meta;
+  uint32_t n_ext;
+  // node table
+  uint64_t* n_cell;
+  uint32_t* n_val;
+  int32_t* n_parent;
+  int32_t* n_child;       // 8 per node
+  uint64_t* n_slot;
+  int32_t* n_extid;      // owning extension or -1
+  uint8_t* n_lvl;
+  int32_t* n_leaf;        // leaf index or -1
+  double4* n_box;         // min xyz, size
+  uint64_t* n_first;      // leaf: first point; inner: first voxel
+  uint32_t* n_count;      // leaf: points; inner: voxels
+  uint32_t n_nodes;
+  uint32_t* leaf_node;
+  uint64_t* leaf_first;
+  uint32_t n_leaves;
+};
+
+// Descend the extension chain of a point; returns the finest-cell index inside extension
+// `e_out` (the deepest one containing the point), or false if the point is in none.
+__device__ __forceinline__ bool ext_descend(const SplitView& v, const Cell16& c, uint32_t& e_out, uint32_t& r_out,
+                                            int32_t t) {
+  if (t > -2) return false;
+  uint32_t e = (uint32_t)(-(t + 2));
+  while (true) {
+    const ExtMeta m = v.meta[e];
+    int s = kMaxDepth - (m.base + m.ext);
+    uint32_t rx = (c.x >> s) - ((uint32_t)m.ax << m.ext);
+    uint32_t ry = (c.y >> s) - ((uint32_t)m.ay << m.ext);
+    uint32_t rz = (c.z >> s) - ((uint32_t)m.az << m.ext);
+    uint32_t r = (rx << (2 * m.ext)) | (ry << m.ext) | rz;
+    int32_t nt = v.te[m.tgt_off + r];
+    if (nt > -2) {
+      e_out = e;
+      r_out = r;
+      return true;
+    }
+    e = (uint32_t)(-(nt + 2));
+  }
+}
+
+
+// Leaf id of a point: main finest-cell target, then down the extension chain
+// (partition.py:244-287 insert / _resolve_extended).  -1 if unresolved.
+__device__ __forceinline__ int32_t leaf_of_point(const SplitView& v, const Cell16& c) {
+  int32_t t = v.t8[level_key(c, v.D)];
+  uint32_t e, r;
+  if (ext_descend(v, c, e, r, t)) t = v.te[v.meta[e].tgt_off + r];
+  return t;
+}
+
+// --- split (split_kernels.cu) ---
+int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const double* user_bounds,
+                  cudaStream_t s);
+int launch_count(int fmt, const SplitView& v, cudaStream_t s);
+int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s);
+int launch_find_subanchors(const SplitView& v, uint32_t first_ext, uint32_t n_ext_round, int ext_levels,
+                           uint64_t* list, ScanScratch& scr, cudaStream_t s);
+int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_t count,
+                      const uint64_t* list, uint32_t parent_first, uint64_t pyr_base, uint64_t tgt_base,
+                      int base_depth, int ext_levels, cudaStream_t s);
+int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first_ext, cudaStream_t s);
+int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint32_t* round_count,
+                     const int* round_ext, const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s);
+int launch_count_nodes(const SplitView& v, uint64_t total_slots, uint64_t* slots_out, ScanScratch& scr,
+                       cudaStream_t s);
+int launch_build_nodes(const SplitView& v, const uint64_t* slots, cudaStream_t s);
+int launch_number_leaves(const SplitView& v, ScanScratch& scr, cudaStream_t s);
+int launch_leaf_offsets(const SplitView& v, ScanScratch& scr, cudaStream_t s);
+int launch_targets(const SplitView& v, cudaStream_t s);
+int launch_targets_ext(const SplitView& v, uint32_t first, uint32_t count, int ext, cudaStream_t s);
+int launch_depth_lists(const SplitView& v, uint32_t* depth_count, cudaStream_t s);
+int launch_depth_scatter(const SplitView& v, const uint32_t* depth_off, uint32_t* depth_cursor,
+                         uint32_t* lists, cudaStream_t s);
+int launch_export_nodes(const SplitView& v, lod_node* out, cudaStream_t s);
+
+// --- distribute (distribute.cu) ---
+struct RadixPlan {
+  int passes;             // 0 = single leaf (plain copy)
+  int bits[2];            // digit widths
+  uint32_t tiles;
+  uint64_t* status;       // look-back words, tiles * 2^bits[p] per pass (epoch-tagged)
+  uint64_t status_cap;
+  uint32_t epoch;
+  uint64_t* digit_base;   // per pass: 2^bits global exclusive prefix
+  uint32_t* tile_ticket;  // per pass
+  void* tmp_rec;          // pass-0 output records (2 passes)
+  uint32_t* tmp_leaf;     // pass-0 output leaf ids
+};
+constexpr int kRadixThreads = 512;
+constexpr int kRadixItems = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;
+constexpr int kRadixMaxBits = 11;
+int launch_distribute(int fmt, const SplitView& v, RadixPlan& plan, void* leaf_out, cudaStream_t s);
+
+// --- voxelize (voxelize.cu) ---
+struct VoxView {
+  DevState* st;
+  int fmt;
+  const void* leaf_pts;
+  const uint64_t* n_cell;
+  const int32_t* n_child;
+  const double4* n_box;
+  const int32_t* n_leaf;
+  uint64_t* n_first;
+  uint32_t* n_count;
+  const uint32_t* list;   // inner nodes of this depth
+  uint32_t list_n;
+  uint32_t depth;
+  uint2* vox;             // arena
+  uint64_t vox_cap;
+  uint64_t* scratch;      // per-cluster accumulator slots
+  uint64_t scratch_per_slot;  // u64 words per cluster slot
+  int mode;
+  uint64_t seed;
+};
+int voxelize_smem_bytes();
+int launch_voxelize_level(const VoxView& v, int n_clusters, cudaStream_t s);
+
+// --- generators (generate.cu) ---
+int launch_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, void* out, const double* table,
+                    cudaStream_t s);
+
+}  // namespace lod

@@ -1,0 +1,111 @@
+// Device-wide exclusive scan / order-preserving compaction over a functor domain.
+//
+// Three launches (block sums -> one-block scan of the sums -> per-block rescan + store).
+// Used for the small, structural passes of the split (anchors, node enumeration, leaf
+// numbering, leaf offsets); the per-point passes never go through here.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lod {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive prefix and
+// writes the block total to *total (all threads).
+template <typename T, int NT>
+__device__ __forceinline__ T block_excl_scan(T v, T* total, T* smem /* >= NT/32 + 1 */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T incl = warp_incl_scan(v);
+  if (lane == 31) smem[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    T w = (lane < NT / 32) ? smem[lane] : T(0);
+    T wi = warp_incl_scan(w);
+    if (lane < NT / 32) smem[lane] = wi - w;
+    if (lane == NT / 32 - 1) smem[NT / 32] = wi;
+  }
+  __syncthreads();
+  T out = smem[warp] + incl - v;
+  *total = smem[NT / 32];
+  __syncthreads();
+  return out;
+}
+
+template <class F>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(uint64_t n, F f, uint64_t* block_sums) {
+  __shared__ uint64_t sm[kScanThreads / 32 + 1];
+  uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  uint64_t s = 0;
+#pragma unroll 4
+  for (int k = 0; k < kScanItems; ++k) {
+    uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+    if (i < n) s += f.value(i);
+  }
+  uint64_t tot;
+  block_excl_scan<uint64_t, kScanThreads>(s, &tot, sm);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+// Exclusive scan of block sums in one block; adds *base_in (if any) and writes the grand
+// total (+ base) to *total_out.
+__global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* sums, uint32_t nb, const uint64_t* base_in,
+                                                    uint64_t* total_out);
+
+template <class F>
+__global__ void __launch_bounds__(kScanThreads) k_scan_store(uint64_t n, F f, const uint64_t* block_sums) {
+  __shared__ uint64_t sm[kScanThreads / 32 + 1];
+  // items owned by a thread are contiguous so one sequential pass keeps the order
+  uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint64_t v[kScanItems];
+  uint64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    uint64_t i = base + k;
+    v[k] = (i < n) ? f.value(i) : 0;
+    s += v[k];
+  }
+  uint64_t tot;
+  uint64_t pre = block_excl_scan<uint64_t, kScanThreads>(s, &tot, sm) + block_sums[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    uint64_t i = base + k;
+    if (i < n) f.store(i, pre, v[k]);
+    pre += v[k];
+  }
+}
+
+struct ScanScratch {
+  uint64_t* sums = nullptr;
+  uint64_t cap = 0;
+};
+
+// Runs the scan of f over [0, n). f.value(i) -> u64 item, f.store(i, excl, item).
+// base_in (device, may be null) is added to every prefix; *total_out (device) receives
+// base + sum.  Returns the number of launches.
+template <class F>
+int device_scan(uint64_t n, F f, ScanScratch& scr, const uint64_t* base_in, uint64_t* total_out,
+                cudaStream_t st) {
+  uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
+  if (nb == 0) nb = 1;
+  if (scr.cap < nb + 1) return -1;
+  k_scan_reduce<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
+  k_scan_sums<<<1, 1024, 0, st>>>(scr.sums, nb, base_in, total_out);
+  k_scan_store<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
+  return 3;
+}
+
+}  // namespace lod

@@ -1,0 +1,645 @@
+// Split stage: hierarchical counting sort into octree leaves (reference partition.py).
+//
+//   K1 k_bounds / k_bounds_finalize   world cube            model.py:199-209
+//   K2 k_count                        256^3 counting grid   partition.py:99-105
+//   K3 k_ext_create / k_ext_count     extension pyramids    partition.py:109-151
+//   K4 k_mark_anchors / k_merge       2x2x2 merge pyramid   partition.py:36-61, 155-170
+//   K5 k_build_nodes / k_link / ...   node table + targets  partition.py:174-240
+//
+// Layout in HBM: every counting pyramid (the main one, then one per extension grid) lives
+// in ONE u32 buffer; a pyramid of L levels stores level l at offset (8^l - 1) / 7, x-major
+// within a level.  A node is a non-zero cell ("slot") of that buffer, so node enumeration
+// is one order-preserving compaction over the buffer.
+#include <cooperative_groups.h>
+
+#include "kernels.h"
+
+namespace lod {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int ceil_log2_u64(uint64_t x) { return x <= 1 ? 0 : 64 - __clzll(x - 1); }
+
+// ---------------------------------------------------------------------------
+// K1: bounds
+// ---------------------------------------------------------------------------
+template <int FMT>
+__global__ void __launch_bounds__(kThreads) k_bounds(const void* pts, uint64_t n, DevState* st) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  bool bad = false;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    auto r = Rec<FMT>::load(pts, i);
+    double p[3] = {Rec<FMT>::x(r), Rec<FMT>::y(r), Rec<FMT>::z(r)};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      bad |= !isfinite(p[a]);
+      lo[a] = fmin(lo[a], p[a]);
+      hi[a] = fmax(hi[a], p[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xFFFFFFFFu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xFFFFFFFFu, hi[a], o));
+    }
+  }
+  __shared__ double s_lo[kThreads / 32][3], s_hi[kThreads / 32][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int a = 0; a < 3; ++a) s_lo[warp][a] = lo[a], s_hi[warp][a] = hi[a];
+  if (__syncthreads_or(bad) && threadIdx.x == 0) raise_err(st, ERR_NONFINITE);
+  if (threadIdx.x < 3) {
+    int a = threadIdx.x;
+    double l = s_lo[0][a], h = s_hi[0][a];
+    for (int w = 1; w < kThreads / 32; ++w) l = fmin(l, s_lo[w][a]), h = fmax(h, s_hi[w][a]);
+    atomicMin(&st->lo_key[a], dkey(l));
+    atomicMax(&st->hi_key[a], dkey(h));
+  }
+}
+
+// size = max_axis(max - min), 1.0 when degenerate (model.py:206-209)
+__global__ void k_bounds_finalize(DevState* st, int user, double ux, double uy, double uz, double us) {
+  if (threadIdx.x != 0) return;
+  if (user) {
+    st->lo[0] = ux, st->lo[1] = uy, st->lo[2] = uz, st->size = us;
+    return;
+  }
+  double ext = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    double l = dunkey(st->lo_key[a]), h = dunkey(st->hi_key[a]);
+    st->lo[a] = l;
+    ext = fmax(ext, __dsub_rn(h, l));
+  }
+  st->size = ext > 0.0 ? ext : 1.0;
+}
+
+int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const double* ub, cudaStream_t s) {
+  if (ub) {
+    k_bounds_finalize<<<1, 32, 0, s>>>(st, 1, ub[0], ub[1], ub[2], ub[3]);
+    return 1;
+  }
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, 148ull * 8);
+  if (fmt == LOD_POINTS_F32)
+    k_bounds<LOD_POINTS_F32><<<blocks, kThreads, 0, s>>>(pts, n, st);
+  else
+    k_bounds<LOD_POINTS_F64><<<blocks, kThreads, 0, s>>>(pts, n, st);
+  k_bounds_finalize<<<1, 32, 0, s>>>(st, 0, 0, 0, 0, 0);
+  return 2;
+}
+
+// ---------------------------------------------------------------------------
+// K2: count into the main finest grid, warp-aggregated atomics
+// ---------------------------------------------------------------------------
+constexpr int kCountUnroll = 4;
+
+template <int FMT>
+__global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
+  const DevState st = *v.st;
+  uint32_t* grid = v.pyr + level_off(v.D);
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < v.n; base += stride * kCountUnroll) {
+    typename Rec<FMT>::Raw r[kCountUnroll];
+#pragma unroll
+    for (int u = 0; u < kCountUnroll; ++u) {
+      uint64_t i = base + u * stride + threadIdx.x;
+      if (i < v.n) r[u] = Rec<FMT>::load(v.pts, i);
+    }
+#pragma unroll
+    for (int u = 0; u < kCountUnroll; ++u) {
+      uint64_t i = base + u * stride + threadIdx.x;
+      bool valid = i < v.n;
+      uint32_t key = 0;
+      if (valid) key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
+      unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
+      if (valid) {
+        unsigned peers = __match_any_sync(act, key);
+        if (lane == __ffs(peers) - 1) atomicAdd(grid + key, (uint32_t)__popc(peers));
+      }
+    }
+  }
+  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) raise_err(v.st, ERR_OUTSIDE);
+}
+
+int launch_count(int fmt, const SplitView& v, cudaStream_t s) {
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
+  if (fmt == LOD_POINTS_F32)
+    k_count<LOD_POINTS_F32><<<blocks, kThreads, 0, s>>>(v);
+  else
+    k_count<LOD_POINTS_F64><<<blocks, kThreads, 0, s>>>(v);
+  return 1;
+}
+
+// ---------------------------------------------------------------------------
+// K3: extension pyramids (partition.py:109-151)
+// ---------------------------------------------------------------------------
+struct AnchorF {  // main finest cells with count > T (partition.py:111)
+  const uint32_t* grid;
+  uint32_t T;
+  uint64_t* out;
+  __device__ uint64_t value(uint64_t i) const { return grid[i] > T ? 1 : 0; }
+  __device__ void store(uint64_t i, uint64_t ex, uint64_t v) const {
+    if (v) out[ex] = i;
+  }
+};
+
+int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s) {
+  AnchorF f{v.pyr + level_off(v.D), v.T, list};
+  return device_scan(1ull << (3 * v.D), f, scr, nullptr, &v.st->count_a, s);
+}
+
+struct SubAnchorF {  // extension finest cells with count > T (partition.py:140-143)
+  const uint32_t* pyr;
+  const ExtMeta* meta;
+  uint32_t first;
+  int ext;
+  uint32_t T;
+  uint64_t* out;
+  __device__ uint64_t value(uint64_t i) const {
+    uint64_t cells = 1ull << (3 * ext);
+    const ExtMeta& m = meta[first + i / cells];
+    return pyr[m.pyr_off + level_off(ext) + i % cells] > T ? 1 : 0;
+  }
+  __device__ void store(uint64_t i, uint64_t ex, uint64_t v) const {
+    if (v) out[ex] = i;
+  }
+};
+
+int launch_find_subanchors(const SplitView& v, uint32_t first_ext, uint32_t n_ext_round, int ext_levels,
+                           uint64_t* list, ScanScratch& scr, cudaStream_t s) {
+  SubAnchorF f{v.pyr, v.meta, first_ext, ext_levels, v.T, list};
+  return device_scan((uint64_t)n_ext_round << (3 * ext_levels), f, scr, nullptr, &v.st->count_a, s);
+}
+
+__global__ void k_ext_create(SplitView v, int round, uint32_t first, uint32_t count, const uint64_t* list,
+                             uint32_t parent_first, uint64_t pyr_base, uint64_t tgt_base, int base_depth,
+                             int ext) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint32_t e = first + i;
+  ExtMeta m;
+  m.pyr_off = pyr_base + (uint64_t)i * level_off(ext + 1);
+  m.tgt_off = tgt_base + ((uint64_t)i << (3 * ext));
+  m.base = (uint8_t)base_depth;
+  m.ext = (uint8_t)ext;
+  uint64_t key = list[i];
+  if (round == 0) {  // anchor = main finest cell `key`
+    int D = v.D;
+    uint32_t msk = (1u << D) - 1;
+    m.ax = (uint16_t)(key >> (2 * D));
+    m.ay = (uint16_t)((key >> D) & msk);
+    m.az = (uint16_t)(key & msk);
+    m.anchor_slot = level_off(D) + key;
+    v.t8[key] = -(int32_t)(e + 2);
+  } else {  // anchor = finest cell r of parent extension pyramid
+    const ExtMeta& p = v.meta[parent_first];
+    int pe = p.ext;
+    uint64_t cells = 1ull << (3 * pe);
+    const ExtMeta mp = v.meta[parent_first + key / cells];
+    uint32_t r = (uint32_t)(key % cells), msk = (1u << pe) - 1;
+    m.ax = (uint16_t)(((uint32_t)mp.ax << pe) + (r >> (2 * pe)));
+    m.ay = (uint16_t)(((uint32_t)mp.ay << pe) + ((r >> pe) & msk));
+    m.az = (uint16_t)(((uint32_t)mp.az << pe) + (r & msk));
+    m.anchor_slot = mp.pyr_off + level_off(pe) + r;
+    v.te[mp.tgt_off + r] = -(int32_t)(e + 2);
+  }
+  v.meta[e] = m;
+}
+
+int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_t count, const uint64_t* list,
+                      uint32_t parent_first, uint64_t pyr_base, uint64_t tgt_base, int base_depth,
+                      int ext_levels, cudaStream_t s) {
+  if (!count) return 0;
+  k_ext_create<<<ceil_div_u32(count, kThreads), kThreads, 0, s>>>(v, round, first_ext, count, list, parent_first,
+                                                                   pyr_base, tgt_base, base_depth, ext_levels);
+  return 1;
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(kThreads) k_ext_count(SplitView v, uint32_t round_first) {
+  const DevState st = *v.st;
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < v.n; base += stride) {
+    uint64_t i = base + threadIdx.x;
+    uint64_t slot = ~0ull;
+    if (i < v.n) {
+      auto r = Rec<FMT>::load(v.pts, i);
+      Cell16 c = cell16<FMT>(r, st, bad);
+      int32_t t = v.t8[level_key(c, v.D)];
+      uint32_t e, rr;
+      if (ext_descend(v, c, e, rr, t) && e >= round_first) {
+        const ExtMeta& m = v.meta[e];
+        slot = m.pyr_off + level_off(m.ext) + rr;
+      }
+    }
+    unsigned act = __ballot_sync(0xFFFFFFFFu, slot != ~0ull);
+    if (slot != ~0ull) {
+      unsigned peers = __match_any_sync(act, slot);
+      if (lane == __ffs(peers) - 1) atomicAdd(v.pyr + slot, (uint32_t)__popc(peers));
+    }
+  }
+}
+
+int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStream_t s) {
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
+  if (fmt == LOD_POINTS_F32)
+    k_ext_count<LOD_POINTS_F32><<<blocks, kThreads, 0, s>>>(v, round_first);
+  else
+    k_ext_count<LOD_POINTS_F64><<<blocks, kThreads, 0, s>>>(v, round_first);
+  return 1;
+}
+
+// ---------------------------------------------------------------------------
+// K4: merge (partition.py:36-61 rule; anchors pre-flagged, partition.py:157-159,165-167)
+// ---------------------------------------------------------------------------
+__global__ void k_mark_anchors(SplitView v) {
+  uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < v.n_ext) v.pyr[v.meta[e].anchor_slot] = UNMERGEABLE;
+}
+
+// One parent level `lp` of `n_pyr` equally shaped pyramids starting at `first`, stride `stride`.
+__global__ void __launch_bounds__(kThreads) k_merge(uint32_t* pyr, uint64_t first, uint64_t stride, uint32_t n_pyr,
+                                                     int lp, uint32_t T) {
+  const uint64_t cells = 1ull << (3 * lp);
+  const uint64_t total = cells * n_pyr;
+  const uint32_t dp = 1u << lp, dc = dp << 1, msk = dp - 1;
+  for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t p = idx / cells, c = idx % cells;
+    uint32_t px = (uint32_t)(c >> (2 * lp)), py = (uint32_t)(c >> lp) & msk, pz = (uint32_t)c & msk;
+    uint32_t* base = pyr + first + p * stride;
+    uint32_t* ch = base + level_off(lp + 1);
+    uint64_t sum = 0;
+    bool flag = false;
+    uint64_t at[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t x = 2 * px + (k & 1), y = 2 * py + ((k >> 1) & 1), z = 2 * pz + (k >> 2);
+      at[k] = ((uint64_t)x * dc + y) * dc + z;
+      uint32_t val = ch[at[k]];
+      if (val == UNMERGEABLE)
+        flag = true;
+      else
+        sum += val;
+    }
+    uint32_t parent;
+    if (!flag && sum > 0 && sum < T) {
+      parent = (uint32_t)sum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ch[at[k]] = 0;
+    } else {
+      parent = (flag || sum > 0) ? UNMERGEABLE : 0u;
+    }
+    base[level_off(lp) + c] = parent;
+  }
+}
+
+// Extension roots must come out UNMERGEABLE (partition.py:169-170); the root slot then
+// duplicates the anchor node and is cleared so node enumeration skips it (partition.py:216).
+__global__ void k_ext_roots(SplitView v) {
+  uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= v.n_ext) return;
+  uint64_t s = v.meta[e].pyr_off;
+  if (v.pyr[s] != UNMERGEABLE) raise_err(v.st, ERR_EXT_ROOT, e);
+  v.pyr[s] = 0;
+}
+
+static uint32_t merge_blocks(uint64_t total) {
+  return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + kThreads - 1) / kThreads, 148ull * 16));
+}
+
+int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint32_t* round_count,
+                     const int* round_ext, const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s) {
+  int launches = 0;
+  if (v.n_ext) {
+    k_mark_anchors<<<ceil_div_u32(v.n_ext, kThreads), kThreads, 0, s>>>(v);
+    ++launches;
+  }
+  for (int r = n_rounds - 1; r >= 0; --r) {
+    if (!round_count[r]) continue;
+    int e = round_ext[r];
+    for (int lp = e - 1; lp >= 0; --lp) {
+      k_merge<<<merge_blocks((uint64_t)round_count[r] << (3 * lp)), kThreads, 0, s>>>(
+          v.pyr, round_pyr_base[r], level_off(e + 1), round_count[r], lp, v.T);
+      ++launches;
+    }
+  }
+  if (v.n_ext) {
+    k_ext_roots<<<ceil_div_u32(v.n_ext, kThreads), kThreads, 0, s>>>(v);
+    ++launches;
+  }
+  for (int lp = v.D - 1; lp >= 0; --lp) {
+    k_merge<<<merge_blocks(1ull << (3 * lp)), kThreads, 0, s>>>(v.pyr, 0, 0, 1, lp, v.T);
+    ++launches;
+  }
+  return launches;
+}
+
+// ---------------------------------------------------------------------------
+// K5: node table (partition.py:174-240)
+// ---------------------------------------------------------------------------
+struct NonZeroF {
+  const uint32_t* pyr;
+  uint64_t* out;
+  __device__ uint64_t value(uint64_t i) const { return pyr[i] != 0 ? 1 : 0; }
+  __device__ void store(uint64_t i, uint64_t ex, uint64_t v) const {
+    if (v) out[ex] = i;
+  }
+};
+
+int launch_count_nodes(const SplitView& v, uint64_t total_slots, uint64_t* slots_out, ScanScratch& scr,
+                       cudaStream_t s) {
+  NonZeroF f{v.pyr, slots_out};
+  return device_scan(total_slots, f, scr, nullptr, &v.st->count_b, s);
+}
+
+struct SlotInfo {
+  int32_t ext;      // -1 main
+  int lvl;          // level inside its pyramid
+  uint32_t rx, ry, rz;  // cell inside that level
+};
+
+__device__ __forceinline__ SlotInfo decode_slot(const SplitView& v, uint64_t s) {
+  SlotInfo o;
+  uint64_t local;
+  int top;
+  if (s < v.main_cells) {
+    o.ext = -1;
+    local = s;
+    top = v.D;
+  } else {  // binary search the extension owning the slot (meta sorted by pyr_off)
+    uint32_t lo = 0, hi = v.n_ext;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (v.meta[mid].pyr_off <= s) lo = mid; else hi = mid;
+    }
+    o.ext = (int32_t)lo;
+    local = s - v.meta[lo].pyr_off;
+    top = v.meta[lo].ext;
+  }
+  int l = top;
+  while (l > 0 && level_off(l) > local) --l;
+  o.lvl = l;
+  uint64_t lin = local - level_off(l);
+  uint32_t msk = (1u << l) - 1;
+  o.rx = (uint32_t)(lin >> (2 * l));
+  o.ry = (uint32_t)(lin >> l) & msk;
+  o.rz = (uint32_t)lin & msk;
+  return o;
+}
+
+__global__ void __launch_bounds__(kThreads) k_build_nodes(SplitView v, const uint64_t* slots) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= v.n_nodes) return;
+  uint64_t s = slots[k];
+  SlotInfo si = decode_slot(v, s);
+  uint32_t x = si.rx, y = si.ry, z = si.rz, depth, fine_depth;
+  bool finest;
+  if (si.ext < 0) {
+    depth = si.lvl;
+    finest = si.lvl == v.D;
+    fine_depth = v.D;
+  } else {
+    const ExtMeta& m = v.meta[si.ext];
+    x += (uint32_t)m.ax << si.lvl;
+    y += (uint32_t)m.ay << si.lvl;
+    z += (uint32_t)m.az << si.lvl;
+    depth = m.base + si.lvl;
+    finest = si.lvl == m.ext;
+    fine_depth = m.base + m.ext;
+  }
+  uint32_t val = v.pyr[s];
+  uint32_t flags = 0;
+  if (val != UNMERGEABLE) {
+    flags |= NODE_LEAF;
+    if (val > v.T) {  // oversized only at the finest level at max depth (partition.py:222-224)
+      flags |= NODE_OVERSIZED;
+      if (!(finest && (int)fine_depth >= v.max_depth)) raise_err(v.st, ERR_OVERSIZED, k);
+    }
+  }
+  v.node_idx[s] = (int32_t)k;
+  v.n_cell[k] = pack_cell(x, y, z, depth, flags);
+  v.n_val[k] = val;
+  v.n_slot[k] = s;
+  v.n_extid[k] = si.ext;
+  v.n_lvl[k] = (uint8_t)si.lvl;
+  v.n_parent[k] = -1;
+  v.n_count[k] = 0;
+  v.n_first[k] = 0;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) v.n_child[8ull * k + o] = -1;
+}
+
+__global__ void __launch_bounds__(kThreads) k_link(SplitView v) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= v.n_nodes) return;
+  uint64_t cell = v.n_cell[k];
+  uint32_t depth = (uint32_t)(cell >> 48) & 0xFF;
+  if (depth == 0) {
+    if (k != 0) raise_err(v.st, ERR_NO_ROOT, k);
+    return;
+  }
+  int lvl = v.n_lvl[k];
+  int32_t e = v.n_extid[k];
+  uint64_t s = v.n_slot[k];
+  uint64_t ps;
+  if (e < 0 || lvl >= 2) {
+    uint64_t pyr0 = e < 0 ? 0 : v.meta[e].pyr_off;
+    uint64_t lin = s - pyr0 - level_off(lvl);
+    uint32_t d = 1u << lvl, msk = d - 1;
+    uint32_t rx = (uint32_t)(lin >> (2 * lvl)) >> 1, ry = ((uint32_t)(lin >> lvl) & msk) >> 1,
+             rz = ((uint32_t)lin & msk) >> 1;
+    uint32_t dp = d >> 1;
+    ps = pyr0 + level_off(lvl - 1) + ((uint64_t)rx * dp + ry) * dp + rz;
+  } else {
+    ps = v.meta[e].anchor_slot;  // extension level 1 hangs off its anchor cell
+  }
+  if (v.pyr[ps] != UNMERGEABLE) {
+    raise_err(v.st, ERR_NO_PARENT, k);
+    return;
+  }
+  int32_t p = v.node_idx[ps];
+  uint32_t oct = ((uint32_t)cell & 1) | (((uint32_t)(cell >> 16) & 1) << 1) | (((uint32_t)(cell >> 32) & 1) << 2);
+  v.n_parent[k] = p;
+  v.n_child[8ull * p + oct] = (int32_t)k;
+}
+
+// bounds_at(world, path): sequential child_bounds fold (model.py:62-81, hazard H2)
+__global__ void __launch_bounds__(kThreads) k_node_bounds(SplitView v) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= v.n_nodes) return;
+  uint64_t cell = v.n_cell[k];
+  uint32_t cx = (uint32_t)cell & 0xFFFF, cy = (uint32_t)(cell >> 16) & 0xFFFF, cz = (uint32_t)(cell >> 32) & 0xFFFF;
+  int depth = (int)(cell >> 48) & 0xFF;
+  double x = v.st->lo[0], y = v.st->lo[1], z = v.st->lo[2], size = v.st->size;
+  for (int b = depth - 1; b >= 0; --b) {
+    double h = __ddiv_rn(size, 2.0);
+    x = __dadd_rn(x, __dmul_rn(h, (double)((cx >> b) & 1)));
+    y = __dadd_rn(y, __dmul_rn(h, (double)((cy >> b) & 1)));
+    z = __dadd_rn(z, __dmul_rn(h, (double)((cz >> b) & 1)));
+    size = h;
+  }
+  v.n_box[k] = make_double4(x, y, z, size);
+}
+
+int launch_build_nodes(const SplitView& v, const uint64_t* slots, cudaStream_t s) {
+  uint32_t b = ceil_div_u32(v.n_nodes, kThreads);
+  k_build_nodes<<<b, kThreads, 0, s>>>(v, slots);
+  k_link<<<b, kThreads, 0, s>>>(v);
+  k_node_bounds<<<b, kThreads, 0, s>>>(v);
+  return 3;
+}
+
+struct LeafNumF {
+  const uint32_t* val;
+  int32_t* n_leaf;
+  uint32_t* leaf_node;
+  __device__ uint64_t value(uint64_t k) const { return val[k] != UNMERGEABLE ? 1 : 0; }
+  __device__ void store(uint64_t k, uint64_t ex, uint64_t v) const {
+    n_leaf[k] = v ? (int32_t)ex : -1;
+    if (v) leaf_node[ex] = (uint32_t)k;
+  }
+};
+
+int launch_number_leaves(const SplitView& v, ScanScratch& scr, cudaStream_t s) {
+  LeafNumF f{v.n_val, v.n_leaf, v.leaf_node};
+  return device_scan(v.n_nodes, f, scr, nullptr, &v.st->count_a, s);
+}
+
+// Leaf allocation = exclusive prefix of leaf counts (partition.py:264-265 searchsorted bounds)
+struct LeafOffF {
+  const uint32_t* val;
+  const uint32_t* leaf_node;
+  uint64_t* leaf_first;
+  uint64_t* n_first;
+  uint32_t* n_count;
+  __device__ uint64_t value(uint64_t j) const { return val[leaf_node[j]]; }
+  __device__ void store(uint64_t j, uint64_t ex, uint64_t v) const {
+    uint32_t k = leaf_node[j];
+    leaf_first[j] = ex;
+    n_first[k] = ex;
+    n_count[k] = (uint32_t)v;
+  }
+};
+
+int launch_leaf_offsets(const SplitView& v, ScanScratch& scr, cudaStream_t s) {
+  LeafOffF f{v.n_val, v.leaf_node, v.leaf_first, v.n_first, v.n_count};
+  return device_scan(v.n_leaves, f, scr, nullptr, &v.st->count_b, s);
+}
+
+// Per finest cell: the leaf that owns it after merging, found by walking up the pyramid
+// to the first non-zero cell (partition.py:250-258 "iterate upwards").  Cells that are
+// extension anchors keep their -(ext+2) pointer.
+__global__ void __launch_bounds__(kThreads) k_target_main(SplitView v) {
+  const int D = v.D;
+  const uint64_t cells = 1ull << (3 * D);
+  const uint32_t msk = (1u << D) - 1;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    if (v.t8[c] <= -2) continue;
+    uint32_t x = (uint32_t)(c >> (2 * D)), y = (uint32_t)(c >> D) & msk, z = (uint32_t)c & msk;
+    int32_t t = -1;
+    for (int l = D; l >= 0; --l) {
+      int sh = D - l;
+      uint64_t s = level_off(l) + (((uint64_t)(x >> sh) << (2 * l)) | ((uint64_t)(y >> sh) << l) | (z >> sh));
+      uint32_t val = v.pyr[s];
+      if (val == 0) continue;
+      if (val != UNMERGEABLE) t = v.n_leaf[v.node_idx[s]];
+      break;
+    }
+    v.t8[c] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_target_ext(SplitView v, uint32_t first, uint32_t count, int ext) {
+  const uint64_t cells = 1ull << (3 * ext);
+  const uint64_t total = cells * count;
+  const uint32_t msk = (1u << ext) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const ExtMeta& m = v.meta[first + i / cells];
+    uint64_t r = i % cells;
+    int32_t* tp = v.te + m.tgt_off + r;
+    if (*tp <= -2) continue;
+    uint32_t x = (uint32_t)(r >> (2 * ext)), y = (uint32_t)(r >> ext) & msk, z = (uint32_t)r & msk;
+    int32_t t = -1;
+    for (int l = ext; l >= 1; --l) {
+      int sh = ext - l;
+      uint64_t s = m.pyr_off + level_off(l) +
+                   (((uint64_t)(x >> sh) << (2 * l)) | ((uint64_t)(y >> sh) << l) | (z >> sh));
+      uint32_t val = v.pyr[s];
+      if (val == 0) continue;
+      if (val != UNMERGEABLE) t = v.n_leaf[v.node_idx[s]];
+      break;
+    }
+    *tp = t;
+  }
+}
+
+int launch_targets(const SplitView& v, cudaStream_t s) {
+  k_target_main<<<merge_blocks(1ull << (3 * v.D)), kThreads, 0, s>>>(v);
+  return 1;
+}
+
+int launch_targets_ext(const SplitView& v, uint32_t first, uint32_t count, int ext, cudaStream_t s) {
+  if (!count) return 0;
+  k_target_ext<<<merge_blocks((uint64_t)count << (3 * ext)), kThreads, 0, s>>>(v, first, count, ext);
+  return 1;
+}
+
+__global__ void k_depth_hist(SplitView v, uint32_t* depth_count) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= v.n_nodes) return;
+  uint64_t cell = v.n_cell[k];
+  uint32_t depth = (uint32_t)(cell >> 48) & 0xFF;
+  if (v.n_val[k] == UNMERGEABLE) atomicAdd(depth_count + depth, 1u);
+  atomicMax(depth_count + kMaxDepth + 1, depth);
+}
+
+int launch_depth_lists(const SplitView& v, uint32_t* depth_count, cudaStream_t s) {
+  k_depth_hist<<<ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s>>>(v, depth_count);
+  return 1;
+}
+
+__global__ void k_depth_scatter(SplitView v, const uint32_t* depth_off, uint32_t* cursor, uint32_t* lists) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= v.n_nodes || v.n_val[k] != UNMERGEABLE) return;
+  uint32_t depth = (uint32_t)(v.n_cell[k] >> 48) & 0xFF;
+  lists[depth_off[depth] + atomicAdd(cursor + depth, 1u)] = k;
+}
+
+int launch_depth_scatter(const SplitView& v, const uint32_t* depth_off, uint32_t* depth_cursor, uint32_t* lists,
+                         cudaStream_t s) {
+  k_depth_scatter<<<ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s>>>(v, depth_off, depth_cursor, lists);
+  return 1;
+}
+
+__global__ void k_export_nodes(SplitView v, lod_node* out) {
+  uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= v.n_nodes) return;
+  lod_node o;
+  double4 b = v.n_box[k];
+  o.min[0] = b.x, o.min[1] = b.y, o.min[2] = b.z, o.size = b.w;
+  o.first = v.n_first[k];
+  o.count = v.n_count[k];
+  o.parent = v.n_parent[k];
+  uint64_t c = v.n_cell[k];
+  o.cell[0] = (uint16_t)c, o.cell[1] = (uint16_t)(c >> 16), o.cell[2] = (uint16_t)(c >> 32);
+  o.depth = (uint8_t)(c >> 48);
+  o.flags = (uint8_t)(c >> 56);
+  for (int i = 0; i < 8; ++i) o.child[i] = v.n_child[8ull * k + i];
+  out[k] = o;
+}
+
+int launch_export_nodes(const SplitView& v, lod_node* out, cudaStream_t s) {
+  k_export_nodes<<<ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s>>>(v, out);
+  return 1;
+}
+
+}  // namespace lod

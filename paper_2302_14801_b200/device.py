@@ -1,0 +1,152 @@
+"""Device-side tree handle: uploads point records, runs the C ABI, copies results back.
+
+torch is used only for device buffers and the current CUDA stream; every byte of
+LOD work runs in `liblodb200.so`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from ._abi import LOD_POINTS_F32, LOD_POINTS_F64, LodConfig, LodTreeInfo
+
+REC_F32 = np.dtype([("x", "<f4"), ("y", "<f4"), ("z", "<f4"), ("rgba", "u1", 4)])
+REC_F64 = np.dtype([("x", "<f8"), ("y", "<f8"), ("z", "<f8"), ("rgba", "u1", 4), ("pad", "u1", 4)])
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2302_14801_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+def f32_exact(positions: np.ndarray) -> bool:
+    """True when float64 coordinates survive a float32 round trip (then 16-byte records are exact)."""
+    p = np.asarray(positions, np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        return bool(np.array_equal(p.astype(np.float32).astype(np.float64), p))
+
+
+def pack_records(positions, colors, fmt: int | None = None):
+    """Host record array for `positions` (n,3) and `colors` (n,3) u8; picks F32 when exact."""
+    pos = np.asarray(positions)
+    col = np.asarray(colors, np.uint8).reshape(-1, 3)
+    if fmt is None:
+        fmt = LOD_POINTS_F32 if (pos.dtype == np.float32 or f32_exact(pos)) else LOD_POINTS_F64
+    rec = np.zeros(len(col), REC_F32 if fmt == LOD_POINTS_F32 else REC_F64)
+    rec["x"], rec["y"], rec["z"] = pos[:, 0], pos[:, 1], pos[:, 2]
+    rec["rgba"][:, :3] = col
+    return rec, fmt
+
+
+def unpack_records(raw: np.ndarray, fmt: int):
+    rec = raw.view(REC_F32 if fmt == LOD_POINTS_F32 else REC_F64)
+    pos = np.stack([rec["x"], rec["y"], rec["z"]], axis=1).astype(np.float64)
+    col = np.ascontiguousarray(rec["rgba"][:, :3])
+    return pos, col
+
+
+def make_config(T=50_000, initial_depth=8, extension_depth=4, max_depth=16) -> LodConfig:
+    return LodConfig(int(T), int(initial_depth), int(extension_depth), int(max_depth))
+
+
+def current_stream_ptr():
+    torch = _torch()
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class DeviceTree:
+    """One `lod_tree` handle (grow-only device buffers reused across builds)."""
+
+    def __init__(self, device: int | None = None):
+        torch = _torch()
+        self.lib = _abi.load()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.h = self.lib.lod_tree_create(self.device)
+        if not self.h:
+            raise RuntimeError(self.lib.lod_last_error().decode())
+        self._input = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                self.lib.lod_tree_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    # -- uploads -------------------------------------------------------------
+    def upload(self, positions, colors, fmt: int | None = None):
+        torch = _torch()
+        rec, fmt = pack_records(positions, colors, fmt)
+        buf = torch.from_numpy(rec.view(np.uint8).reshape(-1)).to(f"cuda:{self.device}")
+        return buf, fmt, len(rec)
+
+    # -- C ABI calls -----------------------------------------------------------
+    def split(self, d_records, n: int, fmt: int, config: LodConfig, bounds=None, stream=None):
+        b = None
+        if bounds is not None:
+            b = (C.c_double * 4)(*[float(x) for x in bounds])
+        self._input = d_records  # keep alive for the duration of the call
+        _abi.check(self.lib.lod_split(self.h, C.c_void_p(d_records.data_ptr()), n, fmt, b, C.byref(config),
+                                      stream if stream is not None else current_stream_ptr()))
+        self._input = None
+
+    def voxelize(self, mode: int, seed: int, stream=None):
+        _abi.check(self.lib.lod_voxelize(self.h, mode, int(seed) & ((1 << 64) - 1),
+                                         stream if stream is not None else current_stream_ptr()))
+
+    def build(self, d_records, n: int, fmt: int, config: LodConfig, mode: int, seed: int, stream=None):
+        _abi.check(self.lib.lod_build(self.h, C.c_void_p(d_records.data_ptr()), n, fmt, C.byref(config), mode,
+                                      int(seed) & ((1 << 64) - 1),
+                                      stream if stream is not None else current_stream_ptr()))
+
+    def info(self) -> LodTreeInfo:
+        out = LodTreeInfo()
+        _abi.check(self.lib.lod_tree_get_info(self.h, C.byref(out)))
+        return out
+
+    def nodes(self) -> np.ndarray:
+        info = self.info()
+        arr = np.zeros(info.n_nodes, _abi.node_dtype())
+        _abi.check(self.lib.lod_tree_copy_nodes(self.h, arr.ctypes.data_as(C.c_void_p), current_stream_ptr()))
+        return arr
+
+    def leaf_records(self) -> np.ndarray:
+        info = self.info()
+        size = 16 if info.point_format == LOD_POINTS_F32 else 32
+        raw = np.empty(info.n_points * size, np.uint8)
+        _abi.check(self.lib.lod_tree_copy_leaf_points(self.h, raw.ctypes.data_as(C.c_void_p), current_stream_ptr()))
+        return raw
+
+    def voxels(self) -> np.ndarray:
+        info = self.info()
+        raw = np.empty((info.n_voxels, 2), np.uint32)
+        if info.n_voxels:
+            _abi.check(self.lib.lod_tree_copy_voxels(self.h, raw.ctypes.data_as(C.c_void_p), current_stream_ptr()))
+        return raw
+
+    def device_ptrs(self):
+        lp, vp = C.c_void_p(), C.c_void_p()
+        _abi.check(self.lib.lod_tree_leaf_points(self.h, C.byref(lp)))
+        if self.info().voxel_mode >= 0:
+            _abi.check(self.lib.lod_tree_voxels(self.h, C.byref(vp)))
+        return lp.value, vp.value
+
+    def set_timing(self, on: bool):
+        _abi.check(self.lib.lod_set_timing(self.h, 1 if on else 0))
+
+    def stage_ms(self):
+        out = (C.c_float * 5)()
+        _abi.check(self.lib.lod_tree_stage_ms(self.h, out))
+        return list(out)
+
+    def launches(self) -> int:
+        return int(self.lib.lod_tree_launches(self.h))
+
+    def device_bytes(self) -> int:
+        return int(self.lib.lod_tree_device_bytes(self.h))

@@ -1,0 +1,55 @@
+"""GPU parity: the CUDA path through the C ABI vs the reference's golden digests.
+
+Every case in tests/golden/cases.py was produced by the unmodified reference
+(`make_golden.py`).  Bit-exact requirements:
+  node hierarchy (paths, leaf/inner), per-leaf point counts, oversized flags,
+  fp64 node bounds, leaf contents in input order, voxel coordinates and colours for
+  random and average ("color_filter") sampling, and the reference's
+  ConsistencyError on the 2^20 random-sampling limit.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden_available, load_golden
+from cases import CASES, make_input
+from helpers import diff_dicts, tree_split_digest, tree_voxel_digest
+
+pytestmark = pytest.mark.gpu
+
+QUICK = [c for c in CASES if c["quick"]]
+LARGE = [c for c in CASES if not c["quick"]]
+
+
+def run_case(case):
+    from paper_2302_14801_b200 import BuildConfig, ConsistencyError, PointCloud, build_lod, partition
+    g = load_golden(case["name"])
+    pos, col = make_input(case)
+    cloud = PointCloud(np.asarray(pos, np.float64), col)
+    tree = partition(cloud, BuildConfig(**case["cfg"]))
+    assert [float(v).hex() for v in tree.world_bounds.min] + [float(tree.world_bounds.size).hex()] == g["world"]
+    got = tree_split_digest(tree)
+    bad, nbad = diff_dicts(got, g["split"])
+    assert nbad == 0, f"{case['name']}: {nbad} split mismatches, e.g. {bad}"
+    for mode, exp in g["modes"].items():
+        strat, _, seed = mode.partition(":")
+        if "error" in exp:
+            with pytest.raises(ConsistencyError) as ei:
+                build_lod(tree, strat, int(seed or 0))
+            assert str(ei.value) == exp["error"]
+            continue
+        build_lod(tree, strat, int(seed or 0))
+        got_v = tree_voxel_digest(tree)
+        bad, nbad = diff_dicts(got_v, exp)
+        assert nbad == 0, f"{case['name']} {mode}: {nbad} voxel mismatches, e.g. {bad}"
+
+
+@pytest.mark.parametrize("case", QUICK, ids=[c["name"] for c in QUICK])
+def test_gpu_matches_reference(case):
+    run_case(case)
+
+
+@pytest.mark.parametrize("case", LARGE, ids=[c["name"] for c in LARGE])
+def test_gpu_matches_reference_large(case):
+    if not golden_available(case["name"]):
+        pytest.skip("golden not generated")
+    run_case(case)
