@@ -88,9 +88,9 @@ struct lod_tree {
 
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
   DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
-  DevBuf leaf_node, leaf_first, depth_count, depth_off, depth_cursor, depth_lists;
+  DevBuf leaf_node, leaf_first, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
   DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf;
-  DevBuf vox, scratch, export_buf;
+  DevBuf vox, scratch, export_buf, stash;
   DevState* host_state = nullptr;  // pinned mirror
 
   uint32_t n_nodes = 0, n_leaves = 0, n_ext = 0, max_depth_used = 0;
@@ -207,6 +207,8 @@ SplitView make_view(lod_tree* t, const void* pts) {
   v.n_nodes = t->n_nodes;
   v.leaf_node = t->leaf_node.as<uint32_t>();
   v.leaf_first = t->leaf_first.as<uint64_t>();
+  v.leaf_pbox = t->leaf_pbox.as<double4>();
+  v.leaf_pinv = t->leaf_pinv.as<double>();
   v.n_leaves = t->n_leaves;
   return v;
 }
@@ -375,6 +377,8 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   CK(ensure(t->n_count, nn * 4));
   CK(ensure(t->leaf_node, nn * 4));
   CK(ensure(t->leaf_first, nn * 8));
+  CK(ensure(t->leaf_pbox, nn * 32));
+  CK(ensure(t->leaf_pinv, nn * 8));
   CK(ensure(t->depth_count, 64 * 4));
   CK(cudaMemsetAsync(t->depth_count.p, 0, 64 * 4, s));
   v = make_view(t, pts);
@@ -389,6 +393,7 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   t->n_leaves = (uint32_t)t->host_state->count_a;
   v = make_view(t, pts);
   RUN(launch_leaf_offsets(v, scr, s));
+  RUN(launch_leaf_parent_boxes(v, s));
   RUN(launch_targets(v, s));
   for (auto& rd : t->rounds) RUN(launch_targets_ext(v, rd.first, rd.count, rd.ext, s));
   // per-depth inner-node lists for the voxelizer
@@ -409,7 +414,8 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   int bits = ceil_log2(t->n_leaves);
   if (bits > 2 * kRadixMaxBits)
     return fail(LOD_EUNSUPPORTED, "%u leaves exceed the 2-pass distribute limit", t->n_leaves);
-  p.passes = bits == 0 ? 0 : (bits <= kRadixMaxBits ? 1 : 2);
+  // a root leaf needs no stash; any other tree takes at least one (stable) pass
+  p.passes = t->n_nodes == 1 ? 0 : (bits <= kRadixMaxBits ? 1 : 2);
   p.bits[0] = p.passes == 2 ? bits / 2 : bits;
   p.bits[1] = p.passes == 2 ? bits - bits / 2 : 0;
   p.tiles = (uint32_t)((n + kRadixTile - 1) / kRadixTile);
@@ -439,6 +445,8 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
     p.tmp_rec = t->tmp_rec.p;
     p.tmp_leaf = t->tmp_leaf.as<uint32_t>();
     p.epoch = t->epoch;
+    CK(ensure(t->stash, n * 8));
+    p.stash = t->stash.as<uint2>();
   }
   v = make_view(t, pts);
   RUN(launch_distribute(fmt, v, p, t->leaf_pts.p, s));
@@ -485,6 +493,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
     vv.st = t->state.as<DevState>();
     vv.fmt = t->fmt;
     vv.leaf_pts = t->leaf_pts.p;
+    vv.stash = t->stash.as<uint2>();
     vv.n_cell = t->n_cell.as<uint64_t>();
     vv.n_child = t->n_child.as<int32_t>();
     vv.n_box = t->n_box.as<double4>();
@@ -543,8 +552,9 @@ void lod_tree_destroy(lod_tree* t) {
   DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan, &t->slots,
                    &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid, &t->n_lvl,
                    &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node, &t->leaf_first,
-                   &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
-                   &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf};
+                   &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
+                   &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf,
+                   &t->stash};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -637,9 +647,9 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
   const DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan,
                          &t->slots, &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid,
                          &t->n_lvl, &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node,
-                         &t->leaf_first, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists,
+                         &t->leaf_first, &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists,
                          &t->leaf_pts, &t->status, &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf,
-                         &t->vox, &t->scratch, &t->export_buf};
+                         &t->vox, &t->scratch, &t->export_buf, &t->stash};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;

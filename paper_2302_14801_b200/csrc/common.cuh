@@ -44,6 +44,7 @@ struct DevState {
   unsigned long long hi_key[3];
   double lo[3];                   // world cube (model.py:199-209 or caller bounds)
   double size;
+  double inv_size;                // RN(1 / size), fast-path projection
   uint32_t err;
   uint32_t err_detail;            // node id for voxelize errors
   unsigned long long err_value;   // e.g. the sample count of the 2^20 violation
@@ -131,12 +132,25 @@ struct Rec<LOD_POINTS_F64> {
 // projection (reference model.py:84-98; hazard H1: correctly rounded fp64)
 // ---------------------------------------------------------------------------
 
+// floor(RN(rel / size) * 2^k) exactly.  Fast path multiplies by inv = RN(1/size): the
+// product is within 2 ulp of RN(rel/size), i.e. within 2^(k-51) of the exact scaled value,
+// so the floor can only differ when the scaled value lies within 2^-30 of an integer; those
+// (about 1e-9 of the points) take the correctly rounded division (hazard H1).
+template <int K>
+__device__ __forceinline__ double exact_scaled_floor(double rel, double size, double inv) {
+  constexpr double scale = (double)(1u << K);
+  double f = __dmul_rn(__dmul_rn(rel, inv), scale);
+  double c = floor(f);
+  double fr = __dsub_rn(f, c);
+  if (fr < 0x1p-30 || fr > 1.0 - 0x1p-30) c = floor(__dmul_rn(__ddiv_rn(rel, size), scale));
+  return c;
+}
+
 // One axis of the depth-16 cell; sets *bad if p lies outside [lo, lo + size].
-__device__ __forceinline__ uint32_t quant16(double p, double lo, double size, bool& bad) {
+__device__ __forceinline__ uint32_t quant16(double p, double lo, double size, double inv, bool& bad) {
   double rel = __dsub_rn(p, lo);
   bad |= !(rel >= 0.0) || (rel > size);
-  double q = __ddiv_rn(rel, size);
-  double f = floor(__dmul_rn(q, 65536.0));
+  double f = exact_scaled_floor<16>(rel, size, inv);
   f = fmin(fmax(f, 0.0), 65535.0);
   return (uint32_t)f;
 }
@@ -148,10 +162,18 @@ struct Cell16 {
 template <int FMT>
 __device__ __forceinline__ Cell16 cell16(const typename Rec<FMT>::Raw& r, const DevState& st, bool& bad) {
   Cell16 c;
-  c.x = quant16(Rec<FMT>::x(r), st.lo[0], st.size, bad);
-  c.y = quant16(Rec<FMT>::y(r), st.lo[1], st.size, bad);
-  c.z = quant16(Rec<FMT>::z(r), st.lo[2], st.size, bad);
+  c.x = quant16(Rec<FMT>::x(r), st.lo[0], st.size, st.inv_size, bad);
+  c.y = quant16(Rec<FMT>::y(r), st.lo[1], st.size, st.inv_size, bad);
+  c.z = quant16(Rec<FMT>::z(r), st.lo[2], st.size, st.inv_size, bad);
   return c;
+}
+
+// Leaf point -> cell of its parent's 128^3 sampling grid (sampling.py:29-38):
+// clip((p - min) / size * 128, 0, nextafter(128, 0)) floored == clamp(floor(.), 0, 127).
+// `inv` = RN(1/size) of the parent = RN(1/world_size) * 2^depth exactly.
+__device__ __forceinline__ uint32_t grid_cell128(double p, double lo, double size, double inv) {
+  double f = exact_scaled_floor<7>(__dsub_rn(p, lo), size, inv);
+  return (uint32_t)fmin(fmax(f, 0.0), 127.0);
 }
 
 // linear x-major key of the cell at `depth` (partition.py:23-24)

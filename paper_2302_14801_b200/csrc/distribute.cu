@@ -37,9 +37,10 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
 }
 
 template <int FMT, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kRadixThreads, 2)
-    k_radix(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf, int shift,
-            int bits, const uint64_t* digit_base, uint64_t* status, uint32_t epoch, uint32_t* ticket) {
+__global__ void __launch_bounds__(kRadixThreads, 1)
+    k_radix(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
+            uint2* out_stash, int shift, int bits, const uint64_t* digit_base, uint64_t* status, uint32_t epoch,
+            uint32_t* ticket) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int B = 1 << bits;
   uint16_t* wh = reinterpret_cast<uint16_t*>(smem);                       // [kW][B] warp histograms
@@ -54,22 +55,25 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * kRadixItems;
   const uint32_t lt_mask = (1u << lane) - 1;
 
-  DevState st;
-  if (FIRST) st = *v.st;
+  const double lo0 = v.st->lo[0], lo1 = v.st->lo[1], lo2 = v.st->lo[2];
+  const double size = v.st->size, inv = v.st->inv_size;
   bool bad = false, unresolved = false;
   uint32_t leaf[kRadixItems];
   uint16_t rk[kRadixItems];
 
-  // --- 1. leaf ids + stable in-warp ranks ---
+  // --- 1a. leaf ids (no shared memory here, so the record loads of all items overlap) ---
 #pragma unroll
   for (int k = 0; k < kRadixItems; ++k) {
     const uint64_t i = base + (uint64_t)k * 32 + lane;
-    const bool valid = i < v.n;
     uint32_t lf = 0;
-    if (valid) {
+    if (i < v.n) {
       if (FIRST) {
         auto r = Rec<FMT>::load(in_rec, i);
-        int32_t t = leaf_of_point(v, cell16<FMT>(r, st, bad));
+        Cell16 c;
+        c.x = quant16(Rec<FMT>::x(r), lo0, size, inv, bad);
+        c.y = quant16(Rec<FMT>::y(r), lo1, size, inv, bad);
+        c.z = quant16(Rec<FMT>::z(r), lo2, size, inv, bad);
+        int32_t t = leaf_of_point(v, c);
         if (t < 0) {
           unresolved = true;
           t = 0;
@@ -80,7 +84,12 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
       }
     }
     leaf[k] = lf;
-    const uint32_t d = (lf >> shift) & (B - 1);
+  }
+  // --- 1b. stable in-warp ranks (warp-major, round-major, lane order) ---
+#pragma unroll
+  for (int k = 0; k < kRadixItems; ++k) {
+    const bool valid = base + (uint64_t)k * 32 + lane < v.n;
+    const uint32_t d = (leaf[k] >> shift) & (B - 1);
     const unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
     uint32_t rank = 0;
     if (valid) {
@@ -132,15 +141,27 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   }
   __syncthreads();
 
-  // --- 3. scatter (record re-read from L2) ---
+  // --- 3. scatter (record re-read from L2); the last pass also writes each point's cell
+  //        in its leaf-parent's 128^3 grid (the voxelizer's sample stash) ---
 #pragma unroll
   for (int k = 0; k < kRadixItems; ++k) {
     const uint64_t i = base + (uint64_t)k * 32 + lane;
     if (i < v.n) {
       const uint32_t d = (leaf[k] >> shift) & (B - 1);
       const uint64_t dest = tbase[d] + wh[warp * B + d] + rk[k];
-      Rec<FMT>::store(out_rec, dest, Rec<FMT>::load(in_rec, i));
+      auto r = Rec<FMT>::load(in_rec, i);
+      Rec<FMT>::store(out_rec, dest, r);
       if (!LAST) out_leaf[dest] = leaf[k];
+      if (LAST && out_stash) {
+        const double4 b = v.leaf_pbox[leaf[k]];
+        uint32_t key = 0;
+        if (b.w > 0) {
+          const double pinv = v.leaf_pinv[leaf[k]];
+          key = (grid_cell128(Rec<FMT>::x(r), b.x, b.w, pinv) << 14) |
+                (grid_cell128(Rec<FMT>::y(r), b.y, b.w, pinv) << 7) | grid_cell128(Rec<FMT>::z(r), b.z, b.w, pinv);
+        }
+        out_stash[dest] = make_uint2(key, Rec<FMT>::rgb(r));
+      }
     }
   }
   if (FIRST) {
@@ -170,11 +191,12 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
 template <int FMT, bool FIRST, bool LAST>
 void run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
               int shift, int bits, const uint64_t* digit_base, RadixPlan& p, uint32_t* ticket, cudaStream_t s) {
+  uint2* stash = LAST ? p.stash : nullptr;
   size_t smem = (size_t)kW * (1u << bits) * 2 + (size_t)(1u << bits) * 8;
   auto kern = k_radix<FMT, FIRST, LAST>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<p.tiles, kRadixThreads, smem, s>>>(v, in_rec, in_leaf, out_rec, out_leaf, shift, bits, digit_base, p.status,
-                                            p.epoch, ticket);
+  kern<<<p.tiles, kRadixThreads, smem, s>>>(v, in_rec, in_leaf, out_rec, out_leaf, stash, shift, bits, digit_base,
+                                            p.status, p.epoch, ticket);
 }
 
 template <int FMT>

@@ -40,6 +40,8 @@ struct SplitView {
   uint32_t n_nodes;
   uint32_t* leaf_node;
   uint64_t* leaf_first;
+  double4* leaf_pbox;     // per leaf: parent bounds (w < 0 for a root leaf)
+  double* leaf_pinv;      // per leaf: RN(1 / parent size)
   uint32_t n_leaves;
 };
 
@@ -94,6 +96,7 @@ int launch_count_nodes(const SplitView& v, uint64_t total_slots, uint64_t* slots
 int launch_build_nodes(const SplitView& v, const uint64_t* slots, cudaStream_t s);
 int launch_number_leaves(const SplitView& v, ScanScratch& scr, cudaStream_t s);
 int launch_leaf_offsets(const SplitView& v, ScanScratch& scr, cudaStream_t s);
+int launch_leaf_parent_boxes(const SplitView& v, cudaStream_t s);
 int launch_targets(const SplitView& v, cudaStream_t s);
 int launch_targets_ext(const SplitView& v, uint32_t first, uint32_t count, int ext, cudaStream_t s);
 int launch_depth_lists(const SplitView& v, uint32_t* depth_count, cudaStream_t s);
@@ -113,6 +116,7 @@ struct RadixPlan {
   uint32_t* tile_ticket;  // per pass
   void* tmp_rec;          // pass-0 output records (2 passes)
   uint32_t* tmp_leaf;     // pass-0 output leaf ids
+  uint2* stash;           // per leaf-buffer slot: {cell key in the leaf-parent's 128^3 grid, rgb}
 };
 constexpr int kRadixThreads = 512;
 constexpr int kRadixItems = 16;
@@ -125,6 +129,7 @@ struct VoxView {
   DevState* st;
   int fmt;
   const void* leaf_pts;
+  const uint2* stash;     // leaf points as {key in the leaf-parent grid, rgb} (distribute output)
   const uint64_t* n_cell;
   const int32_t* n_child;
   const double4* n_box;

@@ -67,24 +67,77 @@ __global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* sums, uint32_t nb,
 
 template <class F>
 __global__ void __launch_bounds__(kScanThreads) k_scan_store(uint64_t n, F f, const uint64_t* block_sums) {
-  __shared__ uint64_t sm[kScanThreads / 32 + 1];
-  // items owned by a thread are contiguous so one sequential pass keeps the order
-  uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-  uint64_t v[kScanItems];
-  uint64_t s = 0;
-#pragma unroll
+  // 16 coalesced trips of 256 consecutive items; a block-wide scan per trip keeps the order
+  __shared__ uint64_t warp_tot[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t running = block_sums[blockIdx.x];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
   for (int k = 0; k < kScanItems; ++k) {
-    uint64_t i = base + k;
-    v[k] = (i < n) ? f.value(i) : 0;
-    s += v[k];
+    const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
+    const uint64_t v = i < n ? f.value(i) : 0;
+    const uint64_t incl = warp_incl_scan(v);
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    uint64_t off = running, trip = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+      uint64_t t = warp_tot[w];
+      off += w < warp ? t : 0;
+      trip += t;
+    }
+    if (i < n) f.store(i, off + incl - v, v);
+    running += trip;
+    __syncthreads();
   }
-  uint64_t tot;
-  uint64_t pre = block_excl_scan<uint64_t, kScanThreads>(s, &tot, sm) + block_sums[blockIdx.x];
+}
+
+// ---------------------------------------------------------------------------
+// Order-preserving compaction of predicate hits (f.pred(i) -> bool, f.emit(i, pos)).
+// Warps own contiguous 512-item runs of a 4096-item tile and rank hits with ballots, so
+// every load is coalesced and there is one block barrier per tile.
+// ---------------------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(kScanThreads) k_compact_count(uint64_t n, F f, uint64_t* block_sums) {
+  __shared__ uint32_t wc[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)warp * 32 * kScanItems;
+  uint32_t c = 0;
+#pragma unroll 4
+  for (int k = 0; k < kScanItems; ++k) {
+    uint64_t i = base + (uint64_t)k * 32 + lane;
+    c += __popc(__ballot_sync(0xFFFFFFFFu, i < n && f.pred(i)));
+  }
+  if (lane == 0) wc[warp] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) t += wc[w];
+    block_sums[blockIdx.x] = t;
+  }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kScanThreads) k_compact_store(uint64_t n, F f, const uint64_t* block_sums) {
+  __shared__ uint32_t wc[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)warp * 32 * kScanItems;
+  uint32_t hits[kScanItems];
+  uint32_t c = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    uint64_t i = base + k;
-    if (i < n) f.store(i, pre, v[k]);
-    pre += v[k];
+    uint64_t i = base + (uint64_t)k * 32 + lane;
+    hits[k] = __ballot_sync(0xFFFFFFFFu, i < n && f.pred(i));
+    c += __popc(hits[k]);
+  }
+  if (lane == 0) wc[warp] = c;
+  __syncthreads();
+  uint64_t pos = block_sums[blockIdx.x];
+  for (int w = 0; w < warp; ++w) pos += wc[w];
+  const uint32_t lt = (1u << lane) - 1;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (hits[k] >> lane & 1) f.emit(base + (uint64_t)k * 32 + lane, pos + __popc(hits[k] & lt));
+    pos += __popc(hits[k]);
   }
 }
 
@@ -105,6 +158,18 @@ int device_scan(uint64_t n, F f, ScanScratch& scr, const uint64_t* base_in, uint
   k_scan_reduce<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
   k_scan_sums<<<1, 1024, 0, st>>>(scr.sums, nb, base_in, total_out);
   k_scan_store<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
+  return 3;
+}
+
+// Compaction of f.pred hits over [0, n); writes the hit count to *total_out (device).
+template <class F>
+int device_compact(uint64_t n, F f, ScanScratch& scr, uint64_t* total_out, cudaStream_t st) {
+  uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
+  if (nb == 0) nb = 1;
+  if (scr.cap < nb + 1) return -1;
+  k_compact_count<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
+  k_scan_sums<<<1, 1024, 0, st>>>(scr.sums, nb, nullptr, total_out);
+  k_compact_store<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
   return 3;
 }
 

@@ -65,6 +65,7 @@ __global__ void k_bounds_finalize(DevState* st, int user, double ux, double uy, 
   if (threadIdx.x != 0) return;
   if (user) {
     st->lo[0] = ux, st->lo[1] = uy, st->lo[2] = uz, st->size = us;
+    st->inv_size = __drcp_rn(us);
     return;
   }
   double ext = 0.0;
@@ -74,6 +75,7 @@ __global__ void k_bounds_finalize(DevState* st, int user, double ux, double uy, 
     ext = fmax(ext, __dsub_rn(h, l));
   }
   st->size = ext > 0.0 ? ext : 1.0;
+  st->inv_size = __drcp_rn(st->size);
 }
 
 int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const double* ub, cudaStream_t s) {
@@ -141,15 +143,13 @@ struct AnchorF {  // main finest cells with count > T (partition.py:111)
   const uint32_t* grid;
   uint32_t T;
   uint64_t* out;
-  __device__ uint64_t value(uint64_t i) const { return grid[i] > T ? 1 : 0; }
-  __device__ void store(uint64_t i, uint64_t ex, uint64_t v) const {
-    if (v) out[ex] = i;
-  }
+  __device__ bool pred(uint64_t i) const { return __ldg(grid + i) > T; }
+  __device__ void emit(uint64_t i, uint64_t pos) const { out[pos] = i; }
 };
 
 int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s) {
   AnchorF f{v.pyr + level_off(v.D), v.T, list};
-  return device_scan(1ull << (3 * v.D), f, scr, nullptr, &v.st->count_a, s);
+  return device_compact(1ull << (3 * v.D), f, scr, &v.st->count_a, s);
 }
 
 struct SubAnchorF {  // extension finest cells with count > T (partition.py:140-143)
@@ -159,20 +159,18 @@ struct SubAnchorF {  // extension finest cells with count > T (partition.py:140-
   int ext;
   uint32_t T;
   uint64_t* out;
-  __device__ uint64_t value(uint64_t i) const {
+  __device__ bool pred(uint64_t i) const {
     uint64_t cells = 1ull << (3 * ext);
     const ExtMeta& m = meta[first + i / cells];
-    return pyr[m.pyr_off + level_off(ext) + i % cells] > T ? 1 : 0;
+    return pyr[m.pyr_off + level_off(ext) + i % cells] > T;
   }
-  __device__ void store(uint64_t i, uint64_t ex, uint64_t v) const {
-    if (v) out[ex] = i;
-  }
+  __device__ void emit(uint64_t i, uint64_t pos) const { out[pos] = i; }
 };
 
 int launch_find_subanchors(const SplitView& v, uint32_t first_ext, uint32_t n_ext_round, int ext_levels,
                            uint64_t* list, ScanScratch& scr, cudaStream_t s) {
   SubAnchorF f{v.pyr, v.meta, first_ext, ext_levels, v.T, list};
-  return device_scan((uint64_t)n_ext_round << (3 * ext_levels), f, scr, nullptr, &v.st->count_a, s);
+  return device_compact((uint64_t)n_ext_round << (3 * ext_levels), f, scr, &v.st->count_a, s);
 }
 
 __global__ void k_ext_create(SplitView v, int round, uint32_t first, uint32_t count, const uint64_t* list,
@@ -347,16 +345,14 @@ int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint
 struct NonZeroF {
   const uint32_t* pyr;
   uint64_t* out;
-  __device__ uint64_t value(uint64_t i) const { return pyr[i] != 0 ? 1 : 0; }
-  __device__ void store(uint64_t i, uint64_t ex, uint64_t v) const {
-    if (v) out[ex] = i;
-  }
+  __device__ bool pred(uint64_t i) const { return __ldg(pyr + i) != 0; }
+  __device__ void emit(uint64_t i, uint64_t pos) const { out[pos] = i; }
 };
 
 int launch_count_nodes(const SplitView& v, uint64_t total_slots, uint64_t* slots_out, ScanScratch& scr,
                        cudaStream_t s) {
   NonZeroF f{v.pyr, slots_out};
-  return device_scan(total_slots, f, scr, nullptr, &v.st->count_b, s);
+  return device_compact(total_slots, f, scr, &v.st->count_b, s);
 }
 
 struct SlotInfo {
@@ -528,33 +524,73 @@ struct LeafOffF {
   }
 };
 
+// Per leaf, the bounds of its parent (the node whose 128^3 grid its points are sampled
+// into, sampling.py:29-38) and RN(1/size) = RN(1/world_size) * 2^depth (exact scaling).
+__global__ void k_leaf_parent_boxes(SplitView v) {
+  uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.n_leaves) return;
+  int32_t par = v.n_parent[v.leaf_node[j]];
+  if (par < 0) {
+    v.leaf_pbox[j] = make_double4(0, 0, 0, -1.0);
+    v.leaf_pinv[j] = 0;
+    return;
+  }
+  int depth = (int)(v.n_cell[par] >> 48) & 0xFF;
+  v.leaf_pbox[j] = v.n_box[par];
+  v.leaf_pinv[j] = __dmul_rn(v.st->inv_size, (double)(1ull << depth));
+}
+
+int launch_leaf_parent_boxes(const SplitView& v, cudaStream_t s) {
+  k_leaf_parent_boxes<<<ceil_div_u32(v.n_leaves, kThreads), kThreads, 0, s>>>(v);
+  return 1;
+}
+
 int launch_leaf_offsets(const SplitView& v, ScanScratch& scr, cudaStream_t s) {
   LeafOffF f{v.n_val, v.leaf_node, v.leaf_first, v.n_first, v.n_count};
   return device_scan(v.n_leaves, f, scr, nullptr, &v.st->count_b, s);
 }
 
-// Per finest cell: the leaf that owns it after merging, found by walking up the pyramid
-// to the first non-zero cell (partition.py:250-258 "iterate upwards").  Cells that are
-// extension anchors keep their -(ext+2) pointer.
-__global__ void __launch_bounds__(kThreads) k_target_main(SplitView v) {
-  const int D = v.D;
-  const uint64_t cells = 1ull << (3 * D);
-  const uint32_t msk = (1u << D) - 1;
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
-       c += (uint64_t)gridDim.x * blockDim.x) {
-    if (v.t8[c] <= -2) continue;
-    uint32_t x = (uint32_t)(c >> (2 * D)), y = (uint32_t)(c >> D) & msk, z = (uint32_t)c & msk;
-    int32_t t = -1;
-    for (int l = D; l >= 0; --l) {
-      int sh = D - l;
-      uint64_t s = level_off(l) + (((uint64_t)(x >> sh) << (2 * l)) | ((uint64_t)(y >> sh) << l) | (z >> sh));
-      uint32_t val = v.pyr[s];
-      if (val == 0) continue;
-      if (val != UNMERGEABLE) t = v.n_leaf[v.node_idx[s]];
-      break;
-    }
-    v.t8[c] = t;
+// Per cell: the leaf that owns it after merging (partition.py:250-258 "iterate upwards"),
+// computed top-down one level at a time: a plain non-zero cell is its own leaf, an
+// UNMERGEABLE cell owns nothing, an empty cell inherits its parent's owner.  The result is
+// written in place over node_idx (level l reads level l-1's finished targets); the finest
+// level goes to t8, where extension anchors keep their -(ext+2) pointer.
+__device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t c) {
+  const uint64_t s = level_off(l) + c;
+  const uint32_t val = v.pyr[s];
+  int32_t t;
+  if (val == UNMERGEABLE) {
+    t = -1;
+  } else if (val != 0) {
+    t = v.n_leaf[v.node_idx[s]];
+  } else if (l == 0) {
+    t = -1;
+  } else {
+    const uint32_t msk = (1u << l) - 1;
+    uint32_t x = (uint32_t)(c >> (2 * l)) >> 1, y = ((uint32_t)(c >> l) & msk) >> 1, z = ((uint32_t)c & msk) >> 1;
+    uint32_t dp = 1u << (l - 1);
+    t = v.node_idx[level_off(l - 1) + ((uint64_t)x * dp + y) * dp + z];
   }
+  if (l == v.D) {
+    if (val != UNMERGEABLE) v.t8[c] = t;  // anchors keep -(ext+2); t8 was cleared to -1
+  } else {
+    v.node_idx[s] = t;
+  }
+}
+
+// levels 0..top in one block (small levels, block barriers between them)
+__global__ void __launch_bounds__(1024) k_target_small(SplitView v, int top) {
+  for (int l = 0; l <= top; ++l) {
+    for (uint64_t c = threadIdx.x; c < (1ull << (3 * l)); c += blockDim.x) target_cell(v, l, c);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_target_level(SplitView v, int l) {
+  const uint64_t cells = 1ull << (3 * l);
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+       c += (uint64_t)gridDim.x * blockDim.x)
+    target_cell(v, l, c);
 }
 
 __global__ void __launch_bounds__(kThreads) k_target_ext(SplitView v, uint32_t first, uint32_t count, int ext) {
@@ -583,8 +619,12 @@ __global__ void __launch_bounds__(kThreads) k_target_ext(SplitView v, uint32_t f
 }
 
 int launch_targets(const SplitView& v, cudaStream_t s) {
-  k_target_main<<<merge_blocks(1ull << (3 * v.D)), kThreads, 0, s>>>(v);
-  return 1;
+  const int small = std::min(v.D, 3);
+  k_target_small<<<1, 1024, 0, s>>>(v, small);
+  int launches = 1;
+  for (int l = small + 1; l <= v.D; ++l, ++launches)
+    k_target_level<<<merge_blocks(1ull << (3 * l)), kThreads, 0, s>>>(v, l);
+  return launches;
 }
 
 int launch_targets_ext(const SplitView& v, uint32_t first, uint32_t count, int ext, cudaStream_t s) {

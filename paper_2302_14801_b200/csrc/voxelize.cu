@@ -61,33 +61,23 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-// leaf point -> parent grid cell: clip((p - min) / size * 128, 0, nextafter(128, 0)) floored
-// (sampling.py:29-38)
-__device__ __forceinline__ uint32_t gcell(double p, double lo, double size) {
-  double g = __dmul_rn(__ddiv_rn(__dsub_rn(p, lo), size), 128.0);
-  double f = fmin(fmax(floor(g), 0.0), 127.0);
-  return (uint32_t)f;
-}
-
-template <int FMT>
-__device__ __forceinline__ uint32_t sample_key(const VoxView& v, const VoxSmem& s, int o, uint32_t j,
-                                               uint32_t& rgb) {
-  if (s.ckind[o] == 1) {
-    auto r = Rec<FMT>::load(v.leaf_pts, s.cfirst[o] + j);
-    rgb = Rec<FMT>::rgb(r);
-    uint32_t x = gcell(Rec<FMT>::x(r), s.lo[0], s.size);
-    uint32_t y = gcell(Rec<FMT>::y(r), s.lo[1], s.size);
-    uint32_t z = gcell(Rec<FMT>::z(r), s.lo[2], s.size);
-    return (x << 14) | (y << 7) | z;
-  }
-  // child voxel c in octant o -> floor(off + (c + 0.5) / 2) = off + c / 2 (sampling.py:41-44)
-  uint2 vx = __ldg(v.vox + s.cfirst[o] + j);
-  rgb = vx.y;
-  uint32_t k = vx.x;
+// child voxel key c in octant o -> parent key floor(off + (c + 0.5) / 2) = off + c / 2
+// (sampling.py:41-44)
+__device__ __forceinline__ uint32_t voxel_to_parent(int o, uint32_t k) {
   uint32_t x = ((uint32_t)(o & 1) << 6) | (k >> 15);
   uint32_t y = ((uint32_t)((o >> 1) & 1) << 6) | ((k >> 8) & 63);
   uint32_t z = ((uint32_t)(o >> 2) << 6) | ((k & 127) >> 1);
   return (x << 14) | (y << 7) | z;
+}
+
+// floor((2 s + n) / (2 n)) -- round half up (sampling.py:96) -- without a 64-bit divide:
+// a float quotient is within one of the result, an integer check fixes it.
+__device__ __forceinline__ uint32_t mean_round(uint64_t s, uint64_t n) {
+  uint64_t a = 2 * s + n, b = 2 * n;
+  uint32_t q = (uint32_t)__fdividef((float)a, (float)b);
+  if ((uint64_t)q * b > a) --q;
+  else if ((uint64_t)(q + 1) * b <= a) ++q;
+  return q;
 }
 
 __device__ __forceinline__ uint32_t rank_in(const VoxSmem* s, uint32_t k20) {
@@ -95,16 +85,31 @@ __device__ __forceinline__ uint32_t rank_in(const VoxSmem* s, uint32_t k20) {
   return s->super[w >> kSuperShift] + s->rel[w] + __popc(s->bits[w] & ((1u << b) - 1));
 }
 
-// Visit this CTA's samples: fn(ordinal, octant, j)
+// Visit this CTA's samples: fn(ordinal, key in this node's grid, rgb).  Leaf children
+// come from the distribute stash (key already in this grid), inner children from the
+// voxel arena.  Four independent loads per thread per trip keep enough bytes in flight.
 template <class Fn>
-__device__ __forceinline__ void for_my_samples(const VoxSmem& s, Fn fn) {
-  const uint32_t total = s.mine_pre[s.n_mine];
-  for (uint32_t idx = threadIdx.x; idx < total; idx += kVT) {
-    uint32_t c = 0;
-    while (idx >= s.mine_pre[c + 1]) ++c;
-    int o = (int)s.mine[c];
-    uint32_t j = idx - s.mine_pre[c];
-    fn(s.cbase[o] + j, o, j);
+__device__ __forceinline__ void for_my_samples(const VoxView& v, const VoxSmem& s, Fn fn) {
+  constexpr int U = 4;
+  for (uint32_t c = 0; c < s.n_mine; ++c) {
+    const int o = (int)s.mine[c];
+    const uint32_t cnt = s.ccount[o];
+    const bool leaf = s.ckind[o] == 1;
+    const uint2* src = (leaf ? v.stash : v.vox) + s.cfirst[o];
+    const uint32_t ob = s.cbase[o];
+    for (uint32_t j0 = threadIdx.x; j0 < cnt; j0 += U * kVT) {
+      uint2 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t j = j0 + u * kVT;
+        if (j < cnt) r[u] = __ldg(src + j);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        uint32_t j = j0 + u * kVT;
+        if (j < cnt) fn(ob + j, leaf ? r[u].x : voxel_to_parent(o, r[u].x), r[u].y);
+      }
+    }
   }
 }
 
@@ -189,12 +194,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kVT, 1) k_voxelize(V
     }
 
     // ---- pass A: occupancy ----
-    for_my_samples(s, [&](uint32_t, int o, uint32_t j) {
-      uint32_t rgb;
-      uint32_t key = sample_key<FMT>(v, s, o, j, rgb);
+    for_my_samples(v, s, [&](uint32_t, uint32_t key, uint32_t) {
       uint32_t w = (key & 0xFFFFF) >> 5, bit = 1u << (key & 31);
       uint32_t* dst = ((key >> 20) == h) ? s.bits : peer->bits;
-      atomicOr(dst + w, bit);
+      if (!(dst[w] & bit)) atomicOr(dst + w, bit);  // most samples land in an occupied cell
     });
     cluster.sync();
 
@@ -270,18 +273,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kVT, 1) k_voxelize(V
     if (MODE == LOD_MODE_RANDOM) {
       // ---- pass B: max (rand12 | ordinal20) per voxel ----
       const uint64_t hs = s.hash;
-      for_my_samples(s, [&](uint32_t ord, int o, uint32_t j) {
-        uint32_t rgb;
-        uint32_t key = sample_key<FMT>(v, s, o, j, rgb);
+      for_my_samples(v, s, [&](uint32_t ord, uint32_t key, uint32_t) {
         uint32_t enc = ((uint32_t)(mix64(hs ^ (uint64_t)ord) >> 32) & 0xFFF00000u) | (ord & 0xFFFFFu);
         atomicMax(acc32 + global_rank(key), enc);
       });
       __threadfence();
       cluster.sync();
       // ---- pass C: the winning sample writes its colour ----
-      for_my_samples(s, [&](uint32_t ord, int o, uint32_t j) {
-        uint32_t rgb;
-        uint32_t key = sample_key<FMT>(v, s, o, j, rgb);
+      for_my_samples(v, s, [&](uint32_t ord, uint32_t key, uint32_t rgb) {
         uint32_t enc = ((uint32_t)(mix64(hs ^ (uint64_t)ord) >> 32) & 0xFFF00000u) | (ord & 0xFFFFFu);
         uint32_t r = global_rank(key);
         if (__ldcg(acc32 + r) == enc) v.vox[vbase + r].y = rgb;
@@ -290,9 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kVT, 1) k_voxelize(V
       const int passes = wide ? 3 : 1;
       for (int p = 0; p < passes; ++p) {
         // ---- pass B: exact integer sums + counts ----
-        for_my_samples(s, [&](uint32_t, int o, uint32_t j) {
-          uint32_t rgb;
-          uint32_t key = sample_key<FMT>(v, s, o, j, rgb);
+        for_my_samples(v, s, [&](uint32_t, uint32_t key, uint32_t rgb) {
           uint32_t r = global_rank(key);
           if (!wide) {
             atomicAdd((unsigned long long*)(acc + 2ull * r),
@@ -313,13 +310,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kVT, 1) k_voxelize(V
           uint64_t a = __ldcg(acc + 2ull * r), b = __ldcg(acc + 2ull * r + 1);
           if (!wide) {
             uint64_t n = b >> 32;
-            uint64_t cr = (2 * (a & 0xFFFFFFFFull) + n) / (2 * n);
-            uint64_t cgc = (2 * (a >> 32) + n) / (2 * n);
-            uint64_t cb = (2 * (b & 0xFFFFFFFFull) + n) / (2 * n);
-            v.vox[vbase + r].y = (uint32_t)(cr | (cgc << 8) | (cb << 16));
+            v.vox[vbase + r].y = mean_round(a & 0xFFFFFFFFull, n) | (mean_round(a >> 32, n) << 8) |
+                                 (mean_round(b & 0xFFFFFFFFull, n) << 16);
           } else {
-            uint64_t c = (2 * a + b) / (2 * b);
-            v.vox[vbase + r].y |= (uint32_t)c << (8 * p);
+            v.vox[vbase + r].y |= mean_round(a, b) << (8 * p);
             acc[2ull * r] = 0;
             acc[2ull * r + 1] = 0;
           }
