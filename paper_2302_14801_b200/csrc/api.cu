@@ -91,6 +91,7 @@ struct lod_tree {
   DevBuf leaf_node, leaf_first, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
   DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf;
   DevBuf vox, scratch, export_buf, stash;
+  DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vleaf_chunks, vvchunks;
   DevState* host_state = nullptr;  // pinned mirror
 
   uint32_t n_nodes = 0, n_leaves = 0, n_ext = 0, max_depth_used = 0;
@@ -99,6 +100,7 @@ struct lod_tree {
   std::vector<Round> rounds;
   uint64_t total_slots = 0;
   double world[4] = {};
+  double inv_world = 0;
   RadixPlan plan{};
   uint32_t epoch = 1;
 };
@@ -445,8 +447,7 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
     p.tmp_rec = t->tmp_rec.p;
     p.tmp_leaf = t->tmp_leaf.as<uint32_t>();
     p.epoch = t->epoch;
-    CK(ensure(t->stash, n * 8));
-    p.stash = t->stash.as<uint2>();
+
   }
   v = make_view(t, pts);
   RUN(launch_distribute(fmt, v, p, t->leaf_pts.p, s));
@@ -457,6 +458,7 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   if (t->host_state->count_b != n) return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
   for (int a = 0; a < 3; ++a) t->world[a] = t->host_state->lo[a];
   t->world[3] = t->host_state->size;
+  t->inv_world = t->host_state->inv_size;
   CK(cudaGetLastError());
   t->split_done = true;
   return LOD_OK;
@@ -470,7 +472,8 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
   t->voxel_mode = -1;
   t->n_voxels = 0;
   uint32_t inner_total = 0, widest = 0;
-  for (int d = 0; d <= kMaxDepth; ++d) inner_total += t->inner_per_depth[d], widest = std::max(widest, t->inner_per_depth[d]);
+  for (int d = 0; d <= kMaxDepth; ++d)
+    inner_total += t->inner_per_depth[d], widest = std::max(widest, t->inner_per_depth[d]);
   mark(t, 4, s);
   if (inner_total == 0) {  // single-leaf root: nothing to voxelize (test_sampling.py:163-166)
     t->voxel_mode = mode;
@@ -479,46 +482,80 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
-  const int n_clusters = (int)std::max<uint32_t>(1, std::min<uint32_t>(widest, (uint32_t)(sms / 2)));
-  const uint64_t slot_words = 2ull << 21;  // 2 u64 accumulators x up to 128^3 voxels
-  CK(ensure(t->scratch, (size_t)n_clusters * slot_words * 8));
+  const uint64_t kWordsPerNode = 1ull << 16;
+  CK(ensure(t->vbits, 2ull * widest * kWordsPerNode * 4));
+  CK(ensure(t->vpre, 2ull * widest * kWordsPerNode * 4));
+  CK(ensure(t->vinfo, 2ull * widest * sizeof(VoxNode)));
+  CK(ensure(t->vblk, (size_t)widest * 16 * 4));
+  CK(ensure(t->vcount, 64 * 4 * (kMaxDepth + 1)));
+  CK(ensure(t->vlevel_start, 8 * (kMaxDepth + 1)));
+  CK(ensure(t->node_slot, (size_t)t->n_nodes * 4));
   uint64_t cap = std::max<uint64_t>(t->n + t->n / 2, 1ull << 21);
   if (t->vox.cap / 8 > cap) cap = t->vox.cap / 8;
-  for (int attempt = 0; attempt < 6; ++attempt) {
+  uint64_t acc_cap = std::max<uint64_t>(t->n / 2, 1ull << 21);
+  if (t->vacc.cap / 16 > acc_cap) acc_cap = t->vacc.cap / 16;
+  for (int attempt = 0; attempt < 8; ++attempt) {
     CK(ensure(t->vox, cap * 8));
     cap = t->vox.cap / 8;
+    CK(ensure(t->vacc, acc_cap * 16));
+    acc_cap = t->vacc.cap / 16;
+    const uint64_t chunk_cap = voxelize_chunk_capacity(t->n + cap, widest);
+    const uint64_t vchunk_cap = voxelize_vchunk_capacity(cap, widest);
+    CK(ensure(t->vchunks, chunk_cap * 16));
+    CK(ensure(t->vleaf_chunks, chunk_cap * 16));
+    CK(ensure(t->vvchunks, vchunk_cap * 8));
     CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
                        sizeof(DevState) - offsetof(DevState, err), s));
-    VoxView vv{};
-    vv.st = t->state.as<DevState>();
-    vv.fmt = t->fmt;
-    vv.leaf_pts = t->leaf_pts.p;
-    vv.stash = t->stash.as<uint2>();
-    vv.n_cell = t->n_cell.as<uint64_t>();
-    vv.n_child = t->n_child.as<int32_t>();
-    vv.n_box = t->n_box.as<double4>();
-    vv.n_leaf = t->n_leaf.as<int32_t>();
-    vv.n_first = t->n_first.as<uint64_t>();
-    vv.n_count = t->n_count.as<uint32_t>();
-    vv.vox = t->vox.as<uint2>();
-    vv.vox_cap = cap;
-    vv.scratch = t->scratch.as<uint64_t>();
-    vv.scratch_per_slot = slot_words;
-    vv.mode = mode;
-    vv.seed = seed;
+    CK(cudaMemsetAsync(t->vcount.p, 0, 64 * 4 * (kMaxDepth + 1), s));
+    VoxLevel L{};
+    L.st = t->state.as<DevState>();
+    CK(ensure(t->stash, t->n * 8));
+    L.stash = t->stash.as<uint2>();
+    L.fmt = t->fmt;
+    L.leaf_pts = t->leaf_pts.p;
+    L.n_box = t->n_box.as<double4>();
+    L.inv_world = t->inv_world;
+    L.n_cell = t->n_cell.as<uint64_t>();
+    L.n_child = t->n_child.as<int32_t>();
+    L.n_leaf = t->n_leaf.as<int32_t>();
+    L.n_first = t->n_first.as<uint64_t>();
+    L.n_count = t->n_count.as<uint32_t>();
+    L.node_slot = t->node_slot.as<uint32_t>();
+    L.slots = widest;
+    L.bits = t->vbits.as<uint32_t>();
+    L.pre = t->vpre.as<uint32_t>();
+    L.blk_sum = t->vblk.as<uint32_t>();
+    L.chunks = t->vchunks.as<uint4>();
+    L.leaf_chunks = t->vleaf_chunks.as<uint4>();
+    L.vchunks = t->vvchunks.as<uint2>();
+    L.vox = t->vox.as<uint2>();
+    L.vox_cap = cap;
+    L.acc = t->vacc.as<uint64_t>();
+    L.acc_cap = acc_cap;
+    L.mode = mode;
+    L.seed = seed;
     for (int d = kMaxDepth; d >= 0; --d) {  // deepest first (sampling.py:171)
       if (!t->inner_per_depth[d]) continue;
-      vv.depth = d;
-      vv.list = t->depth_lists.as<uint32_t>() + t->inner_off[d];
-      vv.list_n = t->inner_per_depth[d];
-      int nc = (int)std::min<uint32_t>(vv.list_n, (uint32_t)n_clusters);
-      RUN(launch_voxelize_level(vv, nc, s));
+      L.list = t->depth_lists.as<uint32_t>() + t->inner_off[d];
+      L.list_n = t->inner_per_depth[d];
+      L.parity = d & 1;
+      L.chunk = voxelize_chunk(L.list_n);
+      L.vchunk = voxelize_vchunk(L.list_n);
+      L.info = t->vinfo.as<VoxNode>() + (size_t)L.parity * widest;
+      L.cinfo = t->vinfo.as<VoxNode>() + (size_t)(L.parity ^ 1) * widest;
+      L.counters = t->vcount.as<uint32_t>() + 64 * d;
+      L.level_start = t->vlevel_start.as<uint64_t>() + d;
+      CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
+                         (size_t)L.list_n * kWordsPerNode * 4, s));
+      RUN(launch_voxelize_level(L, sms, s));
     }
     int r = read_state(t, s);
     if (r) return r;
     CK(cudaGetLastError());
     if ((t->host_state->err & ERR_ARENA) && !(t->host_state->err & ERR_RANDOM_LIMIT)) {
-      cap = std::max<uint64_t>(cap * 2, t->host_state->vox_cursor + (t->host_state->vox_cursor >> 2));
+      uint64_t need = t->host_state->err_value;
+      cap = std::max<uint64_t>(cap * 2, need + (need >> 2));
+      acc_cap = std::max<uint64_t>(acc_cap * 2, need / 2);
       continue;
     }
     if ((r = check_errors(t, s))) return r;
@@ -554,7 +591,8 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node, &t->leaf_first,
                    &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
                    &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf,
-                   &t->stash};
+                   &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
+                   &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -649,7 +687,9 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->n_lvl, &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node,
                          &t->leaf_first, &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists,
                          &t->leaf_pts, &t->status, &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf,
-                         &t->vox, &t->scratch, &t->export_buf, &t->stash};
+                         &t->vox, &t->scratch, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
+                         &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
+                         &t->vleaf_chunks, &t->vvchunks};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;

@@ -37,9 +37,9 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
 }
 
 template <int FMT, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kRadixThreads, 1)
+__global__ void __launch_bounds__(kRadixThreads, 2)
     k_radix(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
-            uint2* out_stash, int shift, int bits, const uint64_t* digit_base, uint64_t* status, uint32_t epoch,
+            int shift, int bits, const uint64_t* digit_base, uint64_t* status, uint32_t epoch,
             uint32_t* ticket) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int B = 1 << bits;
@@ -61,29 +61,53 @@ __global__ void __launch_bounds__(kRadixThreads, 1)
   uint32_t leaf[kRadixItems];
   uint16_t rk[kRadixItems];
 
-  // --- 1a. leaf ids (no shared memory here, so the record loads of all items overlap) ---
+  // --- 1a. leaf ids.  Straight-line batches (clamped indices, no per-item branches) so
+  //     the 16 record loads, then the 16 target-table loads, are all in flight together.
+  if (FIRST) {
+    uint32_t key[kRadixItems];
 #pragma unroll
-  for (int k = 0; k < kRadixItems; ++k) {
-    const uint64_t i = base + (uint64_t)k * 32 + lane;
-    uint32_t lf = 0;
-    if (i < v.n) {
-      if (FIRST) {
-        auto r = Rec<FMT>::load(in_rec, i);
+    for (int k0 = 0; k0 < kRadixItems; k0 += 8) {
+      typename Rec<FMT>::Raw r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint64_t i = base + (uint64_t)(k0 + u) * 32 + lane;
+        r[u] = Rec<FMT>::load(in_rec, i < v.n ? i : v.n - 1);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        Cell16 c;
+        c.x = quant16(Rec<FMT>::x(r[u]), lo0, size, inv, bad);
+        c.y = quant16(Rec<FMT>::y(r[u]), lo1, size, inv, bad);
+        c.z = quant16(Rec<FMT>::z(r[u]), lo2, size, inv, bad);
+        key[k0 + u] = (uint32_t)level_key(c, v.D);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kRadixItems; ++k) leaf[k] = (uint32_t)__ldg(v.t8 + key[k]);
+#pragma unroll
+    for (int k = 0; k < kRadixItems; ++k) {
+      int32_t t = (int32_t)leaf[k];
+      if (t <= -2) {  // inside an extension grid (rare): recompute the cell, descend
+        const uint64_t i = base + (uint64_t)k * 32 + lane;
+        const auto r = Rec<FMT>::load(in_rec, i < v.n ? i : v.n - 1);
         Cell16 c;
         c.x = quant16(Rec<FMT>::x(r), lo0, size, inv, bad);
         c.y = quant16(Rec<FMT>::y(r), lo1, size, inv, bad);
         c.z = quant16(Rec<FMT>::z(r), lo2, size, inv, bad);
-        int32_t t = leaf_of_point(v, c);
-        if (t < 0) {
-          unresolved = true;
-          t = 0;
-        }
-        lf = (uint32_t)t;
-      } else {
-        lf = __ldg(in_leaf + i);
+        t = leaf_of_point(v, c);
       }
+      if (t < 0) {
+        unresolved |= base + (uint64_t)k * 32 + lane < v.n;
+        t = 0;
+      }
+      leaf[k] = (uint32_t)t;
     }
-    leaf[k] = lf;
+  } else {
+#pragma unroll
+    for (int k = 0; k < kRadixItems; ++k) {
+      const uint64_t i = base + (uint64_t)k * 32 + lane;
+      leaf[k] = __ldg(in_leaf + (i < v.n ? i : v.n - 1));
+    }
   }
   // --- 1b. stable in-warp ranks (warp-major, round-major, lane order) ---
 #pragma unroll
@@ -94,7 +118,7 @@ __global__ void __launch_bounds__(kRadixThreads, 1)
     uint32_t rank = 0;
     if (valid) {
       const unsigned peers = __match_any_sync(act, d);
-      const int leader = __ffs(peers) - 1;
+      const int leader = 31 - __clz(peers & (0u - peers));  // lowest peer lane
       uint32_t old = 0;
       if (lane == leader) {
         old = wh[warp * B + d];
@@ -123,17 +147,28 @@ __global__ void __launch_bounds__(kRadixThreads, 1)
       st_relaxed(mine, pack_status(epoch, kFlagP, run));
     } else {
       st_relaxed(mine, pack_status(epoch, kFlagA, run));
+      // look back over up to 8 predecessors per trip (independent loads), summing
+      // aggregates until an inclusive prefix is found
       int64_t t = (int64_t)tile - 1;
-      while (true) {
-        uint64_t w = ld_relaxed(status + (uint64_t)t * B + d);
-        uint64_t flag = (w >> 46) & 3;
-        if ((uint32_t)(w >> 48) != (epoch & 0xFFFF) || flag == 0) {
-          __nanosleep(20);
-          continue;
+      bool done = false;
+      while (!done) {
+        uint64_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = t - q >= 0 ? ld_relaxed(status + (uint64_t)(t - q) * B + d) : 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (done || t - q < 0) break;
+          const uint64_t flag = (w[q] >> 46) & 3;
+          if ((uint32_t)(w[q] >> 48) != (epoch & 0xFFFF) || flag == 0) {  // not published yet
+            t -= q;
+            __nanosleep(20);
+            goto retry;
+          }
+          excl += w[q] & ((1ull << 46) - 1);
+          if (flag == kFlagP) done = true;
         }
-        excl += w & ((1ull << 46) - 1);
-        if (flag == kFlagP) break;
-        --t;
+        t -= 8;
+      retry:;
       }
       st_relaxed(mine, pack_status(epoch, kFlagP, excl + run));
     }
@@ -141,26 +176,25 @@ __global__ void __launch_bounds__(kRadixThreads, 1)
   }
   __syncthreads();
 
-  // --- 3. scatter (record re-read from L2); the last pass also writes each point's cell
-  //        in its leaf-parent's 128^3 grid (the voxelizer's sample stash) ---
+  // --- 3. scatter: records re-read from L2 (the tile was just read), batched so the loads
+  //        overlap; destinations of equal-digit runs are adjacent, so L2 merges the sectors ---
 #pragma unroll
-  for (int k = 0; k < kRadixItems; ++k) {
-    const uint64_t i = base + (uint64_t)k * 32 + lane;
-    if (i < v.n) {
-      const uint32_t d = (leaf[k] >> shift) & (B - 1);
-      const uint64_t dest = tbase[d] + wh[warp * B + d] + rk[k];
-      auto r = Rec<FMT>::load(in_rec, i);
-      Rec<FMT>::store(out_rec, dest, r);
-      if (!LAST) out_leaf[dest] = leaf[k];
-      if (LAST && out_stash) {
-        const double4 b = v.leaf_pbox[leaf[k]];
-        uint32_t key = 0;
-        if (b.w > 0) {
-          const double pinv = v.leaf_pinv[leaf[k]];
-          key = (grid_cell128(Rec<FMT>::x(r), b.x, b.w, pinv) << 14) |
-                (grid_cell128(Rec<FMT>::y(r), b.y, b.w, pinv) << 7) | grid_cell128(Rec<FMT>::z(r), b.z, b.w, pinv);
-        }
-        out_stash[dest] = make_uint2(key, Rec<FMT>::rgb(r));
+  for (int k0 = 0; k0 < kRadixItems; k0 += 4) {
+    typename Rec<FMT>::Raw r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i = base + (uint64_t)(k0 + u) * 32 + lane;
+      r[u] = Rec<FMT>::load(in_rec, i < v.n ? i : v.n - 1);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u;
+      const uint64_t i = base + (uint64_t)k * 32 + lane;
+      if (i < v.n) {
+        const uint32_t d = (leaf[k] >> shift) & (B - 1);
+        const uint64_t dest = tbase[d] + wh[warp * B + d] + rk[k];
+        Rec<FMT>::store(out_rec, dest, r[u]);
+        if (!LAST) out_leaf[dest] = leaf[k];
       }
     }
   }
@@ -191,11 +225,10 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
 template <int FMT, bool FIRST, bool LAST>
 void run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
               int shift, int bits, const uint64_t* digit_base, RadixPlan& p, uint32_t* ticket, cudaStream_t s) {
-  uint2* stash = LAST ? p.stash : nullptr;
   size_t smem = (size_t)kW * (1u << bits) * 2 + (size_t)(1u << bits) * 8;
   auto kern = k_radix<FMT, FIRST, LAST>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<p.tiles, kRadixThreads, smem, s>>>(v, in_rec, in_leaf, out_rec, out_leaf, stash, shift, bits, digit_base,
+  kern<<<p.tiles, kRadixThreads, smem, s>>>(v, in_rec, in_leaf, out_rec, out_leaf, shift, bits, digit_base,
                                             p.status, p.epoch, ticket);
 }
 

@@ -116,38 +116,66 @@ struct RadixPlan {
   uint32_t* tile_ticket;  // per pass
   void* tmp_rec;          // pass-0 output records (2 passes)
   uint32_t* tmp_leaf;     // pass-0 output leaf ids
-  uint2* stash;           // per leaf-buffer slot: {cell key in the leaf-parent's 128^3 grid, rgb}
 };
 constexpr int kRadixThreads = 512;
-constexpr int kRadixItems = 16;
+constexpr int kRadixItems = 8;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;
 constexpr int kRadixMaxBits = 11;
 int launch_distribute(int fmt, const SplitView& v, RadixPlan& plan, void* leaf_out, cudaStream_t s);
 
 // --- voxelize (voxelize.cu) ---
-struct VoxView {
+struct VoxNode {           // per inner node of the level being sampled (by list slot)
+  uint32_t node, S, m, skip;
+  uint64_t vbase, hash;    // first voxel in the arena; seed ^ path_hash(seed, path)
+  double4 box;             // node bounds (min xyz, size) for projecting leaf points
+  double inv;              // RN(1 / size)
+  uint64_t cfirst[8];      // child's first point (leaf) / first voxel (inner)
+  uint32_t cbase[8];       // ordinal of the child's first sample (octant order)
+  uint32_t ccount[8];
+  int32_t cslot[8];        // -2 absent, -1 leaf child, >= 0 slot of an inner child
+};
+
+struct VoxLevel {
   DevState* st;
   int fmt;
-  const void* leaf_pts;
-  const uint2* stash;     // leaf points as {key in the leaf-parent grid, rgb} (distribute output)
+  const void* leaf_pts;    // leaf buffer (input record format)
+  uint2* stash;            // per leaf point {key in the leaf-parent grid, rgb}, written by K1
   const uint64_t* n_cell;
   const int32_t* n_child;
-  const double4* n_box;
   const int32_t* n_leaf;
+  const double4* n_box;
+  double inv_world;        // RN(1 / world size)
   uint64_t* n_first;
   uint32_t* n_count;
-  const uint32_t* list;   // inner nodes of this depth
+  uint32_t* node_slot;     // node id -> slot in its level's list
+  const uint32_t* list;    // inner nodes of this depth
   uint32_t list_n;
-  uint32_t depth;
-  uint2* vox;             // arena
+  int parity;              // depth & 1: which bitmap/prefix/info buffers this level owns
+  uint32_t slots;          // slots per parity
+  uint32_t* bits;          // [2][slots][2^16] occupancy words
+  uint32_t* pre;           // [2][slots][2^16] exclusive popcount prefix per word
+  VoxNode* info;           // this level's infos (parity slice)
+  const VoxNode* cinfo;    // child level's infos (other parity slice)
+  uint32_t* blk_sum;       // [list_n * 16]
+  uint32_t* counters;      // [3]: sample chunks, leaf chunks, voxel chunks
+  uint4* chunks;
+  uint4* leaf_chunks;
+  uint2* vchunks;
+  uint64_t* level_start;   // arena cursor at the start of this level
+  uint2* vox;              // arena: {key, rgb}
   uint64_t vox_cap;
-  uint64_t* scratch;      // per-cluster accumulator slots
-  uint64_t scratch_per_slot;  // u64 words per cluster slot
+  uint64_t* acc;           // per voxel of this level: 2 u64 (average) or u32 (random)
+  uint64_t acc_cap;        // voxels
+  uint32_t chunk;          // samples per K1/K3 chunk
+  uint32_t vchunk;         // voxels per K4 chunk
   int mode;
   uint64_t seed;
 };
-int voxelize_smem_bytes();
-int launch_voxelize_level(const VoxView& v, int n_clusters, cudaStream_t s);
+int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s);
+uint32_t voxelize_chunk(uint32_t nodes);
+uint32_t voxelize_vchunk(uint32_t nodes);
+uint64_t voxelize_chunk_capacity(uint64_t samples, uint32_t nodes);
+uint64_t voxelize_vchunk_capacity(uint64_t voxels, uint32_t nodes);
 
 // --- generators (generate.cu) ---
 int launch_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, void* out, const double* table,

@@ -117,10 +117,14 @@ __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
       bool valid = i < v.n;
       uint32_t key = 0;
       if (valid) key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
-      unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
-      if (valid) {
-        unsigned peers = __match_any_sync(act, key);
-        if (lane == __ffs(peers) - 1) atomicAdd(grid + key, (uint32_t)__popc(peers));
+      // warp-uniform cell (coherent scans, dense clusters): one aggregated add;
+      // otherwise one fire-and-forget RED per point (MATCH would saturate the ADU pipe)
+      const uint32_t k0 = __shfl_sync(0xFFFFFFFFu, key, 0);
+      const unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
+      if (__all_sync(0xFFFFFFFFu, !valid || key == k0)) {
+        if (lane == 0 && act) atomicAdd(grid + k0, (uint32_t)__popc(act));
+      } else if (valid) {
+        atomicAdd(grid + key, 1u);
       }
     }
   }

@@ -1,58 +1,42 @@
-// Voxel sampling of inner nodes, one launch per octree depth, deepest first
+// Voxel sampling of inner nodes, one level at a time, deepest first
 // (reference sampling.py:165-176 build_lod; per node sampling.py:21-97).
 //
-// One 2-CTA cluster per node (persistent clusters pull node tickets).  The node's 128^3
-// sampling grid is an occupancy BITMAP split by the x-high bit across the pair's shared
-// memory (2 x 128 KB, DSMEM for the rare cross-half sample).  Because keys are x-major,
-// every key of half 0 precedes every key of half 1, so
-//     voxel index of key = rank(key) = #occupied keys < key
-// is a local prefix-popcount lookup (+ half 0's total for half 1).  Voxels therefore come
-// out in ascending key order (sampling.py:83-85, 97) with no sort, and the per-voxel
-// accumulators are compact (m entries, L2-resident) instead of a 128^3 dense grid.
+// Level-wide data parallel design (every SM works on every level, however few nodes it has):
 //
-//   pass A  samples -> atomicOr occupancy bits
-//   rank    per-word prefix popcounts (u16 within 64-word superblocks + u32 superblock base)
-//   emit    voxel keys in rank order, accumulators zeroed
-//   pass B  average: exact integer channel sums + counts (sampling.py:88-97)
-//           random : atomicMax of (rand12 | ordinal20) (sampling.py:69-85, PAPER Listing 1)
-//   final   average: (2*sum + n) / (2*n) per channel; random: winner's colour (pass C)
+//   per inner node at this depth, an occupancy BITMAP of its 128^3 grid (2^21 bits, 256 KB)
+//   plus a per-word exclusive popcount PREFIX (256 KB) live in HBM/L2.  Because keys are
+//   x-major, the voxel index of a key is its rank among occupied keys:
+//       rank(key) = prefix[key >> 5] + popc(bits[key >> 5] & ((1 << (key & 31)) - 1))
+//   so voxels come out in ascending key order (sampling.py:83-85, 97) with no sort.
 //
-// CTA h of the pair processes the children whose octant has x-bit h: voxel children map
-// into half h exactly, leaf children except at the boundary, so DSMEM traffic is rare.
-#include <cooperative_groups.h>
-
+//   K0 setup     one thread per node: children, ordinals, sample chunks (sampling.py:21-47)
+//   K1 occupy    all samples, test-and-set their bit (L2 atomics only on first touch)
+//   K2 words     per 4096-word block: popcount sums; node offsets; prefix + key emission
+//   K3 scatter   LEAF-point samples only: integer channel sums + counts (average,
+//                sampling.py:88-97) or atomicMax of (rand12 | ordinal20) (random,
+//                sampling.py:69-85 / PAPER Listing 1)
+//   K4 finalize  per voxel.  A voxel in an octant whose child is an inner node takes its
+//                samples from that child's 2x2x2 block of voxels (off + c/2, sampling.py:
+//                41-44): they are GATHERED through the child's kept bitmap + prefix, so
+//                voxel children need no atomics at all; leaf-point contributions (incl.
+//                the rare boundary spill into a neighbouring octant) come from K3.
+//   Average: (2*sum + n) // (2*n) per channel over the children's ROUNDED colours (H5).
+//   Random : max (rand12 | ordinal20); the winning ordinal names the sample directly.
+//
+// Bitmaps/prefixes of a level are kept until the next (coarser) level has gathered from
+// them: two buffers alternate by depth parity.
 #include "kernels.h"
-
-namespace cg = cooperative_groups;
 
 namespace lod {
 
 namespace {
 
-constexpr int kVT = 1024;
-constexpr int kHalfWords = 1 << 15;  // 2^20 cells per half / 32
-constexpr int kSuperShift = 6;       // 64 words per superblock
-constexpr int kNumSuper = kHalfWords >> kSuperShift;
-constexpr uint32_t kWideS = 1u << 24;  // below this, 32-bit channel sums cannot overflow
-
-struct __align__(16) VoxSmem {
-  uint32_t bits[kHalfWords];
-  uint16_t rel[kHalfWords];
-  uint32_t super[kNumSuper];
-  uint64_t cfirst[8];
-  uint32_t ccount[8];
-  uint32_t cbase[8];   // ordinal of the child's first sample (octant order over ALL children)
-  int32_t ckind[8];    // 1 leaf, 0 inner, -1 absent
-  uint32_t mine[4];    // octants processed by this CTA
-  uint32_t mine_pre[5];
-  double lo[3];
-  double size;
-  unsigned long long hash;
-  unsigned long long vbase;
-  uint32_t node, S, total, peer_total, ticket, n_mine;
-  int skip;
-  uint32_t scan[kVT / 32 + 1];
-};
+constexpr uint32_t kWords = 1u << 16;        // 2^21 cells / 32
+constexpr uint32_t kBlkWords = 4096;         // words per K2 block
+constexpr uint32_t kBlksPerNode = kWords / kBlkWords;
+constexpr uint32_t kChunk = 8192;            // samples per K1/K3 chunk
+constexpr uint32_t kVoxChunk = 2048;         // voxels per K4 chunk
+constexpr int kT = 256;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -61,8 +45,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-// child voxel key c in octant o -> parent key floor(off + (c + 0.5) / 2) = off + c / 2
-// (sampling.py:41-44)
+// child voxel key c in octant o -> parent key off + c / 2 (floor(off + (c + 0.5) / 2))
 __device__ __forceinline__ uint32_t voxel_to_parent(int o, uint32_t k) {
   uint32_t x = ((uint32_t)(o & 1) << 6) | (k >> 15);
   uint32_t y = ((uint32_t)((o >> 1) & 1) << 6) | ((k >> 8) & 63);
@@ -70,8 +53,7 @@ __device__ __forceinline__ uint32_t voxel_to_parent(int o, uint32_t k) {
   return (x << 14) | (y << 7) | z;
 }
 
-// floor((2 s + n) / (2 n)) -- round half up (sampling.py:96) -- without a 64-bit divide:
-// a float quotient is within one of the result, an integer check fixes it.
+// floor((2 s + n) / (2 n)): round half up (sampling.py:96) without a 64-bit divide
 __device__ __forceinline__ uint32_t mean_round(uint64_t s, uint64_t n) {
   uint64_t a = 2 * s + n, b = 2 * n;
   uint32_t q = (uint32_t)__fdividef((float)a, (float)b);
@@ -80,281 +62,401 @@ __device__ __forceinline__ uint32_t mean_round(uint64_t s, uint64_t n) {
   return q;
 }
 
-__device__ __forceinline__ uint32_t rank_in(const VoxSmem* s, uint32_t k20) {
-  uint32_t w = k20 >> 5, b = k20 & 31;
-  return s->super[w >> kSuperShift] + s->rel[w] + __popc(s->bits[w] & ((1u << b) - 1));
+__device__ __forceinline__ uint32_t rand_enc(uint64_t hash, uint32_t ord) {
+  return ((uint32_t)(mix64(hash ^ (uint64_t)ord) >> 32) & 0xFFF00000u) | (ord & 0xFFFFFu);
 }
 
-// Visit this CTA's samples: fn(ordinal, key in this node's grid, rgb).  Leaf children
-// come from the distribute stash (key already in this grid), inner children from the
-// voxel arena.  Four independent loads per thread per trip keep enough bytes in flight.
-template <class Fn>
-__device__ __forceinline__ void for_my_samples(const VoxView& v, const VoxSmem& s, Fn fn) {
-  constexpr int U = 4;
-  for (uint32_t c = 0; c < s.n_mine; ++c) {
-    const int o = (int)s.mine[c];
-    const uint32_t cnt = s.ccount[o];
-    const bool leaf = s.ckind[o] == 1;
-    const uint2* src = (leaf ? v.stash : v.vox) + s.cfirst[o];
-    const uint32_t ob = s.cbase[o];
-    for (uint32_t j0 = threadIdx.x; j0 < cnt; j0 += U * kVT) {
+__device__ __forceinline__ uint32_t* bits_of(const VoxLevel& L, int parity, uint32_t slot) {
+  return L.bits + ((uint64_t)parity * L.slots + slot) * kWords;
+}
+__device__ __forceinline__ uint32_t* pre_of(const VoxLevel& L, int parity, uint32_t slot) {
+  return L.pre + ((uint64_t)parity * L.slots + slot) * kWords;
+}
+
+// ---------------------------------------------------------------------------
+// K0: per-node setup
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= L.list_n || (L.st->err & ERR_ARENA)) return;
+  const uint32_t node = L.list[s];
+  VoxNode info;
+  uint32_t ord = 0;
+  bool empty = false;
+  for (int o = 0; o < 8; ++o) {
+    int32_t c = L.n_child[8ull * node + o];
+    info.cbase[o] = ord;
+    info.ccount[o] = 0;
+    info.cfirst[o] = 0;
+    info.cslot[o] = -2;  // absent
+    if (c < 0) continue;
+    bool leaf = L.n_leaf[c] >= 0;
+    uint32_t cnt = L.n_count[c];
+    info.ccount[o] = cnt;
+    info.cfirst[o] = L.n_first[c];
+    info.cslot[o] = leaf ? -1 : (int32_t)L.node_slot[c];
+    empty |= cnt == 0;
+    ord += cnt;
+  }
+  info.S = ord;
+  info.node = node;
+  // path_hash(seed, path): key = mix64(8 key + octant + 1) per digit (rng.py:48-53)
+  uint64_t cell = L.n_cell[node];
+  uint32_t cx = (uint32_t)cell & 0xFFFF, cy = (uint32_t)(cell >> 16) & 0xFFFF, cz = (uint32_t)(cell >> 32) & 0xFFFF;
+  int depth = (int)(cell >> 48) & 0xFF;
+  uint64_t key = L.seed;
+  for (int b = depth - 1; b >= 0; --b) {
+    uint32_t oc = ((cx >> b) & 1) | (((cy >> b) & 1) << 1) | (((cz >> b) & 1) << 2);
+    key = mix64(key * 8 + oc + 1);
+  }
+  info.hash = L.seed ^ key;
+  info.box = L.n_box[node];
+  info.inv = __dmul_rn(L.inv_world, (double)(1ull << depth));
+  info.vbase = 0;
+  info.m = 0;
+  L.node_slot[node] = s;
+  bool skip = false;
+  if (empty) {
+    skip = true;
+    raise_err(L.st, ERR_EMPTY_CHILD, node);
+  } else if (L.mode == LOD_MODE_RANDOM && ord >= (uint32_t)kRandomLimit) {
+    skip = true;
+    raise_err(L.st, ERR_RANDOM_LIMIT, node, ord);
+  }
+  info.skip = skip;
+  L.info[s] = info;
+  if (skip) return;
+  // chunks of one node are contiguous in the lists: blocks walking the lists in order keep
+  // only a few nodes' bitmaps, prefixes and accumulators live in L2 at any time
+  const uint32_t chunk = L.chunk;
+  uint32_t tot = 0, ltot = 0;
+  for (int o = 0; o < 8; ++o) {
+    uint32_t nch = (info.ccount[o] + chunk - 1) / chunk;
+    tot += nch;
+    if (info.cslot[o] == -1) ltot += nch;
+  }
+  uint32_t at = atomicAdd(L.counters + 0, tot);
+  uint32_t lat = ltot ? atomicAdd(L.counters + 1, ltot) : 0;
+  for (int o = 0; o < 8; ++o) {
+    const uint32_t cnt = info.ccount[o];
+    const bool leaf = info.cslot[o] == -1;
+    for (uint32_t j = 0; j < cnt; j += chunk) {
+      uint4 ch = make_uint4(s, (uint32_t)o, j, min(cnt, j + chunk));
+      L.chunks[at++] = ch;
+      if (leaf) L.leaf_chunks[lat++] = ch;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: occupancy (test before set: most samples land in an already occupied cell).
+// Leaf points are projected here, once, into the node's grid (sampling.py:29-38) and
+// stashed as {key, rgb} for K3/K4, so the record is read a single time per level.
+// ---------------------------------------------------------------------------
+template <int FMT>
+__global__ void __launch_bounds__(kT) k_occupy(VoxLevel L) {
+  if (L.st->err & ERR_ARENA) return;
+  const uint32_t nch = L.counters[0];
+  constexpr int U = 8;
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint4 ch = L.chunks[c];
+    const VoxNode& nd = L.info[ch.x];
+    uint32_t* bits = bits_of(L, L.parity, ch.x);
+    const int o = (int)ch.y;
+    const uint64_t first = nd.cfirst[o];
+    if (nd.cslot[o] == -1) {
+      const double4 b = nd.box;
+      const double inv = nd.inv;
+      for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kT) {
+        typename Rec<FMT>::Raw r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint32_t j = min(j0 + u * kT, ch.w - 1);
+          r[u] = Rec<FMT>::load(L.leaf_pts, first + j);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint32_t j = j0 + u * kT;
+          if (j >= ch.w) continue;
+          const uint32_t key = (grid_cell128(Rec<FMT>::x(r[u]), b.x, b.w, inv) << 14) |
+                               (grid_cell128(Rec<FMT>::y(r[u]), b.y, b.w, inv) << 7) |
+                               grid_cell128(Rec<FMT>::z(r[u]), b.z, b.w, inv);
+          L.stash[first + j] = make_uint2(key, Rec<FMT>::rgb(r[u]));
+          uint32_t w = key >> 5, bit = 1u << (key & 31);
+          if (!(__ldcg(bits + w) & bit)) atomicOr(bits + w, bit);
+        }
+      }
+    } else {
+      const uint2* src = L.vox + first;
+      for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kT) {
+        uint32_t k[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) k[u] = __ldg(&src[min(j0 + u * kT, ch.w - 1)].x);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (j0 + u * kT >= ch.w) continue;
+          const uint32_t key = voxel_to_parent(o, k[u]);
+          uint32_t w = key >> 5, bit = 1u << (key & 31);
+          if (!(__ldcg(bits + w) & bit)) atomicOr(bits + w, bit);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: popcount sums per 4096-word block, node offsets, prefix + key emission
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_block_sums(VoxLevel L) {
+  const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
+  __shared__ uint32_t red[kT / 32];
+  uint32_t c = 0;
+  if (!L.info[s].skip && !(L.st->err & ERR_ARENA)) {
+    const uint4* b = reinterpret_cast<const uint4*>(bits_of(L, L.parity, s) + blk * kBlkWords);
+    for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT) {
+      uint4 q = __ldcg(b + i);
+      c += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kT / 32; ++w) t += red[w];
+    L.blk_sum[blockIdx.x] = t;
+  }
+}
+
+// one block: per-node voxel counts -> arena offsets (bump pointer), K4 voxel chunks
+__global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
+  if (L.st->err & ERR_ARENA) return;
+  __shared__ uint64_t sm[1024 / 32 + 1];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) {
+    carry = L.st->vox_cursor;
+    L.level_start[0] = carry;
+  }
+  __syncthreads();
+  for (uint32_t s0 = 0; s0 < L.list_n; s0 += 1024) {
+    const uint32_t s = s0 + threadIdx.x;
+    uint32_t m = 0;
+    if (s < L.list_n) {
+      uint32_t run = 0;
+      for (uint32_t b = 0; b < kBlksPerNode; ++b) {
+        uint32_t v = L.blk_sum[s * kBlksPerNode + b];
+        L.blk_sum[s * kBlksPerNode + b] = run;  // becomes the block's exclusive prefix
+        run += v;
+      }
+      m = run;
+    }
+    uint64_t tot;
+    uint64_t ex = block_excl_scan<uint64_t, 1024>(m, &tot, sm);
+    if (s < L.list_n) {
+      VoxNode& nd = L.info[s];
+      uint64_t vb = carry + ex;
+      nd.vbase = vb;
+      nd.m = m;
+      L.n_first[nd.node] = vb;
+      L.n_count[nd.node] = m;
+      uint32_t nv = (m + L.vchunk - 1) / L.vchunk;
+      uint32_t at = atomicAdd(L.counters + 2, nv);
+      for (uint32_t q = 0; q < nv; ++q) L.vchunks[at + q] = make_uint2(s, q * L.vchunk);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (carry > L.vox_cap || carry - L.level_start[0] > L.acc_cap) raise_err(L.st, ERR_ARENA, 0, carry);
+    L.st->vox_cursor = carry;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_prefix_emit(VoxLevel L) {
+  const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
+  const VoxNode& nd = L.info[s];
+  if (nd.skip || L.st->err & ERR_ARENA) return;
+  __shared__ uint32_t sm[kT / 32 + 1];
+  __shared__ __align__(16) uint32_t sbits[kBlkWords];
+  __shared__ __align__(16) uint32_t spre[kBlkWords];
+  const uint32_t* bits = bits_of(L, L.parity, s) + blk * kBlkWords;
+  uint32_t* pre = pre_of(L, L.parity, s) + blk * kBlkWords;
+  // coalesced stage of the block's words
+  for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT)
+    reinterpret_cast<uint4*>(sbits)[i] = __ldcg(reinterpret_cast<const uint4*>(bits) + i);
+  __syncthreads();
+  // prefix over 16 consecutive words per thread
+  constexpr uint32_t per = kBlkWords / kT;
+  uint32_t c = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < per; ++q) c += __popc(sbits[threadIdx.x * per + ((q + threadIdx.x) & (per - 1))]);
+  uint32_t tot;
+  uint32_t r = block_excl_scan<uint32_t, kT>(c, &tot, sm) + L.blk_sum[blockIdx.x];
+#pragma unroll
+  for (uint32_t q = 0; q < per; ++q) {
+    spre[threadIdx.x * per + q] = r;
+    r += __popc(sbits[threadIdx.x * per + q]);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT)
+    reinterpret_cast<uint4*>(pre)[i] = reinterpret_cast<const uint4*>(spre)[i];
+  // emission: lanes own consecutive words, so their voxel ranks are adjacent
+  const uint64_t acc0 = nd.vbase - L.level_start[0];
+  for (uint32_t wi = threadIdx.x; wi < kBlkWords; wi += kT) {
+    uint32_t bw = sbits[wi];
+    uint32_t rr = spre[wi];
+    const uint32_t key0 = (blk * kBlkWords + wi) << 5;
+    while (bw) {
+      uint32_t bit = __ffs(bw) - 1;
+      bw &= bw - 1;
+      L.vox[nd.vbase + rr] = make_uint2(key0 + bit, 0);
+      if (L.mode == LOD_MODE_AVERAGE)
+        reinterpret_cast<ulonglong2*>(L.acc)[acc0 + rr] = make_ulonglong2(0, 0);
+      else
+        reinterpret_cast<uint32_t*>(L.acc)[acc0 + rr] = 0;
+      ++rr;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t rank_of(const uint32_t* bits, const uint32_t* pre, uint32_t key) {
+  const uint32_t w = key >> 5;
+  return __ldcg(pre + w) + __popc(__ldcg(bits + w) & ((1u << (key & 31)) - 1));
+}
+
+// ---------------------------------------------------------------------------
+// K3: leaf-point samples -> accumulators
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_scatter(VoxLevel L) {
+  if (L.st->err & ERR_ARENA) return;
+  const uint32_t nch = L.counters[1];
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint4 ch = L.leaf_chunks[c];
+    const VoxNode& nd = L.info[ch.x];
+    const uint32_t* bits = bits_of(L, L.parity, ch.x);
+    const uint32_t* pre = pre_of(L, L.parity, ch.x);
+    const uint64_t acc0 = nd.vbase - L.level_start[0];
+    const int o = (int)ch.y;
+    const uint2* src = L.stash + nd.cfirst[o];
+    const uint32_t ob = nd.cbase[o];
+    constexpr int U = 4;
+    for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kT) {
       uint2 r[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        uint32_t j = j0 + u * kVT;
-        if (j < cnt) r[u] = __ldg(src + j);
+        uint32_t j = j0 + u * kT;
+        if (j < ch.w) r[u] = __ldg(src + j);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        uint32_t j = j0 + u * kVT;
-        if (j < cnt) fn(ob + j, leaf ? r[u].x : voxel_to_parent(o, r[u].x), r[u].y);
-      }
-    }
-  }
-}
-
-template <int FMT, int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kVT, 1) k_voxelize(VoxView v) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  VoxSmem& s = *reinterpret_cast<VoxSmem*>(smem_raw);
-  cg::cluster_group cluster = cg::this_cluster();
-  const uint32_t h = cluster.block_rank();
-  VoxSmem* peer = cluster.map_shared_rank(&s, (int)(h ^ 1));
-  const int tid = threadIdx.x;
-  uint64_t* acc = v.scratch + (uint64_t)(blockIdx.x >> 1) * v.scratch_per_slot;
-  uint32_t* acc32 = reinterpret_cast<uint32_t*>(acc);
-
-  while (true) {
-    if (h == 0 && tid == 0) {
-      uint32_t t = atomicAdd(&v.st->work[v.depth], 1u);
-      s.ticket = t;
-      peer->ticket = t;
-    }
-    cluster.sync();
-    if (s.ticket >= v.list_n) break;
-
-    // ---- node setup (both CTAs read the same global state) ----
-    if (tid == 0) {
-      uint32_t node = v.list[s.ticket];
-      s.node = node;
-      double4 b = v.n_box[node];
-      s.lo[0] = b.x, s.lo[1] = b.y, s.lo[2] = b.z, s.size = b.w;
-      uint32_t ord = 0, nm = 0;
-      int empty = 0;
-      s.mine_pre[0] = 0;
-      for (int o = 0; o < 8; ++o) {
-        int32_t c = v.n_child[8ull * node + o];
-        s.cbase[o] = ord;
-        if (c < 0) {
-          s.ckind[o] = -1;
-          s.ccount[o] = 0;
-          continue;
-        }
-        s.ckind[o] = v.n_leaf[c] >= 0 ? 1 : 0;
-        s.ccount[o] = v.n_count[c];
-        s.cfirst[o] = v.n_first[c];
-        empty |= v.n_count[c] == 0;
-        ord += v.n_count[c];
-        if ((uint32_t)(o & 1) == h) {
-          s.mine[nm] = o;
-          s.mine_pre[nm + 1] = s.mine_pre[nm] + v.n_count[c];
-          ++nm;
-        }
-      }
-      s.n_mine = nm;
-      s.S = ord;
-      // path_hash(seed, path): key = mix64(8 key + octant + 1) per digit (rng.py:48-53)
-      uint64_t cell = v.n_cell[node];
-      uint32_t cx = (uint32_t)cell & 0xFFFF, cy = (uint32_t)(cell >> 16) & 0xFFFF, cz = (uint32_t)(cell >> 32) & 0xFFFF;
-      int depth = (int)(cell >> 48) & 0xFF;
-      uint64_t key = v.seed;
-      for (int b2 = depth - 1; b2 >= 0; --b2) {
-        uint32_t oc = ((cx >> b2) & 1) | (((cy >> b2) & 1) << 1) | (((cz >> b2) & 1) << 2);
-        key = mix64(key * 8 + oc + 1);
-      }
-      s.hash = v.seed ^ key;
-      int skip = 0;
-      if (empty) {
-        skip = 1;
-        if (h == 0) raise_err(v.st, ERR_EMPTY_CHILD, node);
-      } else if (MODE == LOD_MODE_RANDOM && ord >= (uint32_t)kRandomLimit) {
-        skip = 1;
-        if (h == 0) raise_err(v.st, ERR_RANDOM_LIMIT, node, ord);
-      }
-      s.skip = skip;
-    }
-    for (int w = tid; w < kHalfWords; w += kVT) s.bits[w] = 0;
-    cluster.sync();  // both halves cleared before any cross-half OR
-    if (s.skip) {
-      if (h == 0 && tid == 0) {
-        v.n_count[s.node] = 0;
-        v.n_first[s.node] = 0;
-      }
-      continue;  // the loop-top cluster.sync keeps the pair in step
-    }
-
-    // ---- pass A: occupancy ----
-    for_my_samples(v, s, [&](uint32_t, uint32_t key, uint32_t) {
-      uint32_t w = (key & 0xFFFFF) >> 5, bit = 1u << (key & 31);
-      uint32_t* dst = ((key >> 20) == h) ? s.bits : peer->bits;
-      if (!(dst[w] & bit)) atomicOr(dst + w, bit);  // most samples land in an occupied cell
-    });
-    cluster.sync();
-
-    // ---- rank structure over this half ----
-    {
-      const int warp = tid >> 5, lane = tid & 31;
-      for (int sb = warp; sb < kNumSuper; sb += kVT / 32) {
-        int w0 = (sb << kSuperShift) + 2 * lane;
-        uint32_t c0 = __popc(s.bits[w0]), c1 = __popc(s.bits[w0 + 1]);
-        uint32_t incl = warp_incl_scan(c0 + c1);
-        s.rel[w0] = (uint16_t)(incl - c0 - c1);
-        s.rel[w0 + 1] = (uint16_t)(incl - c1);
-        if (lane == 31) s.super[sb] = incl;
-      }
-      __syncthreads();
-      uint32_t val = tid < kNumSuper ? s.super[tid] : 0;
-      uint32_t tot;
-      uint32_t ex = block_excl_scan<uint32_t, kVT>(val, &tot, s.scan);
-      if (tid < kNumSuper) s.super[tid] = ex;
-      if (tid == 0) {
-        s.total = tot;
-        peer->peer_total = tot;
-      }
-    }
-    cluster.sync();
-    const uint32_t total0 = h == 0 ? s.total : s.peer_total;
-    const uint32_t m = s.total + s.peer_total;
-    if (h == 0 && tid == 0) {
-      unsigned long long b = atomicAdd(&v.st->vox_cursor, (unsigned long long)m);
-      int over = b + m > v.vox_cap;
-      if (over) raise_err(v.st, ERR_ARENA, s.node, b + m);
-      s.vbase = b;
-      peer->vbase = b;
-      s.skip = over;
-      peer->skip = over;
-      v.n_first[s.node] = b;
-      v.n_count[s.node] = over ? 0 : m;
-    }
-    cluster.sync();
-    if (s.skip) continue;
-    const uint64_t vbase = s.vbase;
-    const uint32_t rank_off = h == 0 ? 0 : total0;
-    const bool wide = MODE == LOD_MODE_AVERAGE && s.S >= kWideS;
-
-    // ---- emit keys in rank order, clear accumulators ----
-    for (int w = tid; w < kHalfWords; w += kVT) {
-      uint32_t bw = s.bits[w];
-      if (!bw) continue;
-      uint32_t r = rank_off + s.super[w >> kSuperShift] + s.rel[w];
-      while (bw) {
-        uint32_t b = __ffs(bw) - 1;
-        bw &= bw - 1;
-        v.vox[vbase + r].x = (h << 20) | ((uint32_t)w << 5) | b;
-        if (MODE == LOD_MODE_AVERAGE) {
-          acc[2ull * r] = 0;
-          acc[2ull * r + 1] = 0;
-          if (wide) v.vox[vbase + r].y = 0;
+        uint32_t j = j0 + u * kT;
+        if (j >= ch.w) continue;
+        const uint64_t a = acc0 + rank_of(bits, pre, r[u].x);
+        const uint32_t rgb = r[u].y;
+        if (L.mode == LOD_MODE_AVERAGE) {
+          unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 2 * a;
+          atomicAdd(p, (unsigned long long)(rgb & 0xFF) | ((unsigned long long)((rgb >> 8) & 0xFF) << 32));
+          atomicAdd(p + 1, (unsigned long long)((rgb >> 16) & 0xFF) | (1ull << 32));
         } else {
-          acc32[r] = 0;
-        }
-        ++r;
-      }
-    }
-    __threadfence();
-    cluster.sync();
-
-    auto global_rank = [&](uint32_t key) -> uint32_t {
-      uint32_t kh = key >> 20;
-      const VoxSmem* own = (kh == h) ? &s : peer;
-      return (kh ? total0 : 0) + rank_in(own, key & 0xFFFFF);
-    };
-
-    if (MODE == LOD_MODE_RANDOM) {
-      // ---- pass B: max (rand12 | ordinal20) per voxel ----
-      const uint64_t hs = s.hash;
-      for_my_samples(v, s, [&](uint32_t ord, uint32_t key, uint32_t) {
-        uint32_t enc = ((uint32_t)(mix64(hs ^ (uint64_t)ord) >> 32) & 0xFFF00000u) | (ord & 0xFFFFFu);
-        atomicMax(acc32 + global_rank(key), enc);
-      });
-      __threadfence();
-      cluster.sync();
-      // ---- pass C: the winning sample writes its colour ----
-      for_my_samples(v, s, [&](uint32_t ord, uint32_t key, uint32_t rgb) {
-        uint32_t enc = ((uint32_t)(mix64(hs ^ (uint64_t)ord) >> 32) & 0xFFF00000u) | (ord & 0xFFFFFu);
-        uint32_t r = global_rank(key);
-        if (__ldcg(acc32 + r) == enc) v.vox[vbase + r].y = rgb;
-      });
-    } else {
-      const int passes = wide ? 3 : 1;
-      for (int p = 0; p < passes; ++p) {
-        // ---- pass B: exact integer sums + counts ----
-        for_my_samples(v, s, [&](uint32_t, uint32_t key, uint32_t rgb) {
-          uint32_t r = global_rank(key);
-          if (!wide) {
-            atomicAdd((unsigned long long*)(acc + 2ull * r),
-                      (unsigned long long)(rgb & 0xFF) | ((unsigned long long)((rgb >> 8) & 0xFF) << 32));
-            atomicAdd((unsigned long long*)(acc + 2ull * r + 1),
-                      (unsigned long long)((rgb >> 16) & 0xFF) | (1ull << 32));
-          } else {
-            atomicAdd((unsigned long long*)(acc + 2ull * r), (unsigned long long)((rgb >> (8 * p)) & 0xFF));
-            atomicAdd((unsigned long long*)(acc + 2ull * r + 1), 1ull);
-          }
-        });
-        __threadfence();
-        cluster.sync();
-        // ---- finalize own ranks: (2*sum + n) // (2*n), round half up (sampling.py:96) ----
-        const uint32_t own = s.total;
-        for (uint32_t i = tid; i < own; i += kVT) {
-          uint32_t r = rank_off + i;
-          uint64_t a = __ldcg(acc + 2ull * r), b = __ldcg(acc + 2ull * r + 1);
-          if (!wide) {
-            uint64_t n = b >> 32;
-            v.vox[vbase + r].y = mean_round(a & 0xFFFFFFFFull, n) | (mean_round(a >> 32, n) << 8) |
-                                 (mean_round(b & 0xFFFFFFFFull, n) << 16);
-          } else {
-            v.vox[vbase + r].y |= mean_round(a, b) << (8 * p);
-            acc[2ull * r] = 0;
-            acc[2ull * r + 1] = 0;
-          }
-        }
-        if (wide && p + 1 < passes) {
-          __threadfence();
-          cluster.sync();
+          atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, rand_enc(nd.hash, ob + j));
         }
       }
     }
   }
 }
 
-template <int FMT, int MODE>
-void launch_one(const VoxView& v, int n_clusters, cudaStream_t st) {
-  auto kern = k_voxelize<FMT, MODE>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(VoxSmem));
-    configured = true;
+// ---------------------------------------------------------------------------
+// K4: finalize every voxel of the level
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
+  if (L.st->err & ERR_ARENA) return;
+  const uint32_t nch = L.counters[2];
+  const int cpar = L.parity ^ 1;
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint2 ch = L.vchunks[c];
+    const VoxNode& nd = L.info[ch.x];
+    const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
+    const uint64_t acc0 = nd.vbase - L.level_start[0];
+    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
+      const uint32_t key = L.vox[nd.vbase + r].x;
+      const uint32_t X = key >> 14, Y = (key >> 7) & 127, Z = key & 127;
+      const int o = (int)((X >> 6) | ((Y >> 6) << 1) | ((Z >> 6) << 2));
+      const int32_t cs = nd.cslot[o];
+      uint64_t sr = 0, sg = 0, sb = 0, n = 0;
+      uint32_t best = 0, best_rgb = 0;
+      bool have = false;
+      if (cs >= 0) {
+        // gather the child's 2x2x2 block: each (cx, cy) row holds both z cells in one word
+        const uint32_t* cb = bits_of(L, cpar, (uint32_t)cs);
+        const uint32_t* cp = pre_of(L, cpar, (uint32_t)cs);
+        const VoxNode& ci = L.cinfo[cs];
+        const uint32_t cx0 = (X & 63) << 1, cy0 = (Y & 63) << 1, cz0 = (Z & 63) << 1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t ck = ((cx0 + (q & 1)) << 14) | ((cy0 + (q >> 1)) << 7) | cz0;
+          const uint32_t w = ck >> 5, b = ck & 31;
+          const uint32_t bw = __ldcg(cb + w);
+          const uint32_t two = (bw >> b) & 3u;
+          if (!two) continue;
+          uint32_t cr = __ldcg(cp + w) + __popc(bw & ((1u << b) - 1));
+#pragma unroll
+          for (int dz = 0; dz < 2; ++dz) {
+            if (!((two >> dz) & 1)) continue;
+            const uint32_t rgb = __ldcg(&L.vox[ci.vbase + cr].y);
+            if (L.mode == LOD_MODE_AVERAGE) {
+              sr += rgb & 0xFF, sg += (rgb >> 8) & 0xFF, sb += (rgb >> 16) & 0xFF, ++n;
+            } else {
+              uint32_t e = rand_enc(nd.hash, nd.cbase[o] + cr);
+              if (!have || e > best) best = e, best_rgb = rgb, have = true;
+            }
+            ++cr;
+          }
+        }
+      }
+      if (L.mode == LOD_MODE_AVERAGE) {
+        const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(L.acc) + acc0 + r);
+        sr += a.x & 0xFFFFFFFFull, sg += a.x >> 32, sb += a.y & 0xFFFFFFFFull, n += a.y >> 32;
+        L.vox[nd.vbase + r].y = mean_round(sr, n) | (mean_round(sg, n) << 8) | (mean_round(sb, n) << 16);
+      } else {
+        const uint32_t e = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
+        if (!have || e > best) {
+          // the winner is a leaf point: its ordinal names (child, index) directly
+          const uint32_t ord = e & 0xFFFFFu;
+          int oo = 7;
+          while (oo > 0 && (nd.cslot[oo] != -1 || nd.cbase[oo] > ord)) --oo;
+          best_rgb = __ldg(&L.stash[nd.cfirst[oo] + (ord - nd.cbase[oo])].y);
+        }
+        L.vox[nd.vbase + r].y = best_rgb;
+      }
+    }
   }
-  kern<<<2 * n_clusters, kVT, sizeof(VoxSmem), st>>>(v);
 }
 
 }  // namespace
 
-int voxelize_smem_bytes() { return (int)sizeof(VoxSmem); }
-
-int launch_voxelize_level(const VoxView& v, int n_clusters, cudaStream_t s) {
-  if (v.fmt == LOD_POINTS_F32) {
-    if (v.mode == LOD_MODE_RANDOM)
-      launch_one<LOD_POINTS_F32, LOD_MODE_RANDOM>(v, n_clusters, s);
-    else
-      launch_one<LOD_POINTS_F32, LOD_MODE_AVERAGE>(v, n_clusters, s);
-  } else {
-    if (v.mode == LOD_MODE_RANDOM)
-      launch_one<LOD_POINTS_F64, LOD_MODE_RANDOM>(v, n_clusters, s);
-    else
-      launch_one<LOD_POINTS_F64, LOD_MODE_AVERAGE>(v, n_clusters, s);
-  }
-  return 1;
+// Runs one depth level; returns launches.  counters[0..2] must be zero on entry and the
+// level's bitmaps cleared.
+int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s) {
+  const int grid = sms * 8;
+  k_setup<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L);
+  if (L.fmt == LOD_POINTS_F32)
+    k_occupy<LOD_POINTS_F32><<<grid, kT, 0, s>>>(L);
+  else
+    k_occupy<LOD_POINTS_F64><<<grid, kT, 0, s>>>(L);
+  k_block_sums<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
+  k_alloc<<<1, 1024, 0, s>>>(L);
+  k_prefix_emit<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
+  k_scatter<<<grid, kT, 0, s>>>(L);
+  k_finalize<<<grid, kT, 0, s>>>(L);
+  return 7;
 }
+
+// chunk sizes: small levels get small chunks so every SM has work
+uint32_t voxelize_chunk(uint32_t nodes) { return nodes <= 8 ? 1024 : 2048; }
+uint32_t voxelize_vchunk(uint32_t nodes) { return nodes <= 8 ? 128 : nodes <= 64 ? 512 : kVoxChunk; }
+uint64_t voxelize_chunk_capacity(uint64_t samples, uint32_t nodes) { return samples / 1024 + 8ull * nodes + 16; }
+uint64_t voxelize_vchunk_capacity(uint64_t voxels, uint32_t nodes) { return voxels / 128 + nodes + 16; }
 
 }  // namespace lod
