@@ -74,88 +74,105 @@ __device__ __forceinline__ uint32_t* pre_of(const VoxLevel& L, int parity, uint3
 }
 
 // ---------------------------------------------------------------------------
-// K0: per-node setup
+// K0: per-node setup; eight lanes per node, one per child octant
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
-  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= L.list_n || (L.st->err & ERR_ARENA)) return;
-  const uint32_t node = L.list[s];
-  VoxNode info;
-  uint32_t ord = 0;
-  bool empty = false;
-  for (int o = 0; o < 8; ++o) {
-    int32_t c = L.n_child[8ull * node + o];
-    info.cbase[o] = ord;
-    info.ccount[o] = 0;
-    info.cfirst[o] = 0;
-    info.cslot[o] = -2;  // absent
-    if (c < 0) continue;
-    bool leaf = L.n_leaf[c] >= 0;
-    uint32_t cnt = L.n_count[c];
-    info.ccount[o] = cnt;
-    info.cfirst[o] = L.n_first[c];
-    info.cslot[o] = leaf ? -1 : (int32_t)L.node_slot[c];
-    empty |= cnt == 0;
-    ord += cnt;
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t s = g >> 3;
+  const int o = (int)(g & 7);
+  const bool live = s < L.list_n && !(L.st->err & ERR_ARENA);
+  const uint32_t node = live ? L.list[s] : 0;
+  const int32_t c = live ? L.n_child[8ull * node + o] : -1;
+  uint32_t cnt = 0;
+  uint64_t first = 0;
+  int32_t cslot = -2;  // absent
+  if (c >= 0) {
+    const bool leaf = L.n_leaf[c] >= 0;
+    cnt = L.n_count[c];
+    first = L.n_first[c];
+    cslot = leaf ? -1 : (int32_t)L.node_slot[c];
   }
-  info.S = ord;
-  info.node = node;
-  // path_hash(seed, path): key = mix64(8 key + octant + 1) per digit (rng.py:48-53)
-  uint64_t cell = L.n_cell[node];
-  uint32_t cx = (uint32_t)cell & 0xFFFF, cy = (uint32_t)(cell >> 16) & 0xFFFF, cz = (uint32_t)(cell >> 32) & 0xFFFF;
-  int depth = (int)(cell >> 48) & 0xFF;
-  uint64_t key = L.seed;
-  for (int b = depth - 1; b >= 0; --b) {
-    uint32_t oc = ((cx >> b) & 1) | (((cy >> b) & 1) << 1) | (((cz >> b) & 1) << 2);
-    key = mix64(key * 8 + oc + 1);
+  // inclusive scan of the counts over the node's 8 lanes -> ordinal bases (sampling.py:5-6)
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 8; d <<= 1) {
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d, 8);
+    if (o >= d) incl += t;
   }
-  info.hash = L.seed ^ key;
-  info.box = L.n_box[node];
-  info.inv = __dmul_rn(L.inv_world, (double)(1ull << depth));
-  info.vbase = 0;
-  info.m = 0;
-  L.node_slot[node] = s;
+  const uint32_t S = __shfl_sync(0xFFFFFFFFu, incl, 7, 8);
+  const bool empty = __any_sync(0xFFFFFFFFu, c >= 0 && cnt == 0) &&
+                     (__ballot_sync(0xFFFFFFFFu, c >= 0 && cnt == 0) >> (threadIdx.x & 24) & 0xFF);
+  if (!live) return;
+  VoxNode& info = L.info[s];
+  info.cbase[o] = incl - cnt;
+  info.ccount[o] = cnt;
+  info.cfirst[o] = first;
+  info.cslot[o] = cslot;
   bool skip = false;
-  if (empty) {
-    skip = true;
-    raise_err(L.st, ERR_EMPTY_CHILD, node);
-  } else if (L.mode == LOD_MODE_RANDOM && ord >= (uint32_t)kRandomLimit) {
-    skip = true;
-    raise_err(L.st, ERR_RANDOM_LIMIT, node, ord);
-  }
-  info.skip = skip;
-  L.info[s] = info;
-  if (skip) return;
-  // chunks of one node are contiguous in the lists: blocks walking the lists in order keep
-  // only a few nodes' bitmaps, prefixes and accumulators live in L2 at any time
-  const uint32_t chunk = L.chunk;
-  uint32_t tot = 0, ltot = 0;
-  for (int o = 0; o < 8; ++o) {
-    uint32_t nch = (info.ccount[o] + chunk - 1) / chunk;
-    tot += nch;
-    if (info.cslot[o] == -1) ltot += nch;
-  }
-  uint32_t at = atomicAdd(L.counters + 0, tot);
-  uint32_t lat = ltot ? atomicAdd(L.counters + 1, ltot) : 0;
-  for (int o = 0; o < 8; ++o) {
-    const uint32_t cnt = info.ccount[o];
-    const bool leaf = info.cslot[o] == -1;
-    for (uint32_t j = 0; j < cnt; j += chunk) {
-      uint4 ch = make_uint4(s, (uint32_t)o, j, min(cnt, j + chunk));
-      L.chunks[at++] = ch;
-      if (leaf) L.leaf_chunks[lat++] = ch;
+  if (empty) skip = true;
+  else if (L.mode == LOD_MODE_RANDOM && S >= (uint32_t)kRandomLimit) skip = true;
+  if (o == 0) {
+    info.S = S;
+    info.node = node;
+    // path_hash(seed, path): key = mix64(8 key + octant + 1) per digit (rng.py:48-53)
+    uint64_t cell = L.n_cell[node];
+    uint32_t cx = (uint32_t)cell & 0xFFFF, cy = (uint32_t)(cell >> 16) & 0xFFFF, cz = (uint32_t)(cell >> 32) & 0xFFFF;
+    int depth = (int)(cell >> 48) & 0xFF;
+    uint64_t key = L.seed;
+    for (int b = depth - 1; b >= 0; --b) {
+      uint32_t oc = ((cx >> b) & 1) | (((cy >> b) & 1) << 1) | (((cz >> b) & 1) << 2);
+      key = mix64(key * 8 + oc + 1);
     }
+    info.hash = L.seed ^ key;
+    info.box = L.n_box[node];
+    info.inv = __dmul_rn(L.inv_world, (double)(1ull << depth));
+    info.vbase = 0;
+    info.m = 0;
+    info.skip = skip;
+    L.node_slot[node] = s;
+    if (empty) raise_err(L.st, ERR_EMPTY_CHILD, node);
+    else if (skip) raise_err(L.st, ERR_RANDOM_LIMIT, node, S);
+  }
+  if (skip || cnt == 0) return;
+  const uint32_t chunk = L.chunk;
+  const uint32_t nch = (cnt + chunk - 1) / chunk;
+  uint32_t at = atomicAdd(L.counters + 0, nch);
+  uint32_t lat = cslot == -1 ? atomicAdd(L.counters + 1, nch) : 0;
+  for (uint32_t j = 0; j < cnt; j += chunk) {
+    uint4 ch = make_uint4(s, (uint32_t)o, j, min(cnt, j + chunk));
+    L.chunks[at++] = ch;
+    if (cslot == -1) L.leaf_chunks[lat++] = ch;
   }
 }
 
 // ---------------------------------------------------------------------------
-// K1: occupancy (test before set: most samples land in an already occupied cell).
+// K1: occupancy.  A chunk holds samples of ONE child octant o, and those land in the node
+// grid's octant-o region (64^3 cells = 8192 words) -- always for voxel children, and for
+// leaf points except the rare boundary spill.  The region bitmap is built in shared memory
+// and OR-ed into the node bitmap once; spills go straight to the global bitmap.
 // Leaf points are projected here, once, into the node's grid (sampling.py:29-38) and
-// stashed as {key, rgb} for K3/K4, so the record is read a single time per level.
+// stashed as {key, rgb} for K3/K4.
 // ---------------------------------------------------------------------------
+constexpr int kRT = 512;                       // threads of the region kernels
+constexpr uint32_t kRegionWords = 8192;        // 64 x 64 rows x 2 words
+
+__device__ __forceinline__ bool region_word(uint32_t key, int o, uint32_t& lw) {
+  const uint32_t x = key >> 14, y = (key >> 7) & 127, z = key & 127;
+  if ((x >> 6) != (uint32_t)(o & 1) || (y >> 6) != (uint32_t)((o >> 1) & 1) || (z >> 6) != (uint32_t)(o >> 2))
+    return false;
+  lw = (((x & 63) << 6) | (y & 63)) << 1 | ((z >> 5) & 1);
+  return true;
+}
+__device__ __forceinline__ uint32_t region_to_global(uint32_t lw, int o) {
+  const uint32_t lx = lw >> 7, ly = (lw >> 1) & 63, lz = lw & 1;
+  return ((((uint32_t)(o & 1) << 6 | lx) << 7) | ((uint32_t)((o >> 1) & 1) << 6 | ly)) << 2 |
+         ((uint32_t)(o >> 2) << 1 | lz);
+}
+
 template <int FMT>
-__global__ void __launch_bounds__(kT) k_occupy(VoxLevel L) {
+__global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
   if (L.st->err & ERR_ARENA) return;
+  __shared__ uint32_t rb[kRegionWords];
   const uint32_t nch = L.counters[0];
   constexpr int U = 8;
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
@@ -164,43 +181,52 @@ __global__ void __launch_bounds__(kT) k_occupy(VoxLevel L) {
     uint32_t* bits = bits_of(L, L.parity, ch.x);
     const int o = (int)ch.y;
     const uint64_t first = nd.cfirst[o];
+    for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) rb[i] = 0;
+    __syncthreads();
+    auto mark = [&](uint32_t key) {
+      const uint32_t bit = 1u << (key & 31);
+      uint32_t lw;
+      if (region_word(key, o, lw)) {
+        if (!(rb[lw] & bit)) atomicOr(rb + lw, bit);
+      } else {  // boundary spill of a leaf point into a neighbouring octant
+        atomicOr(bits + (key >> 5), bit);
+      }
+    };
     if (nd.cslot[o] == -1) {
       const double4 b = nd.box;
       const double inv = nd.inv;
-      for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kT) {
+      for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kRT) {
         typename Rec<FMT>::Raw r[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          uint32_t j = min(j0 + u * kT, ch.w - 1);
-          r[u] = Rec<FMT>::load(L.leaf_pts, first + j);
-        }
+        for (int u = 0; u < U; ++u) r[u] = Rec<FMT>::load(L.leaf_pts, first + min(j0 + u * kRT, ch.w - 1));
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          uint32_t j = j0 + u * kT;
+          const uint32_t j = j0 + u * kRT;
           if (j >= ch.w) continue;
           const uint32_t key = (grid_cell128(Rec<FMT>::x(r[u]), b.x, b.w, inv) << 14) |
                                (grid_cell128(Rec<FMT>::y(r[u]), b.y, b.w, inv) << 7) |
                                grid_cell128(Rec<FMT>::z(r[u]), b.z, b.w, inv);
           L.stash[first + j] = make_uint2(key, Rec<FMT>::rgb(r[u]));
-          uint32_t w = key >> 5, bit = 1u << (key & 31);
-          if (!(__ldcg(bits + w) & bit)) atomicOr(bits + w, bit);
+          mark(key);
         }
       }
     } else {
       const uint2* src = L.vox + first;
-      for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kT) {
+      for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kRT) {
         uint32_t k[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) k[u] = __ldg(&src[min(j0 + u * kT, ch.w - 1)].x);
+        for (int u = 0; u < U; ++u) k[u] = __ldg(&src[min(j0 + u * kRT, ch.w - 1)].x);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (j0 + u * kT >= ch.w) continue;
-          const uint32_t key = voxel_to_parent(o, k[u]);
-          uint32_t w = key >> 5, bit = 1u << (key & 31);
-          if (!(__ldcg(bits + w) & bit)) atomicOr(bits + w, bit);
-        }
+        for (int u = 0; u < U; ++u)
+          if (j0 + u * kRT < ch.w) mark(voxel_to_parent(o, k[u]));
       }
     }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) {
+      const uint32_t v = rb[i];
+      if (v) atomicOr(bits + region_to_global(i, o), v);
+    }
+    __syncthreads();
   }
 }
 
@@ -327,10 +353,15 @@ __device__ __forceinline__ uint32_t rank_of(const uint32_t* bits, const uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// K3: leaf-point samples -> accumulators
+// K3: leaf-point samples -> accumulators.  The octant region's bits + prefixes are staged
+// in shared memory, so a sample's rank costs two shared loads; only the accumulator
+// atomics reach L2.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kT) k_scatter(VoxLevel L) {
+__global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
   if (L.st->err & ERR_ARENA) return;
+  extern __shared__ __align__(16) uint32_t rsm[];
+  uint32_t* rbits = rsm;
+  uint32_t* rpre = rsm + kRegionWords;
   const uint32_t nch = L.counters[1];
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const uint4 ch = L.leaf_chunks[c];
@@ -339,21 +370,31 @@ __global__ void __launch_bounds__(kT) k_scatter(VoxLevel L) {
     const uint32_t* pre = pre_of(L, L.parity, ch.x);
     const uint64_t acc0 = nd.vbase - L.level_start[0];
     const int o = (int)ch.y;
+    for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) {
+      const uint32_t gw = region_to_global(i, o);
+      rbits[i] = __ldcg(bits + gw);
+      rpre[i] = __ldcg(pre + gw);
+    }
+    __syncthreads();
     const uint2* src = L.stash + nd.cfirst[o];
     const uint32_t ob = nd.cbase[o];
     constexpr int U = 4;
-    for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kT) {
+    for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kRT) {
       uint2 r[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        uint32_t j = j0 + u * kT;
-        if (j < ch.w) r[u] = __ldg(src + j);
-      }
+      for (int u = 0; u < U; ++u) r[u] = __ldg(src + min(j0 + u * kRT, ch.w - 1));
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        uint32_t j = j0 + u * kT;
+        const uint32_t j = j0 + u * kRT;
         if (j >= ch.w) continue;
-        const uint64_t a = acc0 + rank_of(bits, pre, r[u].x);
+        const uint32_t key = r[u].x;
+        const uint32_t mask = (1u << (key & 31)) - 1;
+        uint32_t lw, rank;
+        if (region_word(key, o, lw))
+          rank = rpre[lw] + __popc(rbits[lw] & mask);
+        else
+          rank = __ldcg(pre + (key >> 5)) + __popc(__ldcg(bits + (key >> 5)) & mask);
+        const uint64_t a = acc0 + rank;
         const uint32_t rgb = r[u].y;
         if (L.mode == LOD_MODE_AVERAGE) {
           unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 2 * a;
@@ -364,6 +405,7 @@ __global__ void __launch_bounds__(kT) k_scatter(VoxLevel L) {
         }
       }
     }
+    __syncthreads();
   }
 }
 
@@ -440,23 +482,28 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
 // level's bitmaps cleared.
 int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s) {
   const int grid = sms * 8;
-  k_setup<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L);
+  k_setup<<<ceil_div_u32(8ull * L.list_n, kT), kT, 0, s>>>(L);
   if (L.fmt == LOD_POINTS_F32)
-    k_occupy<LOD_POINTS_F32><<<grid, kT, 0, s>>>(L);
+    k_occupy<LOD_POINTS_F32><<<sms * 2, kRT, 0, s>>>(L);
   else
-    k_occupy<LOD_POINTS_F64><<<grid, kT, 0, s>>>(L);
+    k_occupy<LOD_POINTS_F64><<<sms * 2, kRT, 0, s>>>(L);
   k_block_sums<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
   k_alloc<<<1, 1024, 0, s>>>(L);
   k_prefix_emit<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
-  k_scatter<<<grid, kT, 0, s>>>(L);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);
+    configured = true;
+  }
+  k_scatter<<<sms * 2, kRT, 2 * kRegionWords * 4, s>>>(L);
   k_finalize<<<grid, kT, 0, s>>>(L);
   return 7;
 }
 
 // chunk sizes: small levels get small chunks so every SM has work
-uint32_t voxelize_chunk(uint32_t nodes) { return nodes <= 8 ? 1024 : 2048; }
+uint32_t voxelize_chunk(uint32_t nodes) { return nodes <= 8 ? 4096 : 16384; }
 uint32_t voxelize_vchunk(uint32_t nodes) { return nodes <= 8 ? 128 : nodes <= 64 ? 512 : kVoxChunk; }
-uint64_t voxelize_chunk_capacity(uint64_t samples, uint32_t nodes) { return samples / 1024 + 8ull * nodes + 16; }
+uint64_t voxelize_chunk_capacity(uint64_t samples, uint32_t nodes) { return samples / 4096 + 8ull * nodes + 16; }
 uint64_t voxelize_vchunk_capacity(uint64_t voxels, uint32_t nodes) { return voxels / 128 + nodes + 16; }
 
 }  // namespace lod
