@@ -147,6 +147,43 @@ uint64_t lod_tree_launches(const lod_tree* tree);
 int lod_generate(const char* kind, uint64_t seed, uint64_t start, uint64_t n, void* d_out,
                  const double* table_or_null, void* stream);
 
+/* ---------------------------------------------------------------------------------
+ * Multi-GPU stages (one process per GPU; the caller runs the collectives, e.g. NCCL via
+ * torch.distributed -- see paper_2302_14801_b200/dist.py).  Subtree sharding per
+ * world bounds and counting grids are all-reduced, every rank derives the
+ * identical node table, leaves are assigned to ranks by top-level subtree, points are
+ * exchanged all-to-all (source-rank order keeps the global input order), each rank samples
+ * its subtrees and rank 0 merges the coarsest levels from the imported subtree roots.
+ * ------------------------------------------------------------------------------- */
+typedef struct lod_span { void* ptr; uint64_t n; } lod_span; /* device array of uint32 */
+
+/* init + local min xyz / max xyz of this rank's points (host out[6]; +inf/-inf if none) */
+int lod_dist_begin(lod_tree* tree, const void* d_points, uint64_t n_local, int format,
+                   const lod_config* config, double* out_min_max, void* stream);
+/* count the local points in the GLOBAL cube world = {min xyz, size}; *out = the main
+ * counting grid, to be all-reduced (SUM) in place before the next call */
+int lod_dist_count(lod_tree* tree, uint64_t n_global, const double* world, lod_span* out, void* stream);
+/* next extension round from the reduced counts; *out = its grids to all-reduce (SUM) in
+ * place, out->n == 0 when no further round is needed (partition.py:109-151) */
+int lod_dist_extend(lod_tree* tree, lod_span* out, void* stream);
+/* merge + node table + targets on the reduced pyramids, then the stable local distribute;
+ * h_local_leaf_counts (n_leaves) receives this rank's points per leaf */
+int lod_dist_skeleton(lod_tree* tree, uint32_t* h_local_leaf_counts, void* stream);
+/* this rank's points per leaf after lod_dist_skeleton / lod_dist_adopt (n_leaves entries) */
+int lod_dist_leaf_counts(const lod_tree* tree, uint32_t* h_counts);
+/* copy record segments (in records) from d_src to d_dst; NULL = the tree's leaf buffer */
+int lod_dist_copy_segments(lod_tree* tree, const void* d_src, void* d_dst, const uint64_t* h_src,
+                           const uint64_t* h_dst, const uint32_t* h_cnt, uint64_t nseg, void* stream);
+/* make d_records (leaf-major, per-leaf counts h_leaf_counts) this rank's leaf buffer */
+int lod_dist_adopt(lod_tree* tree, const void* d_records, uint64_t n, const uint32_t* h_leaf_counts,
+                   void* stream);
+/* voxelize the inner nodes with h_mask[node] = 1; append = keep earlier results; the
+ * n_imp imported inner nodes (voxels concatenated in d_imp_vox, counts h_imp_counts) are
+ * placed in the arena and made gatherable from parity slot imp_slot_base on */
+int lod_dist_voxelize(lod_tree* tree, int mode, uint64_t seed, const uint8_t* h_mask, int append,
+                      const int32_t* h_imp_nodes, const uint32_t* h_imp_counts, uint32_t n_imp,
+                      uint32_t imp_slot_base, const void* d_imp_vox, void* stream);
+
 /* Message of the last failure on the calling thread. */
 const char* lod_last_error(void);
 

@@ -37,6 +37,10 @@ class LodNode(C.Structure):
                 ("child", C.c_int32 * 8)]
 
 
+class LodSpan(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("n", C.c_uint64)]
+
+
 # numpy view of lod_node (88 bytes)
 NODE_DTYPE = None
 
@@ -71,6 +75,15 @@ SIGNATURES = [
     ("lod_tree_stage_ms", C.c_int, [_P, C.POINTER(C.c_float)]),
     ("lod_tree_launches", C.c_uint64, [_P]),
     ("lod_generate", C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint64, _P, C.POINTER(C.c_double), _P]),
+    ("lod_dist_begin", C.c_int, [_P, _P, C.c_uint64, C.c_int, C.POINTER(LodConfig), _P, _P]),
+    ("lod_dist_count", C.c_int, [_P, C.c_uint64, _P, C.POINTER(LodSpan), _P]),
+    ("lod_dist_extend", C.c_int, [_P, C.POINTER(LodSpan), _P]),
+    ("lod_dist_skeleton", C.c_int, [_P, _P, _P]),
+    ("lod_dist_leaf_counts", C.c_int, [_P, _P]),
+    ("lod_dist_copy_segments", C.c_int, [_P, _P, _P, _P, _P, _P, C.c_uint64, _P]),
+    ("lod_dist_adopt", C.c_int, [_P, _P, C.c_uint64, _P, _P]),
+    ("lod_dist_voxelize", C.c_int, [_P, C.c_int, C.c_uint64, _P, C.c_int, _P, _P, C.c_uint32, C.c_uint32, _P,
+                                    _P]),
     ("lod_last_error", C.c_char_p, []),
     ("lod_version", C.c_char_p, []),
 ]

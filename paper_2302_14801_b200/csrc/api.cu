@@ -88,7 +88,7 @@ struct lod_tree {
 
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
   DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
-  DevBuf leaf_node, leaf_first, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
+  DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
   DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf;
   DevBuf vox, scratch, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vleaf_chunks, vvchunks;
@@ -103,6 +103,16 @@ struct lod_tree {
   double inv_world = 0;
   RadixPlan plan{};
   uint32_t epoch = 1;
+  // split phase state
+  const void* pts = nullptr;
+  uint64_t n_global = 0;
+  uint64_t ext_pyr_used = 0, ext_tgt_used = 0;
+  uint32_t round_cur = 0, round_first = 0, round_parent_first = 0;
+  int round_base = 0;
+  bool dist = false;
+  DevBuf local_main, local_ext;   // multi-GPU: this process's counts before the all-reduce
+  DevBuf plan_lists, seg;
+  int dist_stage = 0;
 };
 
 namespace {
@@ -209,6 +219,7 @@ SplitView make_view(lod_tree* t, const void* pts) {
   v.n_nodes = t->n_nodes;
   v.leaf_node = t->leaf_node.as<uint32_t>();
   v.leaf_first = t->leaf_first.as<uint64_t>();
+  v.leaf_count = t->leaf_count.as<uint32_t>();
   v.leaf_pbox = t->leaf_pbox.as<double4>();
   v.leaf_pinv = t->leaf_pinv.as<double>();
   v.n_leaves = t->n_leaves;
@@ -233,11 +244,16 @@ void mark(lod_tree* t, int i, cudaStream_t s) {
   if (t->timing) cudaEventRecord(t->ev[i], s);
 }
 
-int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub, const lod_config* cfg,
-             cudaStream_t s) {
+// ---------------------------------------------------------------------------
+// split phases.  Single GPU: init, bounds, count, [anchors, {round, subanchors}*],
+// skeleton, distribute.  Multi-GPU (dist.py) calls the same phases with collectives in
+// between (world bounds, counting grids and extension grids are all-reduced).
+// ---------------------------------------------------------------------------
+int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub, const lod_config* cfg,
+               cudaStream_t s) {
   if (!t) return fail(LOD_EVALUE, "null tree");
   if (!cfg) return fail(LOD_EVALUE, "null config");
-  if (n == 0) return fail(LOD_EVALUE, "cannot partition an empty point cloud");
+  if (n == 0 && !t->dist) return fail(LOD_EVALUE, "cannot partition an empty point cloud");
   if (cfg->T < 1) return fail(LOD_EVALUE, "T must be >= 1");
   if (cfg->max_depth < cfg->initial_depth) return fail(LOD_EVALUE, "max_depth must be >= initial_depth");
   if (cfg->max_depth > kMaxDepth) return fail(LOD_EVALUE, "max_depth must be <= %d", kMaxDepth);
@@ -249,24 +265,23 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   if (n >= 0xFFFFFFFFull) return fail(LOD_EUNSUPPORTED, "at most 2^32 - 2 points per GPU build");
   if (ub && !(ub[3] > 0)) return fail(LOD_EVALUE, "AABB size must be positive");
   CK(cudaSetDevice(t->device));
-
   t->split_done = false;
   t->voxel_mode = -1;
   t->n_voxels = 0;
   t->launches = 0;
   t->n = n;
+  t->pts = pts;
   t->fmt = fmt;
   t->cfg = *cfg;
   t->n_ext = 0;
   t->n_nodes = t->n_leaves = 0;
   t->rounds.clear();
+  t->ext_pyr_used = t->ext_tgt_used = 0;
+  t->round_cur = 0;
   const int D = cfg->initial_depth;
   const uint64_t main_cells = level_off(D + 1);
   const uint64_t fine_cells = 1ull << (3 * D);
-  const size_t rec = fmt == LOD_POINTS_F32 ? 16 : 32;
-
   mark(t, 0, s);
-  // device state
   DevState init{};
   for (int a = 0; a < 3; ++a) init.lo_key[a] = ~0ull, init.hi_key[a] = 0;
   *t->host_state = init;
@@ -278,87 +293,118 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   CK(cudaMemsetAsync(t->t8.p, 0xFF, fine_cells * 4, s));
   uint64_t scan_blocks = (std::max<uint64_t>(main_cells, n) + kScanTile - 1) / kScanTile + 2;
   CK(ensure(t->scan, scan_blocks * 8));
-  ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+  return LOD_OK;
+}
 
-  SplitView v = make_view(t, pts);
-  RUN(launch_bounds(fmt, pts, n, v.st, ub, s));
-  RUN(launch_count(fmt, v, s));
+int phase_bounds(lod_tree* t, const double* ub, cudaStream_t s) {
+  SplitView v = make_view(t, t->pts);
+  if (t->n == 0 && !ub) return LOD_OK;  // empty shard: identity min/max keys
+  RUN(launch_bounds(t->fmt, t->pts, t->n, v.st, ub, s));
+  return LOD_OK;
+}
+
+int phase_count(lod_tree* t, cudaStream_t s) {
+  SplitView v = make_view(t, t->pts);
+  if (t->n) RUN(launch_count(t->fmt, v, s));
   mark(t, 1, s);
+  return LOD_OK;
+}
 
-  // ---- extension rounds (partition.py:109-151) ----
-  uint64_t ext_pyr_used = 0, ext_tgt_used = 0;
-  if (cfg->max_depth > D) {
-    uint64_t max_anchor = std::min<uint64_t>(fine_cells, n / ((uint64_t)cfg->T + 1) + 1);
-    CK(ensure(t->list, max_anchor * 8 + 8));
-    RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s));
+// Anchors of the first extension round from the (global) main finest counts.
+int phase_anchors(lod_tree* t, uint32_t* cur, cudaStream_t s) {
+  *cur = 0;
+  const int D = t->cfg.initial_depth;
+  if (t->cfg.max_depth <= D) return LOD_OK;
+  const uint64_t fine_cells = 1ull << (3 * D);
+  uint64_t max_anchor = std::min<uint64_t>(fine_cells, t->n_global / ((uint64_t)t->cfg.T + 1) + 1);
+  CK(ensure(t->list, max_anchor * 8 + 8));
+  ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+  SplitView v = make_view(t, t->pts);
+  RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s));
+  int r = read_state(t, s);
+  if (r) return r;
+  if ((r = check_errors(t, s))) return r;
+  *cur = (uint32_t)t->host_state->count_a;
+  t->round_base = D;
+  t->round_first = 0;
+  t->round_parent_first = 0;
+  t->round_cur = *cur;
+  return LOD_OK;
+}
+
+// Create the next extension round from t->list and count the local points into it.
+int phase_round(lod_tree* t, cudaStream_t s) {
+  const uint32_t cur = t->round_cur;
+  const int base = t->round_base;
+  const int ext = std::min(t->cfg.extension_depth, t->cfg.max_depth - base);
+  const uint64_t main_cells = level_off(t->cfg.initial_depth + 1);
+  const uint64_t psz = level_off(ext + 1), tsz = 1ull << (3 * ext);
+  const uint64_t pyr_base = main_cells + t->ext_pyr_used, tgt_base = t->ext_tgt_used;
+  const uint64_t new_pyr = (uint64_t)cur * psz, new_tgt = (uint64_t)cur * tsz;
+  const uint32_t first = t->round_first;
+  CK(ensure(t->pyr, (pyr_base + new_pyr) * 4, pyr_base * 4, s));
+  CK(ensure(t->te, (tgt_base + new_tgt) * 4, tgt_base * 4, s));
+  CK(ensure(t->meta, (size_t)(first + cur) * sizeof(ExtMeta), (size_t)first * sizeof(ExtMeta), s));
+  CK(cudaMemsetAsync(t->pyr.as<uint32_t>() + pyr_base, 0, new_pyr * 4, s));
+  CK(cudaMemsetAsync(t->te.as<int32_t>() + tgt_base, 0xFF, new_tgt * 4, s));
+  SplitView v = make_view(t, t->pts);
+  RUN(launch_ext_create(v, (int)t->rounds.size(), first, cur, t->list.as<uint64_t>(), t->round_parent_first,
+                        pyr_base, tgt_base, base, ext, s));
+  t->n_ext = first + cur;
+  v = make_view(t, t->pts);
+  if (t->n) RUN(launch_ext_count(t->fmt, v, first, s));
+  t->rounds.push_back(Round{first, cur, ext, base, pyr_base, tgt_base});
+  t->ext_pyr_used += new_pyr;
+  t->ext_tgt_used += new_tgt;
+  return LOD_OK;
+}
+
+// After the last round's counts are final (all-reduced): the next round's anchors.
+int phase_subanchors(lod_tree* t, uint32_t* next, cudaStream_t s) {
+  *next = 0;
+  const Round& rd = t->rounds.back();
+  if (rd.base + rd.ext < t->cfg.max_depth) {
+    const uint64_t tsz = 1ull << (3 * rd.ext);
+    uint64_t cap_needed = std::min<uint64_t>((uint64_t)rd.count * tsz, t->n_global / ((uint64_t)t->cfg.T + 1) + 1);
+    CK(ensure(t->list, cap_needed * 8 + 8));
+    uint64_t sb = ((uint64_t)rd.count * tsz + kScanTile - 1) / kScanTile + 2;
+    CK(ensure(t->scan, sb * 8));
+    ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+    SplitView v = make_view(t, t->pts);
+    RUN(launch_find_subanchors(v, rd.first, rd.count, rd.ext, t->list.as<uint64_t>(), scr, s));
     int r = read_state(t, s);
     if (r) return r;
-    if ((r = check_errors(t, s))) return r;
-    uint32_t cur = (uint32_t)t->host_state->count_a;
-    int base = D;
-    uint32_t first = 0, parent_first = 0;
-    int round = 0;
-    while (cur > 0) {
-      int ext = std::min(cfg->extension_depth, cfg->max_depth - base);
-      uint64_t psz = level_off(ext + 1), tsz = 1ull << (3 * ext);
-      uint64_t pyr_base = main_cells + ext_pyr_used, tgt_base = ext_tgt_used;
-      uint64_t new_pyr = (uint64_t)cur * psz, new_tgt = (uint64_t)cur * tsz;
-      CK(ensure(t->pyr, (pyr_base + new_pyr) * 4, pyr_base * 4, s));
-      CK(ensure(t->te, (tgt_base + new_tgt) * 4, tgt_base * 4, s));
-      CK(ensure(t->meta, (size_t)(first + cur) * sizeof(ExtMeta), (size_t)first * sizeof(ExtMeta), s));
-      CK(cudaMemsetAsync(t->pyr.as<uint32_t>() + pyr_base, 0, new_pyr * 4, s));
-      CK(cudaMemsetAsync(t->te.as<int32_t>() + tgt_base, 0xFF, new_tgt * 4, s));
-      v = make_view(t, pts);
-      RUN(launch_ext_create(v, round, first, cur, t->list.as<uint64_t>(), parent_first, pyr_base, tgt_base, base,
-                            ext, s));
-      t->n_ext = first + cur;
-      v = make_view(t, pts);
-      RUN(launch_ext_count(fmt, v, first, s));
-      t->rounds.push_back(Round{first, cur, ext, base, pyr_base, tgt_base});
-      ext_pyr_used += new_pyr;
-      ext_tgt_used += new_tgt;
-      uint32_t next = 0;
-      if (base + ext < cfg->max_depth) {
-        uint64_t cap_needed = std::min<uint64_t>((uint64_t)cur * tsz, n / ((uint64_t)cfg->T + 1) + 1);
-        CK(ensure(t->list, cap_needed * 8 + 8));
-        uint64_t sb = ((uint64_t)cur * tsz + kScanTile - 1) / kScanTile + 2;
-        CK(ensure(t->scan, sb * 8));
-        scr = ScanScratch{t->scan.as<uint64_t>(), t->scan.cap / 8};
-        v = make_view(t, pts);
-        RUN(launch_find_subanchors(v, first, cur, ext, t->list.as<uint64_t>(), scr, s));
-        if ((r = read_state(t, s))) return r;
-        next = (uint32_t)t->host_state->count_a;
-      }
-      parent_first = first;
-      first += cur;
-      base += ext;
-      cur = next;
-      ++round;
-    }
+    *next = (uint32_t)t->host_state->count_a;
   }
-  mark(t, 2, s);
+  t->round_parent_first = rd.first;
+  t->round_first = rd.first + rd.count;
+  t->round_base = rd.base + rd.ext;
+  t->round_cur = *next;
+  return LOD_OK;
+}
 
-  // ---- merge (partition.py:155-170) ----
+// merge + node table + targets + per-depth inner lists (partition.py:155-240)
+int phase_skeleton(lod_tree* t, cudaStream_t s) {
+  mark(t, 2, s);
+  const int D = t->cfg.initial_depth;
+  const uint64_t main_cells = level_off(D + 1);
   {
     std::vector<uint32_t> rf, rc;
     std::vector<int> re;
     std::vector<uint64_t> rb;
-    for (auto& rd : t->rounds) rf.push_back(rd.first), rc.push_back(rd.count), re.push_back(rd.ext),
-        rb.push_back(rd.pyr_base);
-    v = make_view(t, pts);
+    for (auto& rd : t->rounds)
+      rf.push_back(rd.first), rc.push_back(rd.count), re.push_back(rd.ext), rb.push_back(rd.pyr_base);
+    SplitView v = make_view(t, t->pts);
     RUN(launch_merge_all(v, rf.data(), rc.data(), re.data(), rb.data(), (int)t->rounds.size(), s));
   }
-
-  // ---- node enumeration (partition.py:201-231) ----
-  t->total_slots = main_cells + ext_pyr_used;
-  uint64_t slot_cap = std::min<uint64_t>(t->total_slots, n * (uint64_t)(cfg->max_depth + 1) + 1);
+  t->total_slots = main_cells + t->ext_pyr_used;
+  uint64_t slot_cap = std::min<uint64_t>(t->total_slots, t->n_global * (uint64_t)(t->cfg.max_depth + 1) + 1);
   CK(ensure(t->slots, slot_cap * 8));
   CK(ensure(t->node_idx, t->total_slots * 4));
-  {
-    uint64_t sb = (t->total_slots + kScanTile - 1) / kScanTile + 2;
-    CK(ensure(t->scan, sb * 8));
-    scr = ScanScratch{t->scan.as<uint64_t>(), t->scan.cap / 8};
-  }
+  uint64_t sb = (t->total_slots + kScanTile - 1) / kScanTile + 2;
+  CK(ensure(t->scan, sb * 8));
+  ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+  SplitView v = make_view(t, t->pts);
   RUN(launch_count_nodes(v, t->total_slots, t->slots.as<uint64_t>(), scr, s));
   int r = read_state(t, s);
   if (r) return r;
@@ -379,11 +425,12 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   CK(ensure(t->n_count, nn * 4));
   CK(ensure(t->leaf_node, nn * 4));
   CK(ensure(t->leaf_first, nn * 8));
+  CK(ensure(t->leaf_count, nn * 4));
   CK(ensure(t->leaf_pbox, nn * 32));
   CK(ensure(t->leaf_pinv, nn * 8));
   CK(ensure(t->depth_count, 64 * 4));
   CK(cudaMemsetAsync(t->depth_count.p, 0, 64 * 4, s));
-  v = make_view(t, pts);
+  v = make_view(t, t->pts);
   RUN(launch_build_nodes(v, t->slots.as<uint64_t>(), s));
   RUN(launch_number_leaves(v, scr, s));
   RUN(launch_depth_lists(v, t->depth_count.as<uint32_t>(), s));
@@ -393,12 +440,11 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   if ((r = read_state(t, s))) return r;
   if ((r = check_errors(t, s))) return r;
   t->n_leaves = (uint32_t)t->host_state->count_a;
-  v = make_view(t, pts);
+  v = make_view(t, t->pts);
   RUN(launch_leaf_offsets(v, scr, s));
   RUN(launch_leaf_parent_boxes(v, s));
   RUN(launch_targets(v, s));
   for (auto& rd : t->rounds) RUN(launch_targets_ext(v, rd.first, rd.count, rd.ext, s));
-  // per-depth inner-node lists for the voxelizer
   uint32_t off = 0;
   for (int d = 0; d <= kMaxDepth; ++d) t->inner_off[d] = off, off += t->inner_per_depth[d];
   CK(ensure(t->depth_lists, (size_t)std::max<uint32_t>(off, 1) * 4));
@@ -408,16 +454,24 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   CK(cudaMemsetAsync(t->depth_cursor.p, 0, 64 * 4, s));
   RUN(launch_depth_scatter(v, t->depth_off.as<uint32_t>(), t->depth_cursor.as<uint32_t>(),
                            t->depth_lists.as<uint32_t>(), s));
+  for (int a = 0; a < 3; ++a) t->world[a] = t->host_state->lo[a];
+  t->world[3] = t->host_state->size;
+  t->inv_world = t->host_state->inv_size;
   mark(t, 3, s);
+  return LOD_OK;
+}
 
-  // ---- distribute (partition.py:244-271) ----
-  CK(ensure(t->leaf_pts, n * rec));
+// Stable distribute of the local points into their leaves (partition.py:244-271).  Uses
+// t->leaf_count (per leaf, this process's points) for the digit bases and offsets.
+int phase_distribute(lod_tree* t, cudaStream_t s) {
+  const uint64_t n = t->n;
+  const size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
+  CK(ensure(t->leaf_pts, std::max<uint64_t>(n, 1) * rec));
   RadixPlan& p = t->plan;
   int bits = ceil_log2(t->n_leaves);
   if (bits > 2 * kRadixMaxBits)
     return fail(LOD_EUNSUPPORTED, "%u leaves exceed the 2-pass distribute limit", t->n_leaves);
-  // a root leaf needs no stash; any other tree takes at least one (stable) pass
-  p.passes = t->n_nodes == 1 ? 0 : (bits <= kRadixMaxBits ? 1 : 2);
+  p.passes = (t->n_nodes == 1 || n == 0) ? 0 : (bits <= kRadixMaxBits ? 1 : 2);
   p.bits[0] = p.passes == 2 ? bits / 2 : bits;
   p.bits[1] = p.passes == 2 ? bits - bits / 2 : 0;
   p.tiles = (uint32_t)((n + kRadixTile - 1) / kRadixTile);
@@ -426,11 +480,7 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
     uint64_t words = (uint64_t)p.tiles << maxb;
     size_t old = t->status.cap;
     CK(ensure(t->status, words * 8));
-    if (t->status.cap != old) {  // fresh memory: clear once, epochs keep it valid afterwards
-      CK(cudaMemsetAsync(t->status.p, 0, t->status.cap, s));
-      t->epoch = 1;
-    }
-    if (t->epoch + 4 > 0xFFFF) {
+    if (t->status.cap != old || t->epoch + 4 > 0xFFFF) {  // fresh memory / epoch wrap: clear once
       CK(cudaMemsetAsync(t->status.p, 0, t->status.cap, s));
       t->epoch = 1;
     }
@@ -447,35 +497,86 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
     p.tmp_rec = t->tmp_rec.p;
     p.tmp_leaf = t->tmp_leaf.as<uint32_t>();
     p.epoch = t->epoch;
-
   }
-  v = make_view(t, pts);
-  RUN(launch_distribute(fmt, v, p, t->leaf_pts.p, s));
+  SplitView v = make_view(t, t->pts);
+  RUN(launch_distribute(t->fmt, v, p, t->leaf_pts.p, s));
   if (p.passes) t->epoch = p.epoch;
   mark(t, 4, s);
-  if ((r = read_state(t, s))) return r;
+  int r = read_state(t, s);
+  if (r) return r;
   if ((r = check_errors(t, s))) return r;
-  if (t->host_state->count_b != n) return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
-  for (int a = 0; a < 3; ++a) t->world[a] = t->host_state->lo[a];
-  t->world[3] = t->host_state->size;
-  t->inv_world = t->host_state->inv_size;
   CK(cudaGetLastError());
+  return LOD_OK;
+}
+
+int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub, const lod_config* cfg,
+             cudaStream_t s) {
+  if (t) t->dist = false;
+  int r = phase_init(t, pts, n, fmt, ub, cfg, s);
+  if (r) return r;
+  t->n_global = n;
+  if ((r = phase_bounds(t, ub, s)) || (r = phase_count(t, s))) return r;
+  uint32_t cur = 0;
+  if ((r = phase_anchors(t, &cur, s))) return r;
+  while (cur > 0) {
+    if ((r = phase_round(t, s)) || (r = phase_subanchors(t, &cur, s))) return r;
+  }
+  if ((r = phase_skeleton(t, s)) || (r = phase_distribute(t, s))) return r;
+  if (t->host_state->count_b != n) return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
   t->split_done = true;
   return LOD_OK;
 }
 
-int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
+// Optional restriction of a voxelize call (multi-GPU): which inner nodes to sample here,
+// whether to keep the arena's current contents, and voxel runs imported from other GPUs.
+struct VoxPlan {
+  const uint8_t* mask = nullptr;      // per node: 1 = sample here (host)
+  bool append = false;                // keep the arena and earlier results
+  const int32_t* imp_nodes = nullptr; // imported inner nodes (host)
+  const uint32_t* imp_counts = nullptr;
+  uint32_t n_imp = 0;
+  uint32_t imp_slot_base = 0;         // first parity slot free for imports at their depth
+  const void* d_imp_vox = nullptr;    // their voxels, concatenated (device)
+};
+
+int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxPlan* plan = nullptr) {
   if (!t || !t->split_done) return fail(LOD_EVALUE, "lod_voxelize before a successful lod_split");
   if (mode != LOD_MODE_RANDOM && mode != LOD_MODE_AVERAGE)
     return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
   CK(cudaSetDevice(t->device));
   t->voxel_mode = -1;
-  t->n_voxels = 0;
-  uint32_t inner_total = 0, widest = 0;
-  for (int d = 0; d <= kMaxDepth; ++d)
-    inner_total += t->inner_per_depth[d], widest = std::max(widest, t->inner_per_depth[d]);
+  if (!(plan && plan->append)) t->n_voxels = 0;
+  uint32_t widest = 0;
+  for (int d = 0; d <= kMaxDepth; ++d) widest = std::max(widest, t->inner_per_depth[d]);
+  // per-depth work lists: all inner nodes, or the plan's subset (+ imports)
+  uint32_t lst_n[kMaxDepth + 1] = {}, lst_off[kMaxDepth + 1] = {}, imp_n[kMaxDepth + 1] = {},
+           imp_off[kMaxDepth + 1] = {};
+  const uint32_t* d_lists = t->depth_lists.as<uint32_t>();
+  const uint32_t* d_imp = nullptr;
+  if (plan) {
+    std::vector<uint64_t> cell(t->n_nodes);
+    std::vector<uint32_t> val(t->n_nodes);
+    CK(cudaMemcpy(cell.data(), t->n_cell.p, 8ull * t->n_nodes, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(val.data(), t->n_val.p, 4ull * t->n_nodes, cudaMemcpyDeviceToHost));
+    std::vector<std::vector<uint32_t>> by(kMaxDepth + 1), ib(kMaxDepth + 1);
+    for (uint32_t k = 0; k < t->n_nodes; ++k)
+      if (val[k] == UNMERGEABLE && plan->mask && plan->mask[k]) by[(cell[k] >> 48) & 0xFF].push_back(k);
+    for (uint32_t i = 0; i < plan->n_imp; ++i) ib[(cell[plan->imp_nodes[i]] >> 48) & 0xFF].push_back(plan->imp_nodes[i]);
+    std::vector<uint32_t> flat;
+    for (int d = 0; d <= kMaxDepth; ++d) lst_off[d] = flat.size(), lst_n[d] = by[d].size(), flat.insert(flat.end(), by[d].begin(), by[d].end());
+    for (int d = 0; d <= kMaxDepth; ++d) imp_off[d] = flat.size(), imp_n[d] = ib[d].size(), flat.insert(flat.end(), ib[d].begin(), ib[d].end());
+    for (int d = 0; d <= kMaxDepth; ++d) widest = std::max(widest, plan->imp_slot_base + imp_n[d]);
+    CK(ensure(t->plan_lists, std::max<size_t>(flat.size(), 1) * 4));
+    if (!flat.empty()) CK(cudaMemcpyAsync(t->plan_lists.p, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice, s));
+    d_lists = t->plan_lists.as<uint32_t>();
+    d_imp = d_lists;
+  } else {
+    for (int d = 0; d <= kMaxDepth; ++d) lst_n[d] = t->inner_per_depth[d], lst_off[d] = t->inner_off[d];
+  }
+  uint32_t total = 0;
+  for (int d = 0; d <= kMaxDepth; ++d) total += lst_n[d] + imp_n[d];
   mark(t, 4, s);
-  if (inner_total == 0) {  // single-leaf root: nothing to voxelize (test_sampling.py:163-166)
+  if (total == 0 && !(plan && plan->n_imp)) {  // single-leaf root: nothing to voxelize (test_sampling.py:163-166)
     t->voxel_mode = mode;
     mark(t, 5, s);
     return LOD_OK;
@@ -483,19 +584,23 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
   const uint64_t kWordsPerNode = 1ull << 16;
-  CK(ensure(t->vbits, 2ull * widest * kWordsPerNode * 4));
-  CK(ensure(t->vpre, 2ull * widest * kWordsPerNode * 4));
-  CK(ensure(t->vinfo, 2ull * widest * sizeof(VoxNode)));
+  const size_t keep = plan && plan->append;
+  CK(ensure(t->vbits, 2ull * widest * kWordsPerNode * 4, keep ? t->vbits.cap : 0, s));
+  CK(ensure(t->vpre, 2ull * widest * kWordsPerNode * 4, keep ? t->vpre.cap : 0, s));
+  CK(ensure(t->vinfo, 2ull * widest * sizeof(VoxNode), keep ? t->vinfo.cap : 0, s));
   CK(ensure(t->vblk, (size_t)widest * 16 * 4));
   CK(ensure(t->vcount, 64 * 4 * (kMaxDepth + 1)));
   CK(ensure(t->vlevel_start, 8 * (kMaxDepth + 1)));
-  CK(ensure(t->node_slot, (size_t)t->n_nodes * 4));
-  uint64_t cap = std::max<uint64_t>(t->n + t->n / 2, 1ull << 21);
+  CK(ensure(t->node_slot, (size_t)t->n_nodes * 4, keep ? t->node_slot.cap : 0, s));
+  uint64_t imp_total = 0;
+  for (uint32_t i = 0; plan && i < plan->n_imp; ++i) imp_total += plan->imp_counts[i];
+  const uint64_t base_cursor = keep ? t->n_voxels : 0;
+  uint64_t cap = std::max<uint64_t>(t->n + t->n / 2, 1ull << 21) + base_cursor + imp_total;
   if (t->vox.cap / 8 > cap) cap = t->vox.cap / 8;
   uint64_t acc_cap = std::max<uint64_t>(t->n / 2, 1ull << 21);
   if (t->vacc.cap / 16 > acc_cap) acc_cap = t->vacc.cap / 16;
   for (int attempt = 0; attempt < 8; ++attempt) {
-    CK(ensure(t->vox, cap * 8));
+    CK(ensure(t->vox, cap * 8, base_cursor * 8, s));
     cap = t->vox.cap / 8;
     CK(ensure(t->vacc, acc_cap * 16));
     acc_cap = t->vacc.cap / 16;
@@ -506,10 +611,25 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
     CK(ensure(t->vvchunks, vchunk_cap * 8));
     CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
                        sizeof(DevState) - offsetof(DevState, err), s));
+    // arena: [earlier results][imports][this call's voxels]
+    uint64_t cursor = base_cursor;
+    if (plan && plan->n_imp) {
+      CK(cudaMemcpyAsync(t->vox.as<uint2>() + cursor, plan->d_imp_vox, imp_total * 8, cudaMemcpyDeviceToDevice, s));
+      for (uint32_t i = 0; i < plan->n_imp; ++i) {
+        uint64_t f = cursor;
+        uint32_t c = plan->imp_counts[i];
+        CK(cudaMemcpyAsync(t->n_first.as<uint64_t>() + plan->imp_nodes[i], &f, 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(t->n_count.as<uint32_t>() + plan->imp_nodes[i], &c, 4, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // host sources are stack values
+        cursor += c;
+      }
+    }
+    CK(cudaMemcpyAsync((char*)t->state.p + offsetof(DevState, vox_cursor), &cursor, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
     CK(cudaMemsetAsync(t->vcount.p, 0, 64 * 4 * (kMaxDepth + 1), s));
     VoxLevel L{};
     L.st = t->state.as<DevState>();
-    CK(ensure(t->stash, t->n * 8));
+    CK(ensure(t->stash, std::max<uint64_t>(t->n, 1) * 8));
     L.stash = t->stash.as<uint2>();
     L.fmt = t->fmt;
     L.leaf_pts = t->leaf_pts.p;
@@ -535,19 +655,28 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
     L.mode = mode;
     L.seed = seed;
     for (int d = kMaxDepth; d >= 0; --d) {  // deepest first (sampling.py:171)
-      if (!t->inner_per_depth[d]) continue;
-      L.list = t->depth_lists.as<uint32_t>() + t->inner_off[d];
-      L.list_n = t->inner_per_depth[d];
+      if (!lst_n[d] && !imp_n[d]) continue;
       L.parity = d & 1;
-      L.chunk = voxelize_chunk(L.list_n);
-      L.vchunk = voxelize_vchunk(L.list_n);
       L.info = t->vinfo.as<VoxNode>() + (size_t)L.parity * widest;
       L.cinfo = t->vinfo.as<VoxNode>() + (size_t)(L.parity ^ 1) * widest;
       L.counters = t->vcount.as<uint32_t>() + 64 * d;
       L.level_start = t->vlevel_start.as<uint64_t>() + d;
-      CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
-                         (size_t)L.list_n * kWordsPerNode * 4, s));
-      RUN(launch_voxelize_level(L, sms, s));
+      if (lst_n[d]) {
+        L.list = d_lists + lst_off[d];
+        L.list_n = lst_n[d];
+        L.chunk = voxelize_chunk(L.list_n);
+        L.vchunk = voxelize_vchunk(L.list_n);
+        CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
+                           (size_t)L.list_n * kWordsPerNode * 4, s));
+        RUN(launch_voxelize_level(L, sms, s));
+      }
+      if (imp_n[d]) {
+        L.list = d_imp + imp_off[d];
+        L.list_n = imp_n[d];
+        CK(cudaMemsetAsync(L.bits + ((size_t)L.parity * widest + plan->imp_slot_base) * kWordsPerNode, 0,
+                           (size_t)L.list_n * kWordsPerNode * 4, s));
+        RUN(launch_voxelize_import(L, plan->imp_slot_base, s));
+      }
     }
     int r = read_state(t, s);
     if (r) return r;
@@ -565,6 +694,122 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s) {
     return LOD_OK;
   }
   return fail(LOD_ECUDA, "voxel arena could not be sized");
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU stages (driven by paper_2302_14801_b200/dist.py)
+// ---------------------------------------------------------------------------
+int dist_begin(lod_tree* t, const void* pts, uint64_t n, int fmt, const lod_config* cfg, double* out6,
+               cudaStream_t s) {
+  if (t) t->dist = true;
+  int r = phase_init(t, pts, n, fmt, nullptr, cfg, s);
+  if (r) return r;
+  t->dist_stage = 1;
+  for (int a = 0; a < 3; ++a) out6[a] = INFINITY, out6[3 + a] = -INFINITY;
+  if (n == 0) return LOD_OK;
+  if ((r = phase_bounds(t, nullptr, s)) || (r = read_state(t, s))) return r;
+  if ((r = check_errors(t, s))) return r;
+  for (int a = 0; a < 3; ++a) {  // decode the order-preserving keys on the host
+    uint64_t lk = t->host_state->lo_key[a], hk = t->host_state->hi_key[a];
+    uint64_t lu = (lk >> 63) ? (lk & 0x7FFFFFFFFFFFFFFFull) : ~lk, hu = (hk >> 63) ? (hk & 0x7FFFFFFFFFFFFFFFull) : ~hk;
+    memcpy(&out6[a], &lu, 8);
+    memcpy(&out6[3 + a], &hu, 8);
+  }
+  return LOD_OK;
+}
+
+int dist_count(lod_tree* t, uint64_t n_global, const double* world, lod_span* out, cudaStream_t s) {
+  if (!t || t->dist_stage != 1) return fail(LOD_EVALUE, "lod_dist_count out of order");
+  t->n_global = n_global;
+  SplitView v = make_view(t, t->pts);
+  RUN(launch_bounds(t->fmt, t->pts, t->n, v.st, world, s));  // forced (global) cube
+  int r = phase_count(t, s);
+  if (r) return r;
+  const uint64_t fine = 1ull << (3 * t->cfg.initial_depth);
+  CK(ensure(t->local_main, fine * 4));
+  CK(cudaMemcpyAsync(t->local_main.p, t->pyr.as<uint32_t>() + level_off(t->cfg.initial_depth), fine * 4,
+                     cudaMemcpyDeviceToDevice, s));
+  out->ptr = t->pyr.as<uint32_t>() + level_off(t->cfg.initial_depth);
+  out->n = fine;
+  t->dist_stage = 2;
+  return LOD_OK;
+}
+
+int dist_extend(lod_tree* t, lod_span* out, cudaStream_t s) {
+  if (!t || (t->dist_stage != 2 && t->dist_stage != 3)) return fail(LOD_EVALUE, "lod_dist_extend out of order");
+  out->ptr = nullptr;
+  out->n = 0;
+  uint32_t cur = 0;
+  int r = t->dist_stage == 2 ? phase_anchors(t, &cur, s) : phase_subanchors(t, &cur, s);
+  if (r) return r;
+  if (cur == 0) {
+    t->dist_stage = 4;
+    return LOD_OK;
+  }
+  const uint64_t before = t->ext_pyr_used;
+  if ((r = phase_round(t, s))) return r;
+  const uint64_t main_cells = level_off(t->cfg.initial_depth + 1);
+  const uint64_t n_new = t->ext_pyr_used - before;
+  CK(ensure(t->local_ext, t->ext_pyr_used * 4, before * 4, s));
+  CK(cudaMemcpyAsync(t->local_ext.as<uint32_t>() + before, t->pyr.as<uint32_t>() + main_cells + before, n_new * 4,
+                     cudaMemcpyDeviceToDevice, s));
+  out->ptr = t->pyr.as<uint32_t>() + main_cells + before;
+  out->n = n_new;
+  t->dist_stage = 3;
+  return LOD_OK;
+}
+
+int dist_skeleton(lod_tree* t, uint32_t* h_counts, cudaStream_t s) {
+  if (!t || t->dist_stage != 4) return fail(LOD_EVALUE, "lod_dist_skeleton out of order");
+  int r = phase_skeleton(t, s);
+  if (r) return r;
+  std::vector<uint32_t> rf, rc;
+  std::vector<int> re;
+  std::vector<uint64_t> rb;
+  for (auto& rd : t->rounds) rf.push_back(rd.first), rc.push_back(rd.count), re.push_back(rd.ext), rb.push_back(rd.pyr_base);
+  SplitView v = make_view(t, t->pts);
+  RUN(launch_local_leaf_counts(v, t->local_main.as<uint32_t>(), t->local_ext.as<uint32_t>(), rf.data(), rc.data(),
+                               re.data(), rb.data(), (int)t->rounds.size(), s));
+  ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+  RUN(launch_leaf_offsets_local(v, scr, s));
+  if ((r = phase_distribute(t, s))) return r;
+  if (t->host_state->count_b != t->n)
+    return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
+  if (h_counts) CK(cudaMemcpy(h_counts, t->leaf_count.p, 4ull * t->n_leaves, cudaMemcpyDeviceToHost));
+  t->split_done = true;
+  t->dist_stage = 5;
+  return LOD_OK;
+}
+
+int dist_copy_segments(lod_tree* t, const void* src, void* dst, const uint64_t* hs, const uint64_t* hd,
+                       const uint32_t* hc, uint64_t nseg, cudaStream_t s) {
+  if (!t) return fail(LOD_EVALUE, "null tree");
+  if (!nseg) return LOD_OK;
+  CK(ensure(t->seg, nseg * 20));
+  uint64_t* ds = t->seg.as<uint64_t>();
+  CK(cudaMemcpyAsync(ds, hs, nseg * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ds + nseg, hd, nseg * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ds + 2 * nseg, hc, nseg * 4, cudaMemcpyHostToDevice, s));
+  RUN(launch_copy_segments(src ? src : t->leaf_pts.p, dst ? dst : t->leaf_pts.p, ds, ds + nseg,
+                           reinterpret_cast<uint32_t*>(ds + 2 * nseg), nseg, t->fmt == LOD_POINTS_F32 ? 16 : 32, s));
+  CK(cudaStreamSynchronize(s));
+  return LOD_OK;
+}
+
+int dist_adopt(lod_tree* t, const void* recs, uint64_t n, const uint32_t* h_counts, cudaStream_t s) {
+  if (!t || t->dist_stage != 5) return fail(LOD_EVALUE, "lod_dist_adopt out of order");
+  const size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
+  CK(ensure(t->leaf_pts, std::max<uint64_t>(n, 1) * rec));
+  if (n) CK(cudaMemcpyAsync(t->leaf_pts.p, recs, n * rec, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(t->leaf_count.p, h_counts, 4ull * t->n_leaves, cudaMemcpyHostToDevice, s));
+  ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+  SplitView v = make_view(t, t->pts);
+  RUN(launch_leaf_offsets_local(v, scr, s));
+  int r = read_state(t, s);
+  if (r) return r;
+  if (t->host_state->count_b != n) return fail(LOD_EVALUE, "adopted records do not match the leaf counts");
+  t->n = n;
+  return LOD_OK;
 }
 
 }  // namespace
@@ -588,11 +833,11 @@ void lod_tree_destroy(lod_tree* t) {
   cudaSetDevice(t->device);
   DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan, &t->slots,
                    &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid, &t->n_lvl,
-                   &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node, &t->leaf_first,
+                   &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node, &t->leaf_first, &t->leaf_count,
                    &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
                    &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
-                   &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks};
+                   &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -685,11 +930,11 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
   const DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan,
                          &t->slots, &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid,
                          &t->n_lvl, &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node,
-                         &t->leaf_first, &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists,
+                         &t->leaf_first, &t->leaf_count, &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists,
                          &t->leaf_pts, &t->status, &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf,
                          &t->vox, &t->scratch, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
-                         &t->vleaf_chunks, &t->vvchunks};
+                         &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;
@@ -725,6 +970,44 @@ int lod_generate(const char* kind, uint64_t seed, uint64_t start, uint64_t n, vo
   launch_generate(k, seed, start, n, d_out, table, (cudaStream_t)stream);
   CK(cudaGetLastError());
   return LOD_OK;
+}
+
+int lod_dist_begin(lod_tree* t, const void* d_points, uint64_t n_local, int format, const lod_config* config,
+                   double* out_min_max, void* stream) {
+  return dist_begin(t, d_points, n_local, format, config, out_min_max, (cudaStream_t)stream);
+}
+int lod_dist_count(lod_tree* t, uint64_t n_global, const double* world, lod_span* out, void* stream) {
+  return dist_count(t, n_global, world, out, (cudaStream_t)stream);
+}
+int lod_dist_extend(lod_tree* t, lod_span* out, void* stream) { return dist_extend(t, out, (cudaStream_t)stream); }
+int lod_dist_skeleton(lod_tree* t, uint32_t* h_local_leaf_counts, void* stream) {
+  return dist_skeleton(t, h_local_leaf_counts, (cudaStream_t)stream);
+}
+int lod_dist_leaf_counts(const lod_tree* tc, uint32_t* h) {
+  lod_tree* t = const_cast<lod_tree*>(tc);
+  if (!t || t->dist_stage < 5) return fail(LOD_EVALUE, "no distributed split");
+  CK(cudaMemcpy(h, t->leaf_count.p, 4ull * t->n_leaves, cudaMemcpyDeviceToHost));
+  return LOD_OK;
+}
+int lod_dist_copy_segments(lod_tree* t, const void* d_src, void* d_dst, const uint64_t* h_src, const uint64_t* h_dst,
+                           const uint32_t* h_cnt, uint64_t nseg, void* stream) {
+  return dist_copy_segments(t, d_src, d_dst, h_src, h_dst, h_cnt, nseg, (cudaStream_t)stream);
+}
+int lod_dist_adopt(lod_tree* t, const void* d_records, uint64_t n, const uint32_t* h_leaf_counts, void* stream) {
+  return dist_adopt(t, d_records, n, h_leaf_counts, (cudaStream_t)stream);
+}
+int lod_dist_voxelize(lod_tree* t, int mode, uint64_t seed, const uint8_t* h_mask, int append,
+                      const int32_t* h_imp_nodes, const uint32_t* h_imp_counts, uint32_t n_imp, uint32_t imp_slot_base,
+                      const void* d_imp_vox, void* stream) {
+  VoxPlan p;
+  p.mask = h_mask;
+  p.append = append != 0;
+  p.imp_nodes = h_imp_nodes;
+  p.imp_counts = h_imp_counts;
+  p.n_imp = n_imp;
+  p.imp_slot_base = imp_slot_base;
+  p.d_imp_vox = d_imp_vox;
+  return do_voxelize(t, mode, seed, (cudaStream_t)stream, &p);
 }
 
 const char* lod_last_error(void) { return g_err.c_str(); }

@@ -205,11 +205,11 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
 }
 
 // Global exclusive prefix per digit, from the leaf counts (leaf ids are the sort keys).
-__global__ void k_digit_hist(const uint32_t* n_val, const uint32_t* leaf_node, uint32_t n_leaves, int shift,
-                             int bits, unsigned long long* hist) {
+__global__ void k_digit_hist(const uint32_t* leaf_count, uint32_t n_leaves, int shift, int bits,
+                             unsigned long long* hist) {
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_leaves) return;
-  atomicAdd(hist + ((j >> shift) & ((1u << bits) - 1)), (unsigned long long)n_val[leaf_node[j]]);
+  atomicAdd(hist + ((j >> shift) & ((1u << bits) - 1)), (unsigned long long)leaf_count[j]);
 }
 
 __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
@@ -242,7 +242,7 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
   cudaMemsetAsync(p.digit_base, 0, (size_t)(B0 + B1) * 8, s);
   cudaMemsetAsync(p.tile_ticket, 0, 2 * sizeof(uint32_t), s);
   uint32_t lb = ceil_div_u32(v.n_leaves, 256);
-  k_digit_hist<<<lb, 256, 0, s>>>(v.n_val, v.leaf_node, v.n_leaves, 0, p.bits[0],
+  k_digit_hist<<<lb, 256, 0, s>>>(v.leaf_count, v.n_leaves, 0, p.bits[0],
                                   reinterpret_cast<unsigned long long*>(base0));
   k_digit_scan<<<1, 1024, 0, s>>>(base0, B0);
   launches += 2;
@@ -251,7 +251,7 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
     p.epoch++;
     return launches + 1;
   }
-  k_digit_hist<<<lb, 256, 0, s>>>(v.n_val, v.leaf_node, v.n_leaves, p.bits[0], p.bits[1],
+  k_digit_hist<<<lb, 256, 0, s>>>(v.leaf_count, v.n_leaves, p.bits[0], p.bits[1],
                                   reinterpret_cast<unsigned long long*>(base1));
   k_digit_scan<<<1, 1024, 0, s>>>(base1, B1);
   run_pass<FMT, true, false>(v, v.pts, nullptr, p.tmp_rec, p.tmp_leaf, 0, p.bits[0], base0, p, p.tile_ticket, s);

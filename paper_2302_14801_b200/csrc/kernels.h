@@ -40,6 +40,7 @@ struct SplitView {
   uint32_t n_nodes;
   uint32_t* leaf_node;
   uint64_t* leaf_first;
+  uint32_t* leaf_count;   // per leaf: points of THIS process (global count on one GPU)
   double4* leaf_pbox;     // per leaf: parent bounds (w < 0 for a root leaf)
   double* leaf_pinv;      // per leaf: RN(1 / parent size)
   uint32_t n_leaves;
@@ -96,6 +97,7 @@ int launch_count_nodes(const SplitView& v, uint64_t total_slots, uint64_t* slots
 int launch_build_nodes(const SplitView& v, const uint64_t* slots, cudaStream_t s);
 int launch_number_leaves(const SplitView& v, ScanScratch& scr, cudaStream_t s);
 int launch_leaf_offsets(const SplitView& v, ScanScratch& scr, cudaStream_t s);
+int launch_leaf_offsets_local(const SplitView& v, ScanScratch& scr, cudaStream_t s);
 int launch_leaf_parent_boxes(const SplitView& v, cudaStream_t s);
 int launch_targets(const SplitView& v, cudaStream_t s);
 int launch_targets_ext(const SplitView& v, uint32_t first, uint32_t count, int ext, cudaStream_t s);
@@ -172,10 +174,20 @@ struct VoxLevel {
   uint64_t seed;
 };
 int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s);
+int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s);
 uint32_t voxelize_chunk(uint32_t nodes);
 uint32_t voxelize_vchunk(uint32_t nodes);
 uint64_t voxelize_chunk_capacity(uint64_t samples, uint32_t nodes);
 uint64_t voxelize_vchunk_capacity(uint64_t voxels, uint32_t nodes);
+
+// --- multi-GPU helpers (dist_kernels.cu) ---
+// per-leaf counts of this process's points from its saved (pre all-reduce) counting grids
+int launch_local_leaf_counts(const SplitView& v, const uint32_t* local_main, const uint32_t* local_ext,
+                             const uint32_t* round_first, const uint32_t* round_count, const int* round_ext,
+                             const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s);
+// copy nseg record segments (src, dst, count in records; rec_bytes 16 or 32)
+int launch_copy_segments(const void* src, void* dst, const uint64_t* seg_src, const uint64_t* seg_dst,
+                         const uint32_t* seg_cnt, uint64_t nseg, int rec_bytes, cudaStream_t s);
 
 // --- generators (generate.cu) ---
 int launch_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, void* out, const double* table,

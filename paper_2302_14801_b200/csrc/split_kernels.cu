@@ -514,15 +514,18 @@ int launch_number_leaves(const SplitView& v, ScanScratch& scr, cudaStream_t s) {
 
 // Leaf allocation = exclusive prefix of leaf counts (partition.py:264-265 searchsorted bounds)
 struct LeafOffF {
-  const uint32_t* val;
+  const uint32_t* val;       // per node (pyramid counts) or null
+  const uint32_t* cnt;       // per leaf counts when val is null
   const uint32_t* leaf_node;
   uint64_t* leaf_first;
+  uint32_t* leaf_count;
   uint64_t* n_first;
   uint32_t* n_count;
-  __device__ uint64_t value(uint64_t j) const { return val[leaf_node[j]]; }
+  __device__ uint64_t value(uint64_t j) const { return val ? val[leaf_node[j]] : cnt[j]; }
   __device__ void store(uint64_t j, uint64_t ex, uint64_t v) const {
     uint32_t k = leaf_node[j];
     leaf_first[j] = ex;
+    leaf_count[j] = (uint32_t)v;
     n_first[k] = ex;
     n_count[k] = (uint32_t)v;
   }
@@ -550,7 +553,13 @@ int launch_leaf_parent_boxes(const SplitView& v, cudaStream_t s) {
 }
 
 int launch_leaf_offsets(const SplitView& v, ScanScratch& scr, cudaStream_t s) {
-  LeafOffF f{v.n_val, v.leaf_node, v.leaf_first, v.n_first, v.n_count};
+  LeafOffF f{v.n_val, nullptr, v.leaf_node, v.leaf_first, v.leaf_count, v.n_first, v.n_count};
+  return device_scan(v.n_leaves, f, scr, nullptr, &v.st->count_b, s);
+}
+
+// multi-GPU: leaf offsets from this process's per-leaf counts (already in leaf_count)
+int launch_leaf_offsets_local(const SplitView& v, ScanScratch& scr, cudaStream_t s) {
+  LeafOffF f{nullptr, v.leaf_count, v.leaf_node, v.leaf_first, v.leaf_count, v.n_first, v.n_count};
   return device_scan(v.n_leaves, f, scr, nullptr, &v.st->count_b, s);
 }
 

@@ -478,6 +478,95 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Import path (multi-GPU, rank 0): inner nodes whose voxels were computed on another GPU.
+// Their rank structures (bitmap + prefix) are rebuilt from the voxel keys in slots
+// [slot_base, slot_base + list_n) of the level's parity buffer, so the next level up can
+// gather from them exactly like from locally voxelized children.
+// ---------------------------------------------------------------------------
+__global__ void k_import_setup(VoxLevel L, uint32_t slot_base) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.list_n) return;
+  const uint32_t node = L.list[i], s = slot_base + i;
+  VoxNode info{};
+  info.node = node;
+  info.vbase = L.n_first[node];
+  info.m = L.n_count[node];
+  L.info[s] = info;
+  L.node_slot[node] = s;
+}
+
+__global__ void __launch_bounds__(kT) k_import_bits(VoxLevel L, uint32_t slot_base) {
+  const uint32_t i = blockIdx.x / kBlksPerNode, part = blockIdx.x % kBlksPerNode;
+  const VoxNode& nd = L.info[slot_base + i];
+  uint32_t* bits = bits_of(L, L.parity, slot_base + i);
+  const uint32_t per = (nd.m + kBlksPerNode - 1) / kBlksPerNode;
+  const uint32_t r0 = part * per, r1 = min(nd.m, r0 + per);
+  for (uint32_t r = r0 + threadIdx.x; r < r1; r += kT) {
+    const uint32_t key = __ldg(&L.vox[nd.vbase + r].x);
+    atomicOr(bits + (key >> 5), 1u << (key & 31));
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_import_block_sums(VoxLevel L, uint32_t slot_base) {
+  const uint32_t s = slot_base + blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
+  __shared__ uint32_t red[kT / 32];
+  const uint4* b = reinterpret_cast<const uint4*>(bits_of(L, L.parity, s) + blk * kBlkWords);
+  uint32_t c = 0;
+  for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT) {
+    uint4 q = __ldcg(b + i);
+    c += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kT / 32; ++w) t += red[w];
+    L.blk_sum[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_import_block_prefix(VoxLevel L) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.list_n) return;
+  uint32_t run = 0;
+  for (uint32_t b = 0; b < kBlksPerNode; ++b) {
+    uint32_t v = L.blk_sum[i * kBlksPerNode + b];
+    L.blk_sum[i * kBlksPerNode + b] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_import_prefix(VoxLevel L, uint32_t slot_base) {
+  const uint32_t s = slot_base + blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
+  __shared__ uint32_t sm[kT / 32 + 1];
+  const uint32_t* bits = bits_of(L, L.parity, s) + blk * kBlkWords;
+  uint32_t* pre = pre_of(L, L.parity, s) + blk * kBlkWords;
+  constexpr uint32_t per = kBlkWords / kT;
+  uint32_t w[per], c = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < per; ++q) c += __popc(w[q] = __ldcg(bits + threadIdx.x * per + q));
+  uint32_t tot;
+  uint32_t r = block_excl_scan<uint32_t, kT>(c, &tot, sm) + L.blk_sum[blockIdx.x];
+#pragma unroll
+  for (uint32_t q = 0; q < per; ++q) {
+    pre[threadIdx.x * per + q] = r;
+    r += __popc(w[q]);
+  }
+}
+
+int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s) {
+  if (!L.list_n) return 0;
+  k_import_setup<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L, slot_base);
+  k_import_bits<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
+  k_import_block_sums<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
+  k_import_block_prefix<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L);
+  k_import_prefix<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
+  return 5;
+}
+
 // Runs one depth level; returns launches.  counters[0..2] must be zero on entry and the
 // level's bitmaps cleared.
 int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s) {
