@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--stages", action="store_true", help="also print per-stage device times to stderr")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collectives for --gpus > 1 (gloo = host-staged, for testing on one GPU)")
     return ap.parse_args()
 
 
@@ -192,10 +194,14 @@ def main():
         return run_reference(args)
     import torch
     rank, world, local = dist_env()
+    local %= max(torch.cuda.device_count(), 1)   # (>1 rank per GPU only in --backend gloo tests)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_2302_14801_b200 import _abi
     from paper_2302_14801_b200.device import DeviceTree, make_config
     from paper_2302_14801_b200.generators import CONFIGS
@@ -205,14 +211,23 @@ def main():
     mode_code = _abi.LOD_MODE_RANDOM if args.mode == "random" else _abi.LOD_MODE_AVERAGE
     cfg = make_config(50_000)
 
-    # weak scaling: rank r builds rows [r*n, (r+1)*n) of the cloud (independent shard)
+    # weak scaling: rank r holds rows [r*n, (r+1)*n) of one N*n-point cloud; for N > 1 the
+    # ranks build ONE tree together (dist.py: all-reduced grids, subtree all-to-all, rank-0 merge)
     d_in = make_input_device(torch, kind, n, seed, start=rank * n)
     dev = DeviceTree(local)
     stream = torch.cuda.current_stream()
     sptr = C.c_void_p(stream.cuda_stream)
+    if world > 1:
+        from paper_2302_14801_b200.dist import RankBuilder, TorchComm, build_distributed
+        comm = TorchComm()
+        rb = RankBuilder(rank, world, dev=dev)
 
-    def step():
-        dev.build(d_in, n, _abi.LOD_POINTS_F32, cfg, mode_code, 0, stream=sptr)
+    def step(src=None):
+        src = d_in if src is None else src
+        if world > 1:
+            build_distributed(comm, src, n, _abi.LOD_POINTS_F32, args.mode, 0, builder=rb)
+        else:
+            dev.build(src, n, _abi.LOD_POINTS_F32, cfg, mode_code, 0, stream=sptr)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -252,16 +267,16 @@ def main():
         rec_bytes = n * 16
         h_in = torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True)
         h_in.copy_(d_in.cpu())
-        h_leaf = torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True)
+        h_leaf = torch.empty(rec_bytes * (2 if world > 1 else 1), dtype=torch.uint8, pin_memory=True)
         vox_bytes = info.n_voxels * 8
-        h_vox = torch.empty(max(vox_bytes, 8), dtype=torch.uint8, pin_memory=True)
+        h_vox = torch.empty(max(vox_bytes, 8) * (2 if world > 1 else 1), dtype=torch.uint8, pin_memory=True)
         h_nodes = np.zeros(info.n_nodes, _abi.node_dtype())
         d_stage = torch.empty(rec_bytes, dtype=torch.uint8, device="cuda")
         lib = dev.lib
 
         def e2e_step():
             d_stage.copy_(h_in, non_blocking=True)
-            dev.build(d_stage, n, _abi.LOD_POINTS_F32, cfg, mode_code, 0, stream=sptr)
+            step(d_stage)
             _abi.check(lib.lod_tree_copy_leaf_points(dev.h, C.c_void_p(h_leaf.data_ptr()), sptr))
             _abi.check(lib.lod_tree_copy_voxels(dev.h, C.c_void_p(h_vox.data_ptr()), sptr))
             _abi.check(lib.lod_tree_copy_nodes(dev.h, h_nodes.ctypes.data_as(C.c_void_p), sptr))
@@ -316,7 +331,8 @@ def main():
             "dtype": "f64-geometry/u32-counts", "data": "synthetic",
             "config": {"workload": args.config, "points_per_gpu": n, "mode": args.mode, "T": 50_000,
                        "grid": 128, "l2": "input 16 B/pt x points > 126 MB L2, no flush",
-                       "parallelism": "independent shards" if world > 1 else "single"},
+                       "parallelism": f"subtree-sharded x{world} (NCCL all-reduce + all-to-all + rank-0 merge)"
+                       if world > 1 else "single"},
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "stages_ms": dict(zip(stage_names, stages)),
