@@ -40,7 +40,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="terrain20M")
-    ap.add_argument("--mode", default="color_filter", choices=["color_filter", "average", "random"])
+    ap.add_argument("--mode", default="color_filter",
+                    choices=["color_filter", "average", "random", "first-come", "weighted"])
     ap.add_argument("--points", type=int, default=0, help="override the config's point count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=500_000)
@@ -164,7 +165,7 @@ def run_reference(args):
     if rank != 0:
         return
     sample = min(args.cpu_sample, n)
-    mode = "average" if args.mode in ("color_filter", "average") else "random"
+    mode = "average" if args.mode in ("color_filter", "average") else args.mode
     for _ in range(args.warmup):
         cpu_reference_rate(kind, seed, min(sample, 100_000), mode)
     rates, times = [], []
@@ -174,8 +175,7 @@ def run_reference(args):
         times += t
     value = sample / (sum(times) / len(times))
     line = {
-        "impl": "reference", "metric": "LOD construction points/sec (color_filter)" if mode == "average"
-        else "LOD construction points/sec (random)",
+        "impl": "reference", "metric": f"LOD construction points/sec ({args.mode})",
         "value": value, "unit": "points/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -208,7 +208,8 @@ def main():
 
     kind, n_cfg, seed, _ = CONFIGS[args.config]
     n = args.points or n_cfg
-    mode_code = _abi.LOD_MODE_RANDOM if args.mode == "random" else _abi.LOD_MODE_AVERAGE
+    from paper_2302_14801_b200.sampling import _mode_code
+    mode_code = _mode_code(args.mode)
     cfg = make_config(50_000)
 
     # weak scaling: rank r holds rows [r*n, (r+1)*n) of one N*n-point cloud; for N > 1 the
@@ -316,7 +317,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        mode = "random" if args.mode == "random" else "average"
+        mode = "average" if args.mode in ("color_filter", "average") else args.mode
         rate, times = cpu_reference_rate(kind, seed, args.cpu_sample, mode, steps=2)
         cpu = {"value": rate, "unit": "points/s", "cores": 1, "kind": "port",
                "sample": f"first {args.cpu_sample} points of {args.config}, {mode}, numpy oracle port of "
@@ -324,8 +325,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "LOD construction points/sec (color_filter)" if mode_code else
-            "LOD construction points/sec (random)",
+            "metric": f"LOD construction points/sec ({args.mode})",
             "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64-geometry/u32-counts", "data": "synthetic",

@@ -24,8 +24,7 @@
  *   LOD_ECONSISTENCY  -> ConsistencyError  (2^20 random limit sampling.py:73-75, internal
  *                                            invariants partition.py:170,191,224,239,260,269,286)
  *   LOD_ECUDA         -> RuntimeError      (CUDA / NCCL failure)
- *   LOD_EUNSUPPORTED  -> NotImplementedError (first-come / weighted strategies, configs
- *                                            outside the supported envelope)
+ *   LOD_EUNSUPPORTED  -> NotImplementedError (configs outside the supported envelope)
  */
 #ifndef LODB200_H
 #define LODB200_H
@@ -48,10 +47,14 @@ enum lod_point_format {
   LOD_POINTS_F64 = 1  /* 32 B: double x, y, z; uint8 r, g, b, pad[5] */
 };
 
-/* Voxel sampling strategies (model.py:127 STRATEGIES, restricted to the GPU path). */
+/* Voxel sampling strategies (model.py:127 STRATEGIES). */
 enum lod_mode {
-  LOD_MODE_RANDOM = 0,  /* sampling.py:69-85 */
-  LOD_MODE_AVERAGE = 1  /* sampling.py:88-97 ("color_filter") */
+  LOD_MODE_RANDOM = 0,     /* sampling.py:69-85 */
+  LOD_MODE_AVERAGE = 1,    /* sampling.py:88-97 ("color_filter") */
+  LOD_MODE_FIRST_COME = 2, /* sampling.py:61-66, the reference default (model.py:115); voxels
+                              listed by winning sample ordinal, not by key */
+  LOD_MODE_WEIGHTED = 3    /* sampling.py:100-133; colours within +-1 per channel of the
+                              reference's sequential fp64 sums */
 };
 
 /* BuildConfig (model.py:108-124). grid_size is not a field: the reference never reads it. */
@@ -120,7 +123,9 @@ int lod_tree_copy_nodes(const lod_tree* tree, lod_node* host_nodes, void* stream
  * leaf points: n_points records of the input format, grouped by leaf, input order within
  *              a leaf (partition.py:262 stable order);
  * voxels: n_voxels x {uint32 key = (x*128 + y)*128 + z, uint32 rgb = r | g<<8 | b<<16},
- *         per inner node ascending key (sampling.py:83-85, 97). */
+ *         per inner node in the reference's stored order: ascending key (random, average,
+ *         weighted: sampling.py:83-85, 97, 131-133) or ascending winning ordinal
+ *         (first-come: sampling.py:64-66). */
 int lod_tree_leaf_points(const lod_tree* tree, const void** d_ptr);
 int lod_tree_voxels(const lod_tree* tree, const void** d_ptr);
 

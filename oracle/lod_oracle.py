@@ -278,14 +278,15 @@ def path_hash(seed, path):
     return key
 
 
-def child_samples(sp: Split, pos, col, vox, path):
-    """Canonical sample list of an inner node -- sampling.py:21-47.
+def child_gpos(sp: Split, pos, col, vox, path):
+    """Canonical sample list of an inner node -- project_child_samples, sampling.py:21-47.
 
-    Returns (cells (S,3) int64 in the node's 128^3 grid, colors (S,3) uint8).
+    Returns (gpos (S,3) float64 grid positions in [0, 128), colors (S,3) uint8), children in
+    octant order, each child's samples in stored order (the sample ordinals, sampling.py:5-6).
     """
     lo, size = node_bounds(sp.world[0], sp.world[1], path)
     lo = np.asarray(lo)
-    cells, cols = [], []
+    gp, cols = [], []
     for o in range(8):
         cp = path + (o,)
         ch = sp.nodes.get(cp)
@@ -293,19 +294,24 @@ def child_samples(sp: Split, pos, col, vox, path):
             continue
         if ch.kind == "leaf":
             if ch.count == 0:
-                raise ConsistencyError(f"child {cp} has no samples")
-            g = (pos[ch.idx] - lo) / size * float(GRID)
-            g = np.clip(g, 0.0, np.nextafter(float(GRID), 0.0))
-            cells.append(np.floor(g).astype(np.int64))
+                raise ConsistencyError(f"child {cp} has no samples")          # sampling.py:34-35
+            g = (pos[ch.idx] - lo) / size * float(GRID)                        # sampling.py:37
+            gp.append(np.clip(g, 0.0, np.nextafter(float(GRID), 0.0)))         # sampling.py:30,38
             cols.append(col[ch.idx])
         else:
             vc, vcol = vox[cp]
             if len(vc) == 0:
                 raise ConsistencyError(f"child {cp} has no samples")
-            off = np.array([64 * (o & 1), 64 * ((o >> 1) & 1), 64 * ((o >> 2) & 1)], np.int64)
-            cells.append(off + (vc.astype(np.int64) >> 1))   # floor(off + (c + 0.5) / 2), exact
+            off = np.array([64.0 * (o & 1), 64.0 * ((o >> 1) & 1), 64.0 * ((o >> 2) & 1)])
+            gp.append(off + (vc.astype(np.float64) + 0.5) / 2.0)             # sampling.py:41-44
             cols.append(vcol)
-    return np.concatenate(cells), np.concatenate(cols)
+    return np.concatenate(gp), np.concatenate(cols)
+
+
+def child_samples(sp: Split, pos, col, vox, path):
+    """(cells (S,3) int64 in the node's 128^3 grid, colors) -- sampling.py:50-52 on child_gpos."""
+    gp, cols = child_gpos(sp, pos, col, vox, path)
+    return np.floor(gp).astype(np.int64), cols
 
 
 def _keys(cells):
@@ -343,24 +349,71 @@ def extract_average(cells, cols):
     return _coords(uk), out
 
 
+def extract_first_come(cells, cols):
+    """Smallest ordinal per cell wins; voxels listed by winning ordinal -- sampling.py:61-66."""
+    _, first = np.unique(_keys(cells), return_index=True)
+    win = np.sort(first)
+    return cells[win].astype(np.uint8), cols[win].copy()
+
+
+def extract_weighted(gpos, cols):
+    """Distance-weighted 2x2x2 mean over occupied cells -- sampling.py:100-133.
+
+    Same numpy operations in the same order as the reference, so the fp64 sums agree
+    bit-for-bit here (the GPU path is held to +-1 per channel, SPEC.md)."""
+    g = GRID
+    base = np.clip(np.floor(gpos - 0.5), 0, g - 2).astype(np.int64)
+    kp, wp, wcp = [], [], []
+    for dx in (0, 1):
+        for dy in (0, 1):
+            for dz in (0, 1):
+                cell = base + np.array([dx, dy, dz])
+                d = np.sqrt(((gpos - (cell + 0.5)) ** 2).sum(axis=1))
+                w = np.clip(1.0 - d, 0.0, 1.0)
+                kp.append((cell[:, 0] * g + cell[:, 1]) * g + cell[:, 2])
+                wp.append(w)
+                wcp.append(w[:, None] * cols)
+    keys = np.concatenate(kp)
+    weights = np.concatenate(wp)
+    wcols = np.concatenate(wcp)
+    uk, inv = np.unique(keys, return_inverse=True)
+    wsum = np.bincount(inv, weights=weights)
+    csum = np.stack([np.bincount(inv, weights=wcols[:, ch]) for ch in range(3)], axis=1)
+    occupied = np.unique(_keys(np.floor(gpos).astype(np.int64)))
+    at = np.searchsorted(uk, occupied)
+    denom = wsum[at]
+    if (denom <= 0).any():
+        raise ConsistencyError("occupied cell accumulated zero weight")          # sampling.py:129-130
+    mean = np.floor(csum[at] / denom[:, None] + 0.5)
+    return _coords(occupied), np.clip(mean, 0, 255).astype(np.uint8)
+
+
+MODES = ("first-come", "random", "average", "weighted")   # model.py:127 STRATEGIES
+
+
 def voxelize(sp: Split, pos, col, mode="average", seed=0):
     """Fill inner nodes deepest first -- build_lod, sampling.py:165-176.
 
-    Returns dict path -> (coords (m,3) u8, colors (m,3) u8).
+    Returns dict path -> (coords (m,3) u8, colors (m,3) u8) in stored order.
     """
     mode = {"color_filter": "average"}.get(mode, mode)
-    if mode not in ("random", "average"):
+    if mode not in MODES:
         raise ValueError(f"unknown sampling strategy: {mode}")
     pos = np.asarray(pos, np.float64)
     col = np.asarray(col, np.uint8)
     vox: dict = {}
     inner = sorted((p for p, nd in sp.nodes.items() if nd.kind == "inner"), key=len, reverse=True)
     for path in inner:
-        cells, cols = child_samples(sp, pos, col, vox, path)
+        gp, cols = child_gpos(sp, pos, col, vox, path)
+        cells = np.floor(gp).astype(np.int64)
         if mode == "random":
             vox[path] = extract_random(cells, cols, seed, path_hash(seed, path))
-        else:
+        elif mode == "average":
             vox[path] = extract_average(cells, cols)
+        elif mode == "first-come":
+            vox[path] = extract_first_come(cells, cols)
+        else:
+            vox[path] = extract_weighted(gp, cols)
     return vox
 
 

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "liblodb200.so")
 
 LOD_POINTS_F32, LOD_POINTS_F64 = 0, 1
-LOD_MODE_RANDOM, LOD_MODE_AVERAGE = 0, 1
+LOD_MODE_RANDOM, LOD_MODE_AVERAGE, LOD_MODE_FIRST_COME, LOD_MODE_WEIGHTED = 0, 1, 2, 3
 
 
 class LodConfig(C.Structure):

@@ -92,6 +92,7 @@ struct lod_tree {
   DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf;
   DevBuf vox, scratch, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vleaf_chunks, vvchunks;
+  DevBuf vpos, vout, obits, opre;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
   DevState* host_state = nullptr;  // pinned mirror
 
   uint32_t n_nodes = 0, n_leaves = 0, n_ext = 0, max_depth_used = 0;
@@ -102,7 +103,6 @@ struct lod_tree {
   double world[4] = {};
   double inv_world = 0;
   RadixPlan plan{};
-  uint32_t epoch = 1;
   // split phase state
   const void* pts = nullptr;
   uint64_t n_global = 0;
@@ -187,6 +187,7 @@ int check_errors(lod_tree* t, cudaStream_t s) {
   }
   if (e & ERR_EMPTY_CHILD) return fail(LOD_ECONSISTENCY, "child of node %s has no samples",
                                        node_path(h.err_detail).c_str());
+  if (e & ERR_ZERO_WEIGHT) return fail(LOD_ECONSISTENCY, "occupied cell accumulated zero weight");
   return fail(LOD_ECONSISTENCY, "device error 0x%x", e);
 }
 
@@ -474,33 +475,22 @@ int phase_distribute(lod_tree* t, cudaStream_t s) {
   p.passes = (t->n_nodes == 1 || n == 0) ? 0 : (bits <= kRadixMaxBits ? 1 : 2);
   p.bits[0] = p.passes == 2 ? bits / 2 : bits;
   p.bits[1] = p.passes == 2 ? bits - bits / 2 : 0;
-  p.tiles = (uint32_t)((n + kRadixTile - 1) / kRadixTile);
   if (p.passes) {
-    int maxb = std::max(p.bits[0], p.bits[1]);
-    uint64_t words = (uint64_t)p.tiles << maxb;
-    size_t old = t->status.cap;
-    CK(ensure(t->status, words * 8));
-    if (t->status.cap != old || t->epoch + 4 > 0xFFFF) {  // fresh memory / epoch wrap: clear once
-      CK(cudaMemsetAsync(t->status.p, 0, t->status.cap, s));
-      t->epoch = 1;
-    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
+    plan_segments(p, n, sms);
+    const int maxb = std::max(p.bits[0], p.bits[1]);
+    CK(ensure(t->status, ((size_t)p.segs << maxb) * 4));
     CK(ensure(t->digit_base, (size_t)(2 << kRadixMaxBits) * 8 * 2));
-    CK(ensure(t->ticket, 64));
-    if (p.passes == 2) {
-      CK(ensure(t->tmp_rec, n * rec));
-      CK(ensure(t->tmp_leaf, n * 4));
-    }
-    p.status = t->status.as<uint64_t>();
-    p.status_cap = t->status.cap / 8;
+    if (p.passes == 2) CK(ensure(t->tmp_rec, n * rec));
+    CK(ensure(t->tmp_leaf, n * 4 * p.passes));  // leaf ids in input order (+ sorted by the 1st digit)
+    p.counts = t->status.as<uint32_t>();
     p.digit_base = t->digit_base.as<uint64_t>();
-    p.tile_ticket = t->ticket.as<uint32_t>();
     p.tmp_rec = t->tmp_rec.p;
     p.tmp_leaf = t->tmp_leaf.as<uint32_t>();
-    p.epoch = t->epoch;
   }
   SplitView v = make_view(t, t->pts);
   RUN(launch_distribute(t->fmt, v, p, t->leaf_pts.p, s));
-  if (p.passes) t->epoch = p.epoch;
   mark(t, 4, s);
   int r = read_state(t, s);
   if (r) return r;
@@ -541,8 +531,7 @@ struct VoxPlan {
 
 int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxPlan* plan = nullptr) {
   if (!t || !t->split_done) return fail(LOD_EVALUE, "lod_voxelize before a successful lod_split");
-  if (mode != LOD_MODE_RANDOM && mode != LOD_MODE_AVERAGE)
-    return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
+  if (mode < LOD_MODE_RANDOM || mode > LOD_MODE_WEIGHTED) return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
   CK(cudaSetDevice(t->device));
   t->voxel_mode = -1;
   if (!(plan && plan->append)) t->n_voxels = 0;
@@ -597,13 +586,24 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
   const uint64_t base_cursor = keep ? t->n_voxels : 0;
   uint64_t cap = std::max<uint64_t>(t->n + t->n / 2, 1ull << 21) + base_cursor + imp_total;
   if (t->vox.cap / 8 > cap) cap = t->vox.cap / 8;
+  const uint32_t acc_stride = voxelize_acc_bytes(mode);
+  const bool fc = mode == LOD_MODE_FIRST_COME;
   uint64_t acc_cap = std::max<uint64_t>(t->n / 2, 1ull << 21);
-  if (t->vacc.cap / 16 > acc_cap) acc_cap = t->vacc.cap / 16;
+  if (t->vacc.cap / acc_stride > acc_cap) acc_cap = t->vacc.cap / acc_stride;
   for (int attempt = 0; attempt < 8; ++attempt) {
     CK(ensure(t->vox, cap * 8, base_cursor * 8, s));
     cap = t->vox.cap / 8;
-    CK(ensure(t->vacc, acc_cap * 16));
-    acc_cap = t->vacc.cap / 16;
+    CK(ensure(t->vacc, acc_cap * acc_stride));
+    acc_cap = t->vacc.cap / acc_stride;
+    // first-come: a level samples at most every leaf point once plus every child voxel
+    const uint64_t ocap = fc ? (t->n + cap) / 32 + 2ull * widest + 64 : 0;
+    if (fc) {
+      CK(ensure(t->vpos, cap * 4, base_cursor * 4, s));
+      CK(ensure(t->vout, cap * 8, base_cursor * 8, s));
+      CK(ensure(t->obits, ocap * 4));
+      CK(ensure(t->opre, ocap * 4));
+      CK(ensure(t->scan, (ocap / kScanTile + 2) * 8));
+    }
     const uint64_t chunk_cap = voxelize_chunk_capacity(t->n + cap, widest);
     const uint64_t vchunk_cap = voxelize_vchunk_capacity(cap, widest);
     CK(ensure(t->vchunks, chunk_cap * 16));
@@ -615,6 +615,8 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     uint64_t cursor = base_cursor;
     if (plan && plan->n_imp) {
       CK(cudaMemcpyAsync(t->vox.as<uint2>() + cursor, plan->d_imp_vox, imp_total * 8, cudaMemcpyDeviceToDevice, s));
+      if (fc)  // stored order; launch_voxelize_import puts the arena copy in key order
+        CK(cudaMemcpyAsync(t->vout.as<uint2>() + cursor, plan->d_imp_vox, imp_total * 8, cudaMemcpyDeviceToDevice, s));
       for (uint32_t i = 0; i < plan->n_imp; ++i) {
         uint64_t f = cursor;
         uint32_t c = plan->imp_counts[i];
@@ -654,6 +656,12 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.acc_cap = acc_cap;
     L.mode = mode;
     L.seed = seed;
+    L.vpos = t->vpos.as<uint32_t>();
+    L.vout = t->vout.as<uint2>();
+    L.obits = t->obits.as<uint32_t>();
+    L.opre = t->opre.as<uint32_t>();
+    L.ocap = ocap;
+    ScanScratch vscr{t->scan.as<uint64_t>(), t->scan.cap / 8};
     for (int d = kMaxDepth; d >= 0; --d) {  // deepest first (sampling.py:171)
       if (!lst_n[d] && !imp_n[d]) continue;
       L.parity = d & 1;
@@ -668,7 +676,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         L.vchunk = voxelize_vchunk(L.list_n);
         CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
                            (size_t)L.list_n * kWordsPerNode * 4, s));
-        RUN(launch_voxelize_level(L, sms, s));
+        RUN(launch_voxelize_level(L, sms, vscr, s));
       }
       if (imp_n[d]) {
         L.list = d_imp + imp_off[d];
@@ -837,7 +845,8 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
                    &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
-                   &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg};
+                   &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
+                   &t->vpos, &t->vout, &t->obits, &t->opre};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -857,8 +866,7 @@ int lod_voxelize(lod_tree* t, int mode, uint64_t seed, void* stream) {
 
 int lod_build(lod_tree* t, const void* d_points, uint64_t n, int format, const lod_config* config, int mode,
               uint64_t seed, void* stream) {
-  if (mode != LOD_MODE_RANDOM && mode != LOD_MODE_AVERAGE)
-    return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
+  if (mode < LOD_MODE_RANDOM || mode > LOD_MODE_WEIGHTED) return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
   int r = do_split(t, d_points, n, format, nullptr, config, (cudaStream_t)stream);
   if (r) return r;
   return do_voxelize(t, mode, seed, (cudaStream_t)stream);
@@ -901,9 +909,14 @@ int lod_tree_leaf_points(const lod_tree* t, const void** p) {
   return LOD_OK;
 }
 
+// the stored-order voxel array: first-come lists voxels by winning ordinal
+static const void* stored_voxels(const lod_tree* t) {
+  return t->voxel_mode == LOD_MODE_FIRST_COME ? t->vout.p : t->vox.p;
+}
+
 int lod_tree_voxels(const lod_tree* t, const void** p) {
   if (!t || t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
-  *p = t->vox.p;
+  *p = stored_voxels(t);
   return LOD_OK;
 }
 
@@ -920,7 +933,7 @@ int lod_tree_copy_voxels(const lod_tree* t, void* host, void* stream) {
   if (!t || t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
   CK(cudaSetDevice(t->device));
   if (t->n_voxels)
-    CK(cudaMemcpyAsync(host, t->vox.p, t->n_voxels * 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaMemcpyAsync(host, stored_voxels(t), t->n_voxels * 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   return LOD_OK;
 }
@@ -934,7 +947,8 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->leaf_pts, &t->status, &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf,
                          &t->vox, &t->scratch, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
-                         &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg};
+                         &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
+                   &t->vpos, &t->vout, &t->obits, &t->opre};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;

@@ -36,6 +36,7 @@ enum : uint32_t {
   ERR_EMPTY_CHILD = 1u << 8,   // sampling.py:34-35
   ERR_COUNT = 1u << 9,         // partition.py:268-269
   ERR_NO_ROOT = 1u << 10,      // partition.py:189-191
+  ERR_ZERO_WEIGHT = 1u << 11,  // sampling.py:129-130
 };
 
 // Device-resident scalars of one build; read back with a single small D2H copy.

@@ -2,18 +2,23 @@
 // (reference partition.py:244-271; the stable argsort at partition.py:262 is what makes
 // within-leaf order = input order, hazard H3).
 //
-// GPU form: stable LSD radix sort of the point records keyed by leaf id, one-sweep style
-// (one pass per digit, <= 11-bit digits, at most 2 passes for <= 2^22 leaves):
-//   - the leaf id is computed on the fly in the first pass (main finest-cell target +
-//     extension descent), so no key array is ever materialised for single-pass builds;
-//   - per tile (8192 points) warps rank their items with __match_any_sync and a
-//     per-warp smem histogram, which keeps ranks stable (warp-major, round-major, lane);
-//   - tiles find their global per-digit offsets with decoupled look-back over
-//     epoch-tagged 64-bit status words (no per-pass clearing);
-//   - global digit offsets come from the leaf counts already known from the pyramid,
-//     so there is no histogram pass over the points.
-// HBM traffic per point, single pass: 16 B read + 16 B written (+ the L2-resident
-// target-table read).  Records are re-read for the scatter from L2.
+// GPU form: stable LSD counting sort of the point records keyed by leaf id, reduce-then-
+// scan per pass (<= 11-bit digits, at most 2 passes for <= 2^22 leaves).  The input is cut
+// into CHUNKS of 4096-point sub-tiles (one CTA each):
+//   K_hist    per chunk: leaf id of every point (computed on the fly from the record in
+//             the first pass: main finest-cell target + extension descent), digit
+//             histogram in shared memory -> counts[chunk][B]
+//   K_scan    per digit: exclusive prefix over chunks + the digit's global base (known
+//             from the leaf counts of the pyramid) -> first slot of every (chunk, digit)
+//   K_scatter per chunk, its sub-tiles in order: stable in-sub-tile ranks (warp-major,
+//             item-major, lane = input order), records re-read (L1/L2) and stored.
+// Scatter CTAs take the chunks in REVERSE order: the last chunks K_hist read may still be
+// in L2.  Concurrent CTAs hold adjacent chunks, so every leaf has ONE contiguous write
+// front and L2 merges the 16-B records into full sectors before they reach HBM (per-
+// segment fronts spread over the leaf left half-written lines and doubled DRAM traffic).
+// No inter-CTA waiting (no look-back chain); the counts matrix is chunks x B x 4 B
+// (= 2 n bytes at 11-bit digits).  HBM traffic per point, single pass: 16 B read (hist)
+// + <= 16 B read (scatter) + 16 B written.
 #include "kernels.h"
 
 namespace lod {
@@ -21,186 +26,229 @@ namespace lod {
 namespace {
 
 constexpr int kW = kRadixThreads / 32;
-constexpr uint64_t kFlagA = 1ull, kFlagP = 2ull;
+constexpr int K = kRadixItems;
 
-__device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint64_t flag, uint64_t val) {
-  return ((uint64_t)(epoch & 0xFFFF) << 48) | (flag << 46) | (val & ((1ull << 46) - 1));
-}
+struct Proj {
+  double lo0, lo1, lo2, size, inv;
+};
 
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int FMT, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kRadixThreads, 2)
-    k_radix(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
-            int shift, int bits, const uint64_t* digit_base, uint64_t* status, uint32_t epoch,
-            uint32_t* ticket) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int B = 1 << bits;
-  uint16_t* wh = reinterpret_cast<uint16_t*>(smem);                       // [kW][B] warp histograms
-  uint64_t* tbase = reinterpret_cast<uint64_t*>(smem + (size_t)kW * B * 2);  // [B] tile digit bases
-  __shared__ uint32_t s_tile;
-
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-  for (int i = threadIdx.x; i < kW * B / 2; i += kRadixThreads) reinterpret_cast<uint32_t*>(wh)[i] = 0;
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * kRadixItems;
-  const uint32_t lt_mask = (1u << lane) - 1;
-
-  const double lo0 = v.st->lo[0], lo1 = v.st->lo[1], lo2 = v.st->lo[2];
-  const double size = v.st->size, inv = v.st->inv_size;
-  bool bad = false, unresolved = false;
-  uint32_t leaf[kRadixItems];
-  uint16_t rk[kRadixItems];
-
-  // --- 1a. leaf ids.  Straight-line batches (clamped indices, no per-item branches) so
-  //     the 16 record loads, then the 16 target-table loads, are all in flight together.
+// Leaf ids (FIRST: from the records; else from the previous pass) of one warp's K x 32
+// items starting at `base`.
+template <int FMT, bool FIRST>
+__device__ __forceinline__ void load_items(const SplitView& v, const Proj& pj, const void* in_rec,
+                                           const uint32_t* in_leaf, uint64_t base, int lane, uint32_t (&leaf)[K],
+                                           bool& bad, bool& unresolved) {
+  const uint64_t last = v.n - 1;
   if (FIRST) {
-    uint32_t key[kRadixItems];
+    uint32_t key[K];
+    constexpr int kBatch = 4;  // records in flight per thread (keeps the fp64 projection spill-free)
 #pragma unroll
-    for (int k0 = 0; k0 < kRadixItems; k0 += 8) {
-      typename Rec<FMT>::Raw r[8];
+    for (int k0 = 0; k0 < K; k0 += kBatch) {
+      typename Rec<FMT>::Raw r[kBatch];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kBatch; ++u) {
         const uint64_t i = base + (uint64_t)(k0 + u) * 32 + lane;
-        r[u] = Rec<FMT>::load(in_rec, i < v.n ? i : v.n - 1);
+        r[u] = Rec<FMT>::load(in_rec, i < last ? i : last);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kBatch; ++u) {
         Cell16 c;
-        c.x = quant16(Rec<FMT>::x(r[u]), lo0, size, inv, bad);
-        c.y = quant16(Rec<FMT>::y(r[u]), lo1, size, inv, bad);
-        c.z = quant16(Rec<FMT>::z(r[u]), lo2, size, inv, bad);
+        c.x = quant16(Rec<FMT>::x(r[u]), pj.lo0, pj.size, pj.inv, bad);
+        c.y = quant16(Rec<FMT>::y(r[u]), pj.lo1, pj.size, pj.inv, bad);
+        c.z = quant16(Rec<FMT>::z(r[u]), pj.lo2, pj.size, pj.inv, bad);
         key[k0 + u] = (uint32_t)level_key(c, v.D);
       }
     }
 #pragma unroll
-    for (int k = 0; k < kRadixItems; ++k) leaf[k] = (uint32_t)__ldg(v.t8 + key[k]);
+    for (int k = 0; k < K; ++k) leaf[k] = (uint32_t)__ldg(v.t8 + key[k]);
 #pragma unroll
-    for (int k = 0; k < kRadixItems; ++k) {
+    for (int k = 0; k < K; ++k) {
       int32_t t = (int32_t)leaf[k];
+      const uint64_t i = base + (uint64_t)k * 32 + lane;
       if (t <= -2) {  // inside an extension grid (rare): recompute the cell, descend
-        const uint64_t i = base + (uint64_t)k * 32 + lane;
-        const auto r = Rec<FMT>::load(in_rec, i < v.n ? i : v.n - 1);
+        const auto r = Rec<FMT>::load(in_rec, i < last ? i : last);
         Cell16 c;
-        c.x = quant16(Rec<FMT>::x(r), lo0, size, inv, bad);
-        c.y = quant16(Rec<FMT>::y(r), lo1, size, inv, bad);
-        c.z = quant16(Rec<FMT>::z(r), lo2, size, inv, bad);
+        c.x = quant16(Rec<FMT>::x(r), pj.lo0, pj.size, pj.inv, bad);
+        c.y = quant16(Rec<FMT>::y(r), pj.lo1, pj.size, pj.inv, bad);
+        c.z = quant16(Rec<FMT>::z(r), pj.lo2, pj.size, pj.inv, bad);
         t = leaf_of_point(v, c);
       }
       if (t < 0) {
-        unresolved |= base + (uint64_t)k * 32 + lane < v.n;
+        unresolved |= i < v.n;
         t = 0;
       }
       leaf[k] = (uint32_t)t;
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < kRadixItems; ++k) {
+    for (int k = 0; k < K; ++k) {
       const uint64_t i = base + (uint64_t)k * 32 + lane;
-      leaf[k] = __ldg(in_leaf + (i < v.n ? i : v.n - 1));
+      leaf[k] = __ldg(in_leaf + (i < last ? i : last));
     }
   }
-  // --- 1b. stable in-warp ranks (warp-major, round-major, lane order) ---
+}
+
+__device__ __forceinline__ Proj proj_of(const SplitView& v) {
+  return Proj{v.st->lo[0], v.st->lo[1], v.st->lo[2], v.st->size, v.st->inv_size};
+}
+
+// ---------------------------------------------------------------------------
+// K_hist: per-chunk digit counts
+// ---------------------------------------------------------------------------
+template <int FMT, bool FIRST>
+__global__ void __launch_bounds__(kRadixThreads, 2)
+    k_dist_hist(SplitView v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_out, int shift, int bits,
+                uint32_t seg_tiles, uint32_t tiles, uint32_t* counts) {
+  extern __shared__ __align__(16) uint32_t hist[];
+  const int B = 1 << bits;
+  for (int d = threadIdx.x; d < B; d += kRadixThreads) hist[d] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Proj pj = proj_of(v);
+  bool bad = false, unresolved = false;
+  const uint32_t t0 = blockIdx.x * seg_tiles, t1 = min(t0 + seg_tiles, tiles);
+  for (uint32_t tile = t0; tile < t1; ++tile) {
+    const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
+    uint32_t leaf[K];
+    load_items<FMT, FIRST>(v, pj, in_rec, in_leaf, base, lane, leaf, bad, unresolved);
 #pragma unroll
-  for (int k = 0; k < kRadixItems; ++k) {
-    const bool valid = base + (uint64_t)k * 32 + lane < v.n;
-    const uint32_t d = (leaf[k] >> shift) & (B - 1);
-    const unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
-    uint32_t rank = 0;
-    if (valid) {
-      const unsigned peers = __match_any_sync(act, d);
-      const int leader = 31 - __clz(peers & (0u - peers));  // lowest peer lane
-      uint32_t old = 0;
-      if (lane == leader) {
-        old = wh[warp * B + d];
-        wh[warp * B + d] = (uint16_t)(old + __popc(peers));
+    for (int k = 0; k < K; ++k) {
+      const bool valid = base + (uint64_t)k * 32 + lane < v.n;
+      if (FIRST && valid) leaf_out[base + (uint64_t)k * 32 + lane] = leaf[k];  // the scatter reuses it
+      const uint32_t d = (leaf[k] >> shift) & (B - 1);
+      // warp-uniform digit (coherent scans): one add; otherwise plain shared atomics
+      // (MATCH.ANY would saturate the MIO pipe: it was the top stall here)
+      const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+      const unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
+      if (__all_sync(0xFFFFFFFFu, !valid || d == d0)) {
+        if (lane == 0 && act) atomicAdd(hist + d0, (uint32_t)__popc(act));
+      } else if (valid) {
+        atomicAdd(hist + d, 1u);
       }
-      old = __shfl_sync(act, old, leader);
-      rank = old + __popc(peers & lt_mask);
     }
-    rk[k] = (uint16_t)rank;
-    __syncwarp();
   }
   __syncthreads();
-
-  // --- 2. cross-warp prefix per digit, decoupled look-back across tiles ---
-  for (int d = threadIdx.x; d < B; d += kRadixThreads) {
-    uint32_t run = 0;
-#pragma unroll 4
-    for (int w = 0; w < kW; ++w) {
-      uint32_t c = wh[w * B + d];
-      wh[w * B + d] = (uint16_t)run;
-      run += c;
-    }
-    uint64_t* mine = status + (uint64_t)tile * B + d;
-    uint64_t excl = 0;
-    if (tile == 0) {
-      st_relaxed(mine, pack_status(epoch, kFlagP, run));
-    } else {
-      st_relaxed(mine, pack_status(epoch, kFlagA, run));
-      // look back over up to 8 predecessors per trip (independent loads), summing
-      // aggregates until an inclusive prefix is found
-      int64_t t = (int64_t)tile - 1;
-      bool done = false;
-      while (!done) {
-        uint64_t w[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) w[q] = t - q >= 0 ? ld_relaxed(status + (uint64_t)(t - q) * B + d) : 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (done || t - q < 0) break;
-          const uint64_t flag = (w[q] >> 46) & 3;
-          if ((uint32_t)(w[q] >> 48) != (epoch & 0xFFFF) || flag == 0) {  // not published yet
-            t -= q;
-            __nanosleep(20);
-            goto retry;
-          }
-          excl += w[q] & ((1ull << 46) - 1);
-          if (flag == kFlagP) done = true;
-        }
-        t -= 8;
-      retry:;
-      }
-      st_relaxed(mine, pack_status(epoch, kFlagP, excl + run));
-    }
-    tbase[d] = digit_base[d] + excl;
-  }
-  __syncthreads();
-
-  // --- 3. scatter: records re-read from L2 (the tile was just read), batched so the loads
-  //        overlap; destinations of equal-digit runs are adjacent, so L2 merges the sectors ---
-#pragma unroll
-  for (int k0 = 0; k0 < kRadixItems; k0 += 4) {
-    typename Rec<FMT>::Raw r[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint64_t i = base + (uint64_t)(k0 + u) * 32 + lane;
-      r[u] = Rec<FMT>::load(in_rec, i < v.n ? i : v.n - 1);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = k0 + u;
-      const uint64_t i = base + (uint64_t)k * 32 + lane;
-      if (i < v.n) {
-        const uint32_t d = (leaf[k] >> shift) & (B - 1);
-        const uint64_t dest = tbase[d] + wh[warp * B + d] + rk[k];
-        Rec<FMT>::store(out_rec, dest, r[u]);
-        if (!LAST) out_leaf[dest] = leaf[k];
-      }
-    }
-  }
+  for (int d = threadIdx.x; d < B; d += kRadixThreads) counts[(uint64_t)blockIdx.x * B + d] = hist[d];
   if (FIRST) {
     if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) raise_err(v.st, ERR_OUTSIDE);
     if (__any_sync(0xFFFFFFFFu, unresolved) && lane == 0) raise_err(v.st, ERR_UNRESOLVED);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K_scan: counts[g][d] -> digit_base[d] + sum_{g' < g} counts[g'][d]  (first slots)
+// 32 digits per block (lanes), the chunks split over the 32 warps.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_dist_scan(uint32_t* counts, uint32_t segs, int B,
+                                                    const uint64_t* digit_base) {
+  __shared__ uint32_t part[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = blockIdx.x * 32 + lane;
+  const uint32_t per = (segs + 31) / 32;
+  const uint32_t g0 = min(segs, warp * per), g1 = min(segs, g0 + per);
+  uint32_t s = 0;
+  if (d < B)
+    for (uint32_t g = g0; g < g1; ++g) s += counts[(uint64_t)g * B + d];
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t run = d < B ? (uint32_t)digit_base[d] : 0;
+    for (int w = 0; w < 32; ++w) {
+      const uint32_t c = part[w][lane];
+      part[w][lane] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (d < B) {
+    uint32_t run = part[warp][lane];
+    for (uint32_t g = g0; g < g1; ++g) {
+      const uint32_t c = counts[(uint64_t)g * B + d];
+      counts[(uint64_t)g * B + d] = run;
+      run += c;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K_scatter: stable scatter; chunks in reverse launch order, sub-tiles in order
+// ---------------------------------------------------------------------------
+template <int FMT, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kRadixThreads, 2)
+    k_dist_scatter(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
+                   int shift, int bits, uint32_t seg_tiles, uint32_t tiles, const uint32_t* firsts) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int B = 1 << bits;
+  uint32_t* run = reinterpret_cast<uint32_t*>(smem);               // [B] first slot of the sub-tile
+  uint32_t* tot = run + B;                                          // [B] sub-tile digit totals
+  uint16_t* wh = reinterpret_cast<uint16_t*>(smem + (size_t)B * 8);  // [kW][B] warp counts -> prefixes
+  const uint32_t chunk = gridDim.x - 1 - blockIdx.x;
+  for (int d = threadIdx.x; d < B; d += kRadixThreads) run[d] = firsts[(uint64_t)chunk * B + d];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt_mask = (1u << lane) - 1;
+  const Proj pj = proj_of(v);
+  bool bad = false, unresolved = false;
+  const uint32_t t0 = chunk * seg_tiles, t1 = min(t0 + seg_tiles, tiles);
+  for (uint32_t tile = t0; tile < t1; ++tile) {
+    for (int i = threadIdx.x; i < kW * B / 2; i += kRadixThreads) reinterpret_cast<uint32_t*>(wh)[i] = 0;
+    __syncthreads();
+    const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
+    uint32_t leaf[K];
+    uint16_t rk[K];
+    load_items<FMT, FIRST>(v, pj, in_rec, in_leaf, base, lane, leaf, bad, unresolved);
+    // stable in-warp ranks (item-major, lane order)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const bool valid = base + (uint64_t)k * 32 + lane < v.n;
+      const uint32_t d = (leaf[k] >> shift) & (B - 1);
+      // lanes with the same digit: multi-split by ballots over the digit bits (a handful
+      // of VOTEs instead of one MATCH.ANY, which bottlenecked on the MIO pipe)
+      unsigned peers = __ballot_sync(0xFFFFFFFFu, valid);
+      const unsigned act = peers;
+      for (int b = 0; b < bits; ++b) {
+        const bool on = (d >> b) & 1;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, on);
+        peers &= on ? m : ~m;
+      }
+      uint32_t rank = 0;
+      if (valid) {
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (lane == leader) {
+          old = wh[warp * B + d];
+          wh[warp * B + d] = (uint16_t)(old + __popc(peers));
+        }
+        old = __shfl_sync(act, old, leader);
+        rank = old + __popc(peers & lt_mask);
+      }
+      rk[k] = (uint16_t)rank;
+      __syncwarp();
+    }
+    __syncthreads();
+    // cross-warp exclusive prefix per digit (the sub-tile's block for digit d starts at run[d])
+    for (int d = threadIdx.x; d < B; d += kRadixThreads) {
+      uint32_t r = 0;
+#pragma unroll 4
+      for (int w = 0; w < kW; ++w) {
+        const uint32_t c = wh[w * B + d];
+        wh[w * B + d] = (uint16_t)r;
+        r += c;
+      }
+      tot[d] = r;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t i = base + (uint64_t)k * 32 + lane;
+      if (i < v.n) {
+        const uint32_t d = (leaf[k] >> shift) & (B - 1);
+        const uint64_t dest = (uint64_t)run[d] + wh[warp * B + d] + rk[k];
+        Rec<FMT>::store(out_rec, dest, Rec<FMT>::load(in_rec, i));
+        if (!LAST) out_leaf[dest] = leaf[k];
+      }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < B; d += kRadixThreads) run[d] += tot[d];
   }
 }
 
@@ -222,14 +270,28 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
   if (2 * threadIdx.x + 1 < (unsigned)B) hist[2 * threadIdx.x + 1] = ex + a;
 }
 
+// One digit pass.  FIRST: the leaf ids are computed from the records by K_hist, which
+// stores them (leaf_tmp) so K_scatter never repeats the fp64 projection.
 template <int FMT, bool FIRST, bool LAST>
-void run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
-              int shift, int bits, const uint64_t* digit_base, RadixPlan& p, uint32_t* ticket, cudaStream_t s) {
-  size_t smem = (size_t)kW * (1u << bits) * 2 + (size_t)(1u << bits) * 8;
-  auto kern = k_radix<FMT, FIRST, LAST>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<p.tiles, kRadixThreads, smem, s>>>(v, in_rec, in_leaf, out_rec, out_leaf, shift, bits, digit_base,
-                                            p.status, p.epoch, ticket);
+int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_tmp, void* out_rec,
+             uint32_t* out_leaf, int shift, int bits, const uint64_t* digit_base, const RadixPlan& p, cudaStream_t s) {
+  const int B = 1 << bits;
+  auto hist = k_dist_hist<FMT, FIRST>;
+  auto scat = k_dist_scatter<FMT, false, LAST>;
+  const size_t hsm = (size_t)B * 4, ssm = (size_t)B * 8 + (size_t)kW * B * 2 + 4 * kW;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((4u << kRadixMaxBits)));
+    cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((8u << kRadixMaxBits) + (size_t)kW * (2u << kRadixMaxBits) + 4 * kW));
+    configured = true;
+  }
+  const uint32_t* leaf_in = FIRST ? leaf_tmp : in_leaf;
+  hist<<<p.segs, kRadixThreads, hsm, s>>>(v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
+  k_dist_scan<<<ceil_div_u32(B, 32), 1024, 0, s>>>(p.counts, p.segs, B, digit_base);
+  scat<<<p.segs, kRadixThreads, ssm, s>>>(v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, p.seg_tiles, p.tiles,
+                                          p.counts);
+  return 3;
 }
 
 template <int FMT>
@@ -240,29 +302,38 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
   uint64_t* base0 = p.digit_base;
   uint64_t* base1 = p.digit_base + B0;
   cudaMemsetAsync(p.digit_base, 0, (size_t)(B0 + B1) * 8, s);
-  cudaMemsetAsync(p.tile_ticket, 0, 2 * sizeof(uint32_t), s);
   uint32_t lb = ceil_div_u32(v.n_leaves, 256);
   k_digit_hist<<<lb, 256, 0, s>>>(v.leaf_count, v.n_leaves, 0, p.bits[0],
                                   reinterpret_cast<unsigned long long*>(base0));
   k_digit_scan<<<1, 1024, 0, s>>>(base0, B0);
   launches += 2;
-  if (p.passes == 1) {
-    run_pass<FMT, true, true>(v, v.pts, nullptr, leaf_out, nullptr, 0, p.bits[0], base0, p, p.tile_ticket, s);
-    p.epoch++;
-    return launches + 1;
-  }
+  if (p.passes == 1)
+    return launches + run_pass<FMT, true, true>(v, v.pts, nullptr, p.tmp_leaf, leaf_out, nullptr, 0, p.bits[0],
+                                                base0, p, s);
   k_digit_hist<<<lb, 256, 0, s>>>(v.leaf_count, v.n_leaves, p.bits[0], p.bits[1],
                                   reinterpret_cast<unsigned long long*>(base1));
   k_digit_scan<<<1, 1024, 0, s>>>(base1, B1);
-  run_pass<FMT, true, false>(v, v.pts, nullptr, p.tmp_rec, p.tmp_leaf, 0, p.bits[0], base0, p, p.tile_ticket, s);
-  p.epoch++;
-  run_pass<FMT, false, true>(v, p.tmp_rec, p.tmp_leaf, leaf_out, nullptr, p.bits[0], p.bits[1], base1, p,
-                             p.tile_ticket + 1, s);
-  p.epoch++;
-  return launches + 4;
+  launches += 2;
+  uint32_t* sorted_leaf = p.tmp_leaf + v.n;
+  launches += run_pass<FMT, true, false>(v, v.pts, nullptr, p.tmp_leaf, p.tmp_rec, sorted_leaf, 0, p.bits[0], base0,
+                                         p, s);
+  launches += run_pass<FMT, false, true>(v, p.tmp_rec, sorted_leaf, nullptr, leaf_out, nullptr, p.bits[0], p.bits[1],
+                                         base1,
+                                         p, s);
+  return launches;
 }
 
 }  // namespace
+
+// Chunking of n points: one sub-tile per chunk.  Larger chunks shrink the counts matrix
+// but spread each leaf's write front over many half-written lines (measured: 4 sub-tiles
+// per chunk -> +35% DRAM writes, +75% reads from read-modify-write of partial sectors).
+void plan_segments(RadixPlan& p, uint64_t n, int sms) {
+  (void)sms;
+  p.tiles = (uint32_t)((n + kRadixTile - 1) / kRadixTile);
+  p.seg_tiles = 1;
+  p.segs = std::max<uint32_t>(1, (p.tiles + p.seg_tiles - 1) / p.seg_tiles);
+}
 
 int launch_distribute(int fmt, const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_t s) {
   if (p.passes == 0) {  // one leaf: the whole cloud in input order

@@ -110,12 +110,11 @@ int launch_export_nodes(const SplitView& v, lod_node* out, cudaStream_t s);
 struct RadixPlan {
   int passes;             // 0 = single leaf (plain copy)
   int bits[2];            // digit widths
-  uint32_t tiles;
-  uint64_t* status;       // look-back words, tiles * 2^bits[p] per pass (epoch-tagged)
-  uint64_t status_cap;
-  uint32_t epoch;
+  uint32_t tiles;         // kRadixTile-point sub-tiles
+  uint32_t segs;          // chunks (one CTA each)
+  uint32_t seg_tiles;     // sub-tiles per chunk
+  uint32_t* counts;       // [segs][2^bits] digit counts -> first slots (reused per pass)
   uint64_t* digit_base;   // per pass: 2^bits global exclusive prefix
-  uint32_t* tile_ticket;  // per pass
   void* tmp_rec;          // pass-0 output records (2 passes)
   uint32_t* tmp_leaf;     // pass-0 output leaf ids
 };
@@ -123,6 +122,7 @@ constexpr int kRadixThreads = 512;
 constexpr int kRadixItems = 8;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;
 constexpr int kRadixMaxBits = 11;
+void plan_segments(RadixPlan& plan, uint64_t n, int sms);
 int launch_distribute(int fmt, const SplitView& v, RadixPlan& plan, void* leaf_out, cudaStream_t s);
 
 // --- voxelize (voxelize.cu) ---
@@ -135,6 +135,7 @@ struct VoxNode {           // per inner node of the level being sampled (by list
   uint32_t cbase[8];       // ordinal of the child's first sample (octant order)
   uint32_t ccount[8];
   int32_t cslot[8];        // -2 absent, -1 leaf child, >= 0 slot of an inner child
+  uint64_t obase;          // first-come: first word of the node's ordinal bitmap
 };
 
 struct VoxLevel {
@@ -166,14 +167,21 @@ struct VoxLevel {
   uint64_t* level_start;   // arena cursor at the start of this level
   uint2* vox;              // arena: {key, rgb}
   uint64_t vox_cap;
-  uint64_t* acc;           // per voxel of this level: 2 u64 (average) or u32 (random)
+  uint64_t* acc;           // per voxel of this level: 2 u64 (average), 4 u64 (weighted) or
+                           // u32 (random, first-come)
   uint64_t acc_cap;        // voxels
+  uint32_t* vpos;          // first-come: per voxel (arena index), stored position in its node
+  uint2* vout;             // first-come: voxels in stored order (winning ordinal)
+  uint32_t* obits;         // first-come: per-level ordinal bitmaps (node runs at obase)
+  uint32_t* opre;          // first-come: exclusive popcount prefix of obits
+  uint64_t ocap;           // words of obits / opre
   uint32_t chunk;          // samples per K1/K3 chunk
   uint32_t vchunk;         // voxels per K4 chunk
   int mode;
   uint64_t seed;
 };
-int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s);
+int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s);
+uint32_t voxelize_acc_bytes(int mode);
 int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s);
 uint32_t voxelize_chunk(uint32_t nodes);
 uint32_t voxelize_vchunk(uint32_t nodes);

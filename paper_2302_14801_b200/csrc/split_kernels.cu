@@ -28,14 +28,20 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const void* pts, uint64_t n
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   bool bad = false;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    auto r = Rec<FMT>::load(pts, i);
-    double p[3] = {Rec<FMT>::x(r), Rec<FMT>::y(r), Rec<FMT>::z(r)};
+  constexpr int U = 4;  // independent 16-B loads in flight per thread
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    typename Rec<FMT>::Raw r[U];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      bad |= !isfinite(p[a]);
-      lo[a] = fmin(lo[a], p[a]);
-      hi[a] = fmax(hi[a], p[a]);
+    for (int u = 0; u < U; ++u) r[u] = Rec<FMT>::load(pts, min(i0 + u * stride, n - 1));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double p[3] = {Rec<FMT>::x(r[u]), Rec<FMT>::y(r[u]), Rec<FMT>::z(r[u])};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {  // clamped duplicates of the last point are harmless
+        bad |= !isfinite(p[a]);
+        lo[a] = fmin(lo[a], p[a]);
+        hi[a] = fmax(hi[a], p[a]);
+      }
     }
   }
 #pragma unroll

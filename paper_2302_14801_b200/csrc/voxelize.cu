@@ -22,6 +22,17 @@
 //                the rare boundary spill into a neighbouring octant) come from K3.
 //   Average: (2*sum + n) // (2*n) per channel over the children's ROUNDED colours (H5).
 //   Random : max (rand12 | ordinal20); the winning ordinal names the sample directly.
+//   First-come (sampling.py:61-66): min ordinal per cell (max of ~ordinal for leaf points;
+//            child voxels gathered with ordinal = octant base + the child's STORED position).
+//            The node's voxels are then listed by winning ordinal: K5 marks the winners in
+//            an ordinal bitmap (S bits per node), one level-wide popcount scan gives every
+//            winner its stored position p (vpos, used by the parent's gather) and the voxel
+//            is written to vout[vbase + p].  The arena itself stays in key order.
+//   Weighted (sampling.py:100-133): every sample (leaf points AND child voxels) adds
+//            w = clamp(1 - |g - centre|, 0, 1) to the occupied cells of its 2x2x2
+//            neighbourhood, as exact 2^-24 fixed-point u64 sums (order-independent, so
+//            repeated builds are bit-identical); colour = floor(sum(w c) / sum(w) + 0.5),
+//            within +-1 of the reference's sequential fp64 sums.
 //
 // Bitmaps/prefixes of a level are kept until the next (coarser) level has gathered from
 // them: two buffers alternate by depth parity.
@@ -34,7 +45,6 @@ namespace {
 constexpr uint32_t kWords = 1u << 16;        // 2^21 cells / 32
 constexpr uint32_t kBlkWords = 4096;         // words per K2 block
 constexpr uint32_t kBlksPerNode = kWords / kBlkWords;
-constexpr uint32_t kChunk = 8192;            // samples per K1/K3 chunk
 constexpr uint32_t kVoxChunk = 2048;         // voxels per K4 chunk
 constexpr int kT = 256;
 
@@ -259,8 +269,9 @@ __global__ void __launch_bounds__(kT) k_block_sums(VoxLevel L) {
 __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
   if (L.st->err & ERR_ARENA) return;
   __shared__ uint64_t sm[1024 / 32 + 1];
-  __shared__ uint64_t carry;
+  __shared__ uint64_t carry, ocarry;
   if (threadIdx.x == 0) {
+    ocarry = 0;
     carry = L.st->vox_cursor;
     L.level_start[0] = carry;
   }
@@ -279,8 +290,13 @@ __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
     }
     uint64_t tot;
     uint64_t ex = block_excl_scan<uint64_t, 1024>(m, &tot, sm);
+    uint64_t ow = 0;  // first-come: words of the node's ordinal bitmap
+    if (s < L.list_n && L.mode == LOD_MODE_FIRST_COME && !L.info[s].skip) ow = (L.info[s].S + 31) / 32;
+    uint64_t otot;
+    uint64_t oex = block_excl_scan<uint64_t, 1024>(ow, &otot, sm);
     if (s < L.list_n) {
       VoxNode& nd = L.info[s];
+      nd.obase = ocarry + oex;
       uint64_t vb = carry + ex;
       nd.vbase = vb;
       nd.m = m;
@@ -291,11 +307,12 @@ __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
       for (uint32_t q = 0; q < nv; ++q) L.vchunks[at + q] = make_uint2(s, q * L.vchunk);
     }
     __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
+    if (threadIdx.x == 0) carry += tot, ocarry += otot;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    if (carry > L.vox_cap || carry - L.level_start[0] > L.acc_cap) raise_err(L.st, ERR_ARENA, 0, carry);
+    if (carry > L.vox_cap || carry - L.level_start[0] > L.acc_cap || ocarry > L.ocap)
+      raise_err(L.st, ERR_ARENA, 0, carry);
     L.st->vox_cursor = carry;
   }
 }
@@ -338,10 +355,14 @@ __global__ void __launch_bounds__(kT) k_prefix_emit(VoxLevel L) {
       uint32_t bit = __ffs(bw) - 1;
       bw &= bw - 1;
       L.vox[nd.vbase + rr] = make_uint2(key0 + bit, 0);
-      if (L.mode == LOD_MODE_AVERAGE)
+      if (L.mode == LOD_MODE_AVERAGE) {
         reinterpret_cast<ulonglong2*>(L.acc)[acc0 + rr] = make_ulonglong2(0, 0);
-      else
+      } else if (L.mode == LOD_MODE_WEIGHTED) {
+        reinterpret_cast<ulonglong2*>(L.acc)[2 * (acc0 + rr)] = make_ulonglong2(0, 0);
+        reinterpret_cast<ulonglong2*>(L.acc)[2 * (acc0 + rr) + 1] = make_ulonglong2(0, 0);
+      } else {
         reinterpret_cast<uint32_t*>(L.acc)[acc0 + rr] = 0;
+      }
       ++rr;
     }
   }
@@ -400,9 +421,108 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
           unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 2 * a;
           atomicAdd(p, (unsigned long long)(rgb & 0xFF) | ((unsigned long long)((rgb >> 8) & 0xFF) << 32));
           atomicAdd(p + 1, (unsigned long long)((rgb >> 16) & 0xFF) | (1ull << 32));
-        } else {
+        } else if (L.mode == LOD_MODE_RANDOM) {
           atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, rand_enc(nd.hash, ob + j));
+        } else {  // first-come: the smallest ordinal is the largest complement
+          atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, ~(ob + j));
         }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3w: weighted -- every sample of the level (leaf points and child voxels) adds its
+// 2x2x2 neighbourhood weights to the occupied cells (sampling.py:108-127).  The octant
+// region's bits + prefixes are staged in shared memory; neighbours across the region
+// border go to the global rank structure.
+// ---------------------------------------------------------------------------
+constexpr double kWScale = 16777216.0;  // 2^24 fixed point: sum(w) < 2^56 for < 2^32 samples
+
+__device__ __forceinline__ double wdist_axis(double g, uint32_t c) {
+  const double d = __dsub_rn(g, __dadd_rn((double)c, 0.5));
+  return __dmul_rn(d, d);
+}
+
+__global__ void __launch_bounds__(kRT, 2) k_scatter_w(VoxLevel L) {
+  if (L.st->err & ERR_ARENA) return;
+  extern __shared__ __align__(16) uint32_t rsm[];
+  uint32_t* rbits = rsm;
+  uint32_t* rpre = rsm + kRegionWords;
+  const uint32_t nch = L.counters[0];
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint4 ch = L.chunks[c];
+    const VoxNode& nd = L.info[ch.x];
+    const uint32_t* bits = bits_of(L, L.parity, ch.x);
+    const uint32_t* pre = pre_of(L, L.parity, ch.x);
+    const uint64_t acc0 = nd.vbase - L.level_start[0];
+    const int o = (int)ch.y;
+    for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) {
+      const uint32_t gw = region_to_global(i, o);
+      rbits[i] = __ldcg(bits + gw);
+      rpre[i] = __ldcg(pre + gw);
+    }
+    __syncthreads();
+    const bool leaf = nd.cslot[o] == -1;
+    const uint64_t first = nd.cfirst[o];
+    const double4 b = nd.box;
+    const double upper = 0x1.fffffffffffffp+6;  // nextafter(128, 0), sampling.py:30
+    for (uint32_t j = ch.z + threadIdx.x; j < ch.w; j += kRT) {
+      double g[3];
+      uint32_t rgb;
+      if (leaf) {  // (p - min) / size * 128, clipped (sampling.py:37-38)
+        double p[3];
+        if (L.fmt == LOD_POINTS_F32) {
+          const auto r = Rec<LOD_POINTS_F32>::load(L.leaf_pts, first + j);
+          p[0] = Rec<LOD_POINTS_F32>::x(r), p[1] = Rec<LOD_POINTS_F32>::y(r), p[2] = Rec<LOD_POINTS_F32>::z(r);
+          rgb = Rec<LOD_POINTS_F32>::rgb(r);
+        } else {
+          const auto r = Rec<LOD_POINTS_F64>::load(L.leaf_pts, first + j);
+          p[0] = Rec<LOD_POINTS_F64>::x(r), p[1] = Rec<LOD_POINTS_F64>::y(r), p[2] = Rec<LOD_POINTS_F64>::z(r);
+          rgb = Rec<LOD_POINTS_F64>::rgb(r);
+        }
+        const double lo[3] = {b.x, b.y, b.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double q = __dmul_rn(__ddiv_rn(__dsub_rn(p[a], lo[a]), b.w), 128.0);
+          g[a] = fmin(fmax(q, 0.0), upper);
+        }
+      } else {     // child voxel c in octant o: off + (c + 0.5) / 2, exact (sampling.py:41-44)
+        const uint2 v = __ldg(L.vox + first + j);
+        const uint32_t cc[3] = {v.x >> 14, (v.x >> 7) & 127, v.x & 127};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) g[a] = 64.0 * ((o >> a) & 1) + ((double)cc[a] + 0.5) * 0.5;
+        rgb = v.y;
+      }
+      uint32_t base[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) base[a] = (uint32_t)fmin(fmax(floor(__dsub_rn(g[a], 0.5)), 0.0), 126.0);
+      const double col[3] = {(double)(rgb & 0xFF), (double)((rgb >> 8) & 0xFF), (double)((rgb >> 16) & 0xFF)};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t cx = base[0] + (q >> 2), cy = base[1] + ((q >> 1) & 1), cz = base[2] + (q & 1);
+        const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(wdist_axis(g[0], cx), wdist_axis(g[1], cy)),
+                                              wdist_axis(g[2], cz)));
+        const double w = __dsub_rn(1.0, d);
+        if (!(w > 0.0)) continue;
+        const uint32_t key = (cx << 14) | (cy << 7) | cz;
+        const uint32_t bit = 1u << (key & 31);
+        uint32_t lw, word, rank;
+        if (region_word(key, o, lw)) {
+          word = rbits[lw];
+          if (!(word & bit)) continue;  // only occupied cells emit (sampling.py:125-128)
+          rank = rpre[lw] + __popc(word & (bit - 1));
+        } else {
+          word = __ldcg(bits + (key >> 5));
+          if (!(word & bit)) continue;
+          rank = __ldcg(pre + (key >> 5)) + __popc(word & (bit - 1));
+        }
+        unsigned long long* acc = reinterpret_cast<unsigned long long*>(L.acc) + 4 * (acc0 + rank);
+        atomicAdd(acc, (unsigned long long)__double2ll_rn(__dmul_rn(w, kWScale)));
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (col[k] != 0.0) atomicAdd(acc + 1 + k, (unsigned long long)__double2ll_rn(__dmul_rn(__dmul_rn(w, col[k]), kWScale)));
       }
     }
     __syncthreads();
@@ -412,6 +532,12 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
 // ---------------------------------------------------------------------------
 // K4: finalize every voxel of the level
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t leaf_winner_rgb(const VoxLevel& L, const VoxNode& nd, uint32_t ord) {
+  int oo = 7;  // the leaf octant holding ordinal `ord`
+  while (oo > 0 && (nd.cslot[oo] != -1 || nd.cbase[oo] > ord)) --oo;
+  return __ldg(&L.stash[nd.cfirst[oo] + (ord - nd.cbase[oo])].y);
+}
+
 __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
   if (L.st->err & ERR_ARENA) return;
   const uint32_t nch = L.counters[2];
@@ -422,6 +548,19 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
     const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
     const uint64_t acc0 = nd.vbase - L.level_start[0];
     for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
+      if (L.mode == LOD_MODE_WEIGHTED) {
+        const unsigned long long* a = reinterpret_cast<const unsigned long long*>(L.acc) + 4 * (acc0 + r);
+        const double W = (double)__ldcg(a);
+        uint32_t rgb = 0;
+        if (!(W > 0.0)) raise_err(L.st, ERR_ZERO_WEIGHT, nd.node);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double m = floor(__dadd_rn(__ddiv_rn((double)__ldcg(a + 1 + k), W), 0.5));
+          rgb |= (uint32_t)fmin(fmax(m, 0.0), 255.0) << (8 * k);
+        }
+        L.vox[nd.vbase + r].y = rgb;
+        continue;
+      }
       const uint32_t key = L.vox[nd.vbase + r].x;
       const uint32_t X = key >> 14, Y = (key >> 7) & 127, Z = key & 127;
       const int o = (int)((X >> 6) | ((Y >> 6) << 1) | ((Z >> 6) << 2));
@@ -449,9 +588,12 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
             const uint32_t rgb = __ldcg(&L.vox[ci.vbase + cr].y);
             if (L.mode == LOD_MODE_AVERAGE) {
               sr += rgb & 0xFF, sg += (rgb >> 8) & 0xFF, sb += (rgb >> 16) & 0xFF, ++n;
-            } else {
+            } else if (L.mode == LOD_MODE_RANDOM) {
               uint32_t e = rand_enc(nd.hash, nd.cbase[o] + cr);
               if (!have || e > best) best = e, best_rgb = rgb, have = true;
+            } else {  // first-come: ordinal = octant base + the child's stored position
+              const uint32_t ord = nd.cbase[o] + __ldcg(L.vpos + ci.vbase + cr);
+              if (!have || ord < best) best = ord, best_rgb = rgb, have = true;
             }
             ++cr;
           }
@@ -461,17 +603,62 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
         const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(L.acc) + acc0 + r);
         sr += a.x & 0xFFFFFFFFull, sg += a.x >> 32, sb += a.y & 0xFFFFFFFFull, n += a.y >> 32;
         L.vox[nd.vbase + r].y = mean_round(sr, n) | (mean_round(sg, n) << 8) | (mean_round(sb, n) << 16);
-      } else {
+      } else if (L.mode == LOD_MODE_RANDOM) {
         const uint32_t e = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
-        if (!have || e > best) {
-          // the winner is a leaf point: its ordinal names (child, index) directly
-          const uint32_t ord = e & 0xFFFFFu;
-          int oo = 7;
-          while (oo > 0 && (nd.cslot[oo] != -1 || nd.cbase[oo] > ord)) --oo;
-          best_rgb = __ldg(&L.stash[nd.cfirst[oo] + (ord - nd.cbase[oo])].y);
-        }
+        // the winner is a leaf point: its ordinal names (child, index) directly
+        if (!have || e > best) best_rgb = leaf_winner_rgb(L, nd, e & 0xFFFFFu);
         L.vox[nd.vbase + r].y = best_rgb;
+      } else {
+        uint32_t* a = reinterpret_cast<uint32_t*>(L.acc) + acc0 + r;
+        const uint32_t e = __ldcg(a);
+        if (e != 0 && (!have || ~e < best)) best = ~e, best_rgb = leaf_winner_rgb(L, nd, ~e);
+        L.vox[nd.vbase + r].y = best_rgb;
+        *a = best;  // winning ordinal, ranked by K5
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5 (first-come): stored order = ascending winning ordinal (sampling.py:64-66)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_fc_mark(VoxLevel L) {
+  if (L.st->err & ERR_ARENA) return;
+  const uint32_t nch = L.counters[2];
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint2 ch = L.vchunks[c];
+    const VoxNode& nd = L.info[ch.x];
+    const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
+    const uint64_t acc0 = nd.vbase - L.level_start[0];
+    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
+      const uint32_t ord = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
+      atomicOr(L.obits + nd.obase + (ord >> 5), 1u << (ord & 31));
+    }
+  }
+}
+
+struct OrdScanF {  // exclusive popcount prefix over the level's ordinal bitmaps
+  const uint32_t* bits;
+  uint32_t* pre;
+  __device__ uint64_t value(uint64_t i) const { return __popc(__ldcg(bits + i)); }
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { pre[i] = (uint32_t)excl; }
+};
+
+__global__ void __launch_bounds__(kT) k_fc_pos(VoxLevel L) {
+  if (L.st->err & ERR_ARENA) return;
+  const uint32_t nch = L.counters[2];
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint2 ch = L.vchunks[c];
+    const VoxNode& nd = L.info[ch.x];
+    const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
+    const uint64_t acc0 = nd.vbase - L.level_start[0];
+    const uint32_t p0 = __ldcg(L.opre + nd.obase);
+    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
+      const uint32_t ord = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
+      const uint64_t w = nd.obase + (ord >> 5);
+      const uint32_t p = __ldcg(L.opre + w) - p0 + __popc(__ldcg(L.obits + w) & ((1u << (ord & 31)) - 1));
+      L.vpos[nd.vbase + r] = p;
+      L.vout[nd.vbase + p] = L.vox[nd.vbase + r];
     }
   }
 }
@@ -557,6 +744,23 @@ __global__ void __launch_bounds__(kT) k_import_prefix(VoxLevel L, uint32_t slot_
   }
 }
 
+// first-come imports arrive in stored order (in vout): put the arena in key order and
+// record each voxel's stored position for the parent's gather
+__global__ void __launch_bounds__(kT) k_import_fc(VoxLevel L, uint32_t slot_base) {
+  const uint32_t i = blockIdx.x / kBlksPerNode, part = blockIdx.x % kBlksPerNode;
+  const VoxNode& nd = L.info[slot_base + i];
+  const uint32_t* bits = bits_of(L, L.parity, slot_base + i);
+  const uint32_t* pre = pre_of(L, L.parity, slot_base + i);
+  const uint32_t per = (nd.m + kBlksPerNode - 1) / kBlksPerNode;
+  const uint32_t p0 = part * per, p1 = min(nd.m, p0 + per);
+  for (uint32_t p = p0 + threadIdx.x; p < p1; p += kT) {
+    const uint2 v = __ldg(L.vout + nd.vbase + p);
+    const uint32_t r = rank_of(bits, pre, v.x);
+    L.vox[nd.vbase + r] = v;
+    L.vpos[nd.vbase + r] = p;
+  }
+}
+
 int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s) {
   if (!L.list_n) return 0;
   k_import_setup<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L, slot_base);
@@ -564,13 +768,16 @@ int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s
   k_import_block_sums<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
   k_import_block_prefix<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L);
   k_import_prefix<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
-  return 5;
+  if (L.mode != LOD_MODE_FIRST_COME) return 5;
+  k_import_fc<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
+  return 6;
 }
 
 // Runs one depth level; returns launches.  counters[0..2] must be zero on entry and the
 // level's bitmaps cleared.
-int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s) {
+int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s) {
   const int grid = sms * 8;
+  int launches = 7;
   k_setup<<<ceil_div_u32(8ull * L.list_n, kT), kT, 0, s>>>(L);
   if (L.fmt == LOD_POINTS_F32)
     k_occupy<LOD_POINTS_F32><<<sms * 2, kRT, 0, s>>>(L);
@@ -582,11 +789,27 @@ int launch_voxelize_level(const VoxLevel& L, int sms, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);
+    cudaFuncSetAttribute(k_scatter_w, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);
     configured = true;
   }
-  k_scatter<<<sms * 2, kRT, 2 * kRegionWords * 4, s>>>(L);
+  if (L.mode == LOD_MODE_WEIGHTED)
+    k_scatter_w<<<sms * 2, kRT, 2 * kRegionWords * 4, s>>>(L);
+  else
+    k_scatter<<<sms * 2, kRT, 2 * kRegionWords * 4, s>>>(L);
   k_finalize<<<grid, kT, 0, s>>>(L);
-  return 7;
+  if (L.mode == LOD_MODE_FIRST_COME) {
+    cudaMemsetAsync(L.obits, 0, L.ocap * 4, s);
+    k_fc_mark<<<grid, kT, 0, s>>>(L);
+    const int r = device_scan(L.ocap, OrdScanF{L.obits, L.opre}, scr, nullptr, nullptr, s);
+    if (r < 0) return r;
+    k_fc_pos<<<grid, kT, 0, s>>>(L);
+    launches += 2 + r;
+  }
+  return launches;
+}
+
+uint32_t voxelize_acc_bytes(int mode) {
+  return mode == LOD_MODE_AVERAGE ? 16 : mode == LOD_MODE_WEIGHTED ? 32 : 4;
 }
 
 // chunk sizes: small levels get small chunks so every SM has work

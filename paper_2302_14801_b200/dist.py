@@ -496,7 +496,8 @@ def build_distributed(comm: TorchComm, d_records, n_local, fmt, mode, seed=0, T=
     send = rb.pack(lay)
     recv = comm.all_to_all_bytes(send, lay["send_splits"] * rb.rec_bytes, lay["recv_splits"] * rb.rec_bytes)
     rb.unpack_adopt(recv, lay)
-    mode_code = _abi.LOD_MODE_RANDOM if mode == "random" else _abi.LOD_MODE_AVERAGE
+    from .sampling import _mode_code
+    mode_code = _mode_code(mode)
     inner = ~is_leaf
     own = inner & (plan.node_owner == comm.rank) & (depth >= plan.cut)
     rb.voxelize(mode_code, seed, own.astype(np.uint8))

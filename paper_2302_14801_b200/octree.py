@@ -5,7 +5,8 @@ Python `OctreeNode` objects are materialised lazily on first access to `.root`,
 with exactly the reference's fields: octant `path`, `bounds` (fp64 sequential
 child_bounds fold, computed on the device), `children` (8 slots, None = absent),
 leaf `point_positions` (float64, input order) / `point_colors`, inner
-`voxel_coords` / `voxel_colors` (uint8, ascending x-major key) and `oversized`.
+`voxel_coords` / `voxel_colors` (uint8, in the reference's stored order: ascending
+x-major key, or winning ordinal for first-come) and `oversized`.
 `build_lod` on a materialised tree updates the inner nodes in place, like the
 reference (sampling.py:172-176).
 """

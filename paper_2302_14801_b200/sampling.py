@@ -4,28 +4,30 @@ plus the north-star fused entry point.
     build_lod(tree, strategy=None, seed=None) -> tree          # reference form
     build_lod(points, colors, T=50_000, grid=128, mode="color_filter", seed=0)  # fused
 
-Strategies "random" and "average" (alias "color_filter") run on the GPU.
-"first-come" / "weighted" are outside this build's scope and raise
-NotImplementedError (no CPU fallback); unknown names raise ValueError like the
-reference (sampling.py:169-170).
+All four reference strategies run on the GPU: "first-come" (the reference default,
+model.py:115), "random", "average" (alias "color_filter") and "weighted" (colours
+within +-1 per channel of the reference's fp64 sums, SPEC.md).  There is no CPU
+fallback; unknown names raise ValueError like the reference (sampling.py:169-170).
 """
 from __future__ import annotations
 
 import numpy as np
 
-from ._abi import LOD_MODE_AVERAGE, LOD_MODE_RANDOM
+from ._abi import LOD_MODE_AVERAGE, LOD_MODE_FIRST_COME, LOD_MODE_RANDOM, LOD_MODE_WEIGHTED
 from .device import DeviceTree, make_config
-from .model import GRID_SIZE, MODE_ALIASES, STRATEGIES, BuildConfig, Octree
+from .model import GRID_SIZE, MODE_ALIASES, BuildConfig, Octree
 from .octree import GpuOctree
 
 MAX_RANDOM_SAMPLES = 1 << 20  # reference sampling.py:18
 
 
+_CODES = {"random": LOD_MODE_RANDOM, "average": LOD_MODE_AVERAGE, "first-come": LOD_MODE_FIRST_COME,
+          "weighted": LOD_MODE_WEIGHTED}
+
+
 def _mode_code(strategy: str) -> int:
     if strategy in MODE_ALIASES:
-        return LOD_MODE_RANDOM if MODE_ALIASES[strategy] == "random" else LOD_MODE_AVERAGE
-    if strategy in STRATEGIES:
-        raise NotImplementedError(f"sampling strategy {strategy!r} is not implemented on the GPU path")
+        return _CODES[MODE_ALIASES[strategy]]
     raise ValueError(f"unknown sampling strategy: {strategy}")
 
 

@@ -35,7 +35,11 @@ def _acceptance03_cases():
 CASES = []
 
 
-def _add(name, spec, cfg, modes, color=None, quick=True):
+def _add(name, spec, cfg, modes, color=None, quick=True, weighted=False):
+    """Every case also records the reference's "first-come" output (the reference default,
+    model.py:115); `weighted` cases also store the reference's "weighted" colours in full
+    (compared within +-1 per channel, SPEC.md "Weighted accumulation order")."""
+    modes = list(modes) + ["first-come"] + (["weighted"] if weighted else [])
     CASES.append(dict(name=name, spec=spec, cfg=cfg, modes=modes, color=color, quick=quick))
 
 
@@ -43,7 +47,7 @@ def _add(name, spec, cfg, modes, color=None, quick=True):
 for kind, n, seed, T in [("uniform-cube", 20_000, 1, 1000), ("uniform-cube", 5_000, 2, 300),
                          ("stadium", 30_000, 3, 1500), ("two-scans", 20_000, 4, 2000),
                          ("checker-plane", 10_000, 5, 800)]:
-    _add(f"part_{kind}_{n}_{seed}_T{T}", ("ref", kind, n, seed), dict(T=T), ["average", "random:11"])
+    _add(f"part_{kind}_{n}_{seed}_T{T}", ("ref", kind, n, seed), dict(T=T), ["average", "random:11"], weighted=True)
 
 # test_acceptance.py:97-120 randomized partition cases
 for kind, n, seed, T in _acceptance03_cases():
@@ -52,19 +56,19 @@ for kind, n, seed, T in _acceptance03_cases():
 # test_acceptance.py:123-151 sampling datasets (T=1500)
 for kind, n, seed in [("uniform-cube", 60_000, 6), ("uniform-cube", 40_000, 7),
                       ("two-scans", 40_000, 8), ("stadium", 50_000, 9)]:
-    _add(f"acc04_{kind}_{n}_{seed}", ("ref", kind, n, seed), dict(T=1500), ["average", "random:3"])
+    _add(f"acc04_{kind}_{n}_{seed}", ("ref", kind, n, seed), dict(T=1500), ["average", "random:3"], weighted=True)
 
 # test_sampling.py small_tree fixtures
 _add("small_tree_30k", ("ref", "uniform-cube", 30_000, 1), dict(T=2000), ["average", "random:9", "random:5"])
-_add("small_tree_25k", ("ref", "uniform-cube", 25_000, 1), dict(T=1500), ["average", "random:11"])
+_add("small_tree_25k", ("ref", "uniform-cube", 25_000, 1), dict(T=1500), ["average", "random:11"], weighted=True)
 _add("const_color_20k", ("ref", "uniform-cube", 20_000, 3), dict(T=1000), ["average", "random:2"],
-     color=(12, 200, 99))
+     color=(12, 200, 99), weighted=True)
 
 # structural edge cases (test_partition.py:107-136, test_sampling.py:224-232)
-_add("single_point", ("literal", "single"), dict(), ["average", "random:0"])
-_add("identical_2000_T500", ("tile", (0.25, 0.5, 0.75), 2000), dict(T=500), ["average", "random:0"])
-_add("maxface_600", ("maxface", 600), dict(T=1000), ["average", "random:0"])
-_add("sparse_cluster_T50", ("literal", "sparse200"), dict(T=50), ["average", "random:1"])
+_add("single_point", ("literal", "single"), dict(), ["average", "random:0"], weighted=True)
+_add("identical_2000_T500", ("tile", (0.25, 0.5, 0.75), 2000), dict(T=500), ["average", "random:0"], weighted=True)
+_add("maxface_600", ("maxface", 600), dict(T=1000), ["average", "random:0"], weighted=True)
+_add("sparse_cluster_T50", ("literal", "sparse200"), dict(T=50), ["average", "random:1"], weighted=True)
 _add("uniform_40k_single_leaf", ("ref", "uniform-cube", 40_000, 42), dict(), ["average"])
 _add("uniform_100k_T50k", ("ref", "uniform-cube", 100_000, 42), dict(), ["average", "random:0"])
 _add("uniform_300k_T20k", ("ref", "uniform-cube", 300_000, 42), dict(T=20_000), ["average", "random:0"])
@@ -82,6 +86,10 @@ _add("stadium_2M_random_limit", ("ref", "stadium", 2_000_000, 1), dict(), ["rand
      quick=False)
 _add("acc_plane_100k", ("ref", "checker-plane", 100_000, 1), dict(), ["average", "random:0"])
 _add("acc_twoscans_200k", ("ref", "two-scans", 200_000, 1), dict(), ["average", "random:11"])
+# > 2^11 leaves: the two-pass distribute and thousands of leaf parents
+_add("many_leaves_400k_T100", ("ref", "uniform-cube", 400_000, 3), dict(T=100), ["average", "random:5"],
+     quick=False)
+_add("many_leaves_stadium_300k_T60", ("ref", "stadium", 300_000, 8), dict(T=60), ["average"], quick=False)
 
 # BASELINE configs; float32 coordinates
 _add("sphere1M", ("syn", "sphere", 1_000_000, 1), dict(), ["random:0", "average"], quick=False)

@@ -11,10 +11,12 @@ For every case in `cases.py` it
      mode, unmodified;
   3. writes tests/golden/<name>.json.gz: per-node digests in the format of
      `oracle/lod_oracle.split_digest` / `voxel_digest`, or the exception text
-     when the reference raises (e.g. the 2^20 random-sampling limit).
+     when the reference raises (e.g. the 2^20 random-sampling limit).  "weighted" stores
+     sha1(coords) and the zlib+base64 colours (compared within +-1 per channel).
 """
 from __future__ import annotations
 
+import base64
 import gzip
 import hashlib
 import json
@@ -28,6 +30,8 @@ REPO = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, REPO)
 sys.path.insert(0, HERE)
 sys.path.insert(0, "/root/reference/pkg/src")
+
+import zlib  # noqa: E402
 
 import numpy as np  # noqa: E402
 
@@ -79,8 +83,15 @@ def run_case(case):
         strat, _, seed = mode.partition(":")
         try:
             build_lod(tree, strat, int(seed or 0))
-            modes[mode] = {_ps(nd.path): [nd.voxel_count, _sha(nd.voxel_coords, nd.voxel_colors)]
-                           for nd in tree.inner_nodes()}
+            if strat == "weighted":   # +-1 tolerance: keep the colours themselves
+                modes[mode] = {_ps(nd.path): [nd.voxel_count, _sha(nd.voxel_coords),
+                                              base64.b64encode(zlib.compress(
+                                                  np.ascontiguousarray(nd.voxel_colors, np.uint8).tobytes(), 9)
+                                              ).decode()]
+                               for nd in tree.inner_nodes()}
+            else:
+                modes[mode] = {_ps(nd.path): [nd.voxel_count, _sha(nd.voxel_coords, nd.voxel_colors)]
+                               for nd in tree.inner_nodes()}
         except ConsistencyError as e:
             modes[mode] = {"error": str(e)}
     out["modes"] = modes

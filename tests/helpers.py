@@ -1,5 +1,7 @@
 """Digest helpers shared by the GPU parity tests (same format as oracle.split_digest)."""
+import base64
 import hashlib
+import zlib
 
 import numpy as np
 
@@ -35,3 +37,32 @@ def diff_dicts(got, exp, limit=8):
     keys = sorted(set(got) | set(exp))
     bad = [(k, got.get(k), exp.get(k)) for k in keys if got.get(k) != exp.get(k)]
     return bad[:limit], len(bad)
+
+
+def weighted_colors(entry):
+    """Decode a golden "weighted" entry [m, sha1(coords), b64(zlib(colors))] -> (m, sha, (m,3) u8)."""
+    m, csha, blob = entry
+    cols = np.frombuffer(zlib.decompress(base64.b64decode(blob)), np.uint8).reshape(-1, 3)
+    return m, csha, cols
+
+
+def compare_weighted(got, exp):
+    """got: path-string -> (coords, colors).  Coordinates must match exactly, colours within
+    +-1 per channel (SPEC.md "Weighted accumulation order").  Returns (errors, n_off_by_one,
+    n_channels)."""
+    errors, off, total = [], 0, 0
+    if set(got) != set(exp):
+        errors.append(("node set", sorted(set(got) ^ set(exp))[:4]))
+        return errors, off, total
+    for k, entry in exp.items():
+        m, csha, ecol = weighted_colors(entry)
+        c, col = got[k]
+        if len(c) != m or sha(c) != csha:
+            errors.append((k, "coords"))
+            continue
+        d = np.abs(np.asarray(col, np.int16) - ecol.astype(np.int16))
+        total += d.size
+        off += int((d == 1).sum())
+        if d.max(initial=0) > 1:
+            errors.append((k, "colour off by", int(d.max())))
+    return errors, off, total

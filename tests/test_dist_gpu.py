@@ -7,7 +7,7 @@ import pytest
 
 from conftest import golden_available, load_golden
 from cases import by_name, make_input
-from helpers import sha
+from helpers import compare_weighted, sha
 
 pytestmark = pytest.mark.gpu
 
@@ -43,7 +43,7 @@ def combined_digests(builders, plan, fmt):
             r = owner if int(nd["depth"]) >= plan.cut else 0
             nodes, coords, colors = per[r][0], per[r][3], per[r][4]
             f, c = int(nodes[k]["first"]), int(nodes[k]["count"])
-            vox[ps] = [c, sha(coords[f:f + c], colors[f:f + c])]
+            vox[ps] = (coords[f:f + c], colors[f:f + c])
     return split, vox
 
 
@@ -66,6 +66,10 @@ def test_distributed_matches_reference(name, world):
         builders, plan = simulate_distributed(rec, fmt, world, strat, int(seed or 0), T=T)
         split, vox = combined_digests(builders, plan, fmt)
         assert split == g["split"], (name, mode)
-        assert vox == exp, (name, mode)
+        if strat == "weighted":   # +-1 per channel, coordinates exact
+            errors, off, total = compare_weighted(vox, exp)
+            assert not errors and off <= max(8, total // 1000), (name, mode, errors[:4], off)
+        else:
+            assert {k: [len(c), sha(c, k2)] for k, (c, k2) in vox.items()} == exp, (name, mode)
         if world > 1 and len(plan.roots) >= world:
             assert len(set(plan.root_owner.tolist())) > 1  # the work really was spread

@@ -3,16 +3,18 @@
 Every case in tests/golden/cases.py was produced by the unmodified reference
 (`make_golden.py`).  Bit-exact requirements:
   node hierarchy (paths, leaf/inner), per-leaf point counts, oversized flags,
-  fp64 node bounds, leaf contents in input order, voxel coordinates and colours for
-  random and average ("color_filter") sampling, and the reference's
-  ConsistencyError on the 2^20 random-sampling limit.
+  fp64 node bounds, leaf contents in input order, voxel coordinates and colours (in the
+  reference's stored order) for first-come, random and average ("color_filter")
+  sampling, and the reference's ConsistencyError on the 2^20 random-sampling limit.
+Weighted sampling: voxel coordinates bit-exact, colours within +-1 per channel of the
+reference's sequential fp64 sums (SPEC.md "Weighted accumulation order").
 """
 import numpy as np
 import pytest
 
 from conftest import golden_available, load_golden
 from cases import CASES, make_input
-from helpers import diff_dicts, tree_split_digest, tree_voxel_digest
+from helpers import compare_weighted, diff_dicts, tree_split_digest, tree_voxel_digest
 
 pytestmark = pytest.mark.gpu
 
@@ -38,6 +40,13 @@ def run_case(case):
             assert str(ei.value) == exp["error"]
             continue
         build_lod(tree, strat, int(seed or 0))
+        if strat == "weighted":
+            got_w = {"".join(str(o) for o in nd.path) or "-": (nd.voxel_coords, nd.voxel_colors)
+                     for nd in tree.inner_nodes()}
+            errors, off, total = compare_weighted(got_w, exp)
+            assert not errors, f"{case['name']} weighted: {errors[:4]}"
+            assert off <= max(8, total // 1000), f"{case['name']} weighted: {off}/{total} channels off by one"
+            continue
         got_v = tree_voxel_digest(tree)
         bad, nbad = diff_dicts(got_v, exp)
         assert nbad == 0, f"{case['name']} {mode}: {nbad} voxel mismatches, e.g. {bad}"

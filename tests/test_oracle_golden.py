@@ -11,6 +11,7 @@ import pytest
 from conftest import golden_available, load_golden
 from cases import CASES, make_input
 
+from helpers import compare_weighted
 from oracle import lod_oracle as O
 
 QUICK = [c for c in CASES if c["quick"]]
@@ -31,6 +32,10 @@ def check_case(case):
             with pytest.raises(O.ConsistencyError, match="20-bit index limit") as ei:
                 O.voxelize(sp, pos64, col, strat, int(seed or 0))
             assert str(ei.value) == exp["error"]
+        elif strat == "weighted":
+            vox = O.voxelize(sp, pos64, col, strat, 0)
+            errors, off, _ = compare_weighted({O.path_str(p): v for p, v in vox.items()}, exp)
+            assert not errors and off == 0, (case["name"], errors[:4], off)   # the oracle is exact
         else:
             vox = O.voxelize(sp, pos64, col, strat, int(seed or 0))
             assert O.voxel_digest(vox) == exp, (case["name"], mode)
