@@ -89,7 +89,7 @@ struct lod_tree {
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
   DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
   DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
-  DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf;
+  DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf, pkey;
   DevBuf vox, scratch, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vleaf_chunks, vvchunks;
   DevBuf vpos, vout, obits, opre;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
@@ -203,6 +203,7 @@ SplitView make_view(lod_tree* t, const void* pts) {
   v.main_cells = level_off(v.D + 1);
   v.node_idx = t->node_idx.as<int32_t>();
   v.t8 = t->t8.as<int32_t>();
+  v.pkey = t->pkey.as<uint32_t>();
   v.te = t->te.as<int32_t>();
   v.meta = t->meta.as<ExtMeta>();
   v.n_ext = t->n_ext;
@@ -292,6 +293,7 @@ int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* 
   CK(cudaMemsetAsync(t->pyr.p, 0, main_cells * 4, s));
   CK(ensure(t->t8, fine_cells * 4));
   CK(cudaMemsetAsync(t->t8.p, 0xFF, fine_cells * 4, s));
+  CK(ensure(t->pkey, std::max<uint64_t>(n, 1) * 4));
   uint64_t scan_blocks = (std::max<uint64_t>(main_cells, n) + kScanTile - 1) / kScanTile + 2;
   CK(ensure(t->scan, scan_blocks * 8));
   return LOD_OK;
@@ -846,7 +848,7 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
                    &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->opre};
+                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -948,7 +950,7 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->vox, &t->scratch, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
                          &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->opre};
+                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;

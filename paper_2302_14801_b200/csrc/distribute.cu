@@ -5,9 +5,10 @@
 // GPU form: stable LSD counting sort of the point records keyed by leaf id, reduce-then-
 // scan per pass (<= 11-bit digits, at most 2 passes for <= 2^22 leaves).  The input is cut
 // into CHUNKS of 4096-point sub-tiles (one CTA each):
-//   K_hist    per chunk: leaf id of every point (computed on the fly from the record in
-//             the first pass: main finest-cell target + extension descent), digit
-//             histogram in shared memory -> counts[chunk][B]
+//   K_hist    per chunk: leaf id of every point (first pass: through the target table from
+//             the finest main-grid key K_count stored per point, pkey -- no record read,
+//             extension descent only inside extension grids; the ids are stored for the
+//             scatter), digit histogram in shared memory -> counts[chunk][B]
 //   K_scan    per digit: exclusive prefix over chunks + the digit's global base (known
 //             from the leaf counts of the pyramid) -> first slot of every (chunk, digit)
 //   K_scatter per chunk, its sub-tiles in order: stable in-sub-tile ranks (warp-major,
@@ -16,9 +17,12 @@
 // in L2.  Concurrent CTAs hold adjacent chunks, so every leaf has ONE contiguous write
 // front and L2 merges the 16-B records into full sectors before they reach HBM (per-
 // segment fronts spread over the leaf left half-written lines and doubled DRAM traffic).
+// The same happens when more records are in flight at once: 8192-point tiles, or 3 CTAs
+// per SM instead of 2, raised DRAM writes from 1.0x to 2.0-2.4x of the 16 B/pt (each half-
+// written sector evicted early costs a read-modify-write), so the tile stays at 4096 x 2.
 // No inter-CTA waiting (no look-back chain); the counts matrix is chunks x B x 4 B
-// (= 2 n bytes at 11-bit digits).  HBM traffic per point, single pass: 16 B read (hist)
-// + <= 16 B read (scatter) + 16 B written.
+// (= 2 n bytes at 11-bit digits).  HBM traffic per point, single pass: 4 B read + 4 B
+// written (hist), 4 B + 16 B read and 16 B written (scatter).
 #include "kernels.h"
 
 namespace lod {
@@ -32,47 +36,47 @@ struct Proj {
   double lo0, lo1, lo2, size, inv;
 };
 
-// Leaf ids (FIRST: from the records; else from the previous pass) of one warp's K x 32
-// items starting at `base`.
+__device__ __forceinline__ Proj proj_of(const SplitView& v) {
+  return Proj{v.st->lo[0], v.st->lo[1], v.st->lo[2], v.st->size, v.st->inv_size};
+}
+
+// Leaf of point i from its stored finest main-grid key (K_count wrote pkey), descending
+// the extension grids from the record when the target says so; -1 if unresolved.
+template <int FMT>
+__device__ __forceinline__ int32_t leaf_from_record(const SplitView& v, const Proj& pj, uint64_t i, int32_t t,
+                                                 bool& bad) {
+  const auto r = Rec<FMT>::load(v.pts, i);
+  Cell16 c;
+  c.x = quant16(Rec<FMT>::x(r), pj.lo0, pj.size, pj.inv, bad);
+  c.y = quant16(Rec<FMT>::y(r), pj.lo1, pj.size, pj.inv, bad);
+  c.z = quant16(Rec<FMT>::z(r), pj.lo2, pj.size, pj.inv, bad);
+  uint32_t e, rr;
+  if (ext_descend(v, c, e, rr, t)) t = v.te[v.meta[e].tgt_off + rr];
+  return t;
+}
+
+// Leaf ids of one warp's K x 32 items starting at `base`.  FIRST: through the target table
+// from the point's finest main-grid key (no record read, no fp64 projection except for
+// points inside extension grids); else the ids of the previous pass.
 template <int FMT, bool FIRST>
-__device__ __forceinline__ void load_items(const SplitView& v, const Proj& pj, const void* in_rec,
-                                           const uint32_t* in_leaf, uint64_t base, int lane, uint32_t (&leaf)[K],
-                                           bool& bad, bool& unresolved) {
+__device__ __forceinline__ void load_items(const SplitView& v, const Proj& pj, const uint32_t* in_leaf,
+                                           uint64_t base, int lane, uint32_t (&leaf)[K], bool& bad,
+                                           bool& unresolved) {
   const uint64_t last = v.n - 1;
   if (FIRST) {
     uint32_t key[K];
-    constexpr int kBatch = 4;  // records in flight per thread (keeps the fp64 projection spill-free)
 #pragma unroll
-    for (int k0 = 0; k0 < K; k0 += kBatch) {
-      typename Rec<FMT>::Raw r[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const uint64_t i = base + (uint64_t)(k0 + u) * 32 + lane;
-        r[u] = Rec<FMT>::load(in_rec, i < last ? i : last);
-      }
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        Cell16 c;
-        c.x = quant16(Rec<FMT>::x(r[u]), pj.lo0, pj.size, pj.inv, bad);
-        c.y = quant16(Rec<FMT>::y(r[u]), pj.lo1, pj.size, pj.inv, bad);
-        c.z = quant16(Rec<FMT>::z(r[u]), pj.lo2, pj.size, pj.inv, bad);
-        key[k0 + u] = (uint32_t)level_key(c, v.D);
-      }
+    for (int k = 0; k < K; ++k) {
+      const uint64_t i = base + (uint64_t)k * 32 + lane;
+      key[k] = __ldg(v.pkey + (i < last ? i : last));
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) leaf[k] = (uint32_t)__ldg(v.t8 + key[k]);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      int32_t t = (int32_t)leaf[k];
       const uint64_t i = base + (uint64_t)k * 32 + lane;
-      if (t <= -2) {  // inside an extension grid (rare): recompute the cell, descend
-        const auto r = Rec<FMT>::load(in_rec, i < last ? i : last);
-        Cell16 c;
-        c.x = quant16(Rec<FMT>::x(r), pj.lo0, pj.size, pj.inv, bad);
-        c.y = quant16(Rec<FMT>::y(r), pj.lo1, pj.size, pj.inv, bad);
-        c.z = quant16(Rec<FMT>::z(r), pj.lo2, pj.size, pj.inv, bad);
-        t = leaf_of_point(v, c);
-      }
+      int32_t t = (int32_t)leaf[k];
+      if (t <= -2) t = leaf_from_record<FMT>(v, pj, i < last ? i : last, t, bad);
       if (t < 0) {
         unresolved |= i < v.n;
         t = 0;
@@ -88,9 +92,6 @@ __device__ __forceinline__ void load_items(const SplitView& v, const Proj& pj, c
   }
 }
 
-__device__ __forceinline__ Proj proj_of(const SplitView& v) {
-  return Proj{v.st->lo[0], v.st->lo[1], v.st->lo[2], v.st->size, v.st->inv_size};
-}
 
 // ---------------------------------------------------------------------------
 // K_hist: per-chunk digit counts
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
     uint32_t leaf[K];
-    load_items<FMT, FIRST>(v, pj, in_rec, in_leaf, base, lane, leaf, bad, unresolved);
+    load_items<FMT, FIRST>(v, pj, in_leaf, base, lane, leaf, bad, unresolved);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const bool valid = base + (uint64_t)k * 32 + lane < v.n;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
     uint32_t leaf[K];
     uint16_t rk[K];
-    load_items<FMT, FIRST>(v, pj, in_rec, in_leaf, base, lane, leaf, bad, unresolved);
+    load_items<FMT, FIRST>(v, pj, in_leaf, base, lane, leaf, bad, unresolved);
     // stable in-warp ranks (item-major, lane order)
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -270,8 +271,8 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
   if (2 * threadIdx.x + 1 < (unsigned)B) hist[2 * threadIdx.x + 1] = ex + a;
 }
 
-// One digit pass.  FIRST: the leaf ids are computed from the records by K_hist, which
-// stores them (leaf_tmp) so K_scatter never repeats the fp64 projection.
+// One digit pass.  FIRST: the leaf ids are resolved once by K_hist, which stores them
+// (leaf_tmp) for K_scatter.
 template <int FMT, bool FIRST, bool LAST>
 int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_tmp, void* out_rec,
              uint32_t* out_leaf, int shift, int bits, const uint64_t* digit_base, const RadixPlan& p, cudaStream_t s) {

@@ -22,6 +22,7 @@ struct SplitView {
   uint64_t main_cells;    // cells of the main pyramid = level_off(D + 1)
   int32_t* node_idx;      // slot -> node id (valid at non-zero slots)
   int32_t* t8;            // main finest level: leaf id, -(ext+2), or -1
+  uint32_t* pkey;         // per point: its main finest-level key (written by K_count)
   int32_t* te;            // ext finest levels: same encoding
   ExtMeta* meta;
   uint32_t n_ext;
@@ -116,7 +117,7 @@ struct RadixPlan {
   uint32_t* counts;       // [segs][2^bits] digit counts -> first slots (reused per pass)
   uint64_t* digit_base;   // per pass: 2^bits global exclusive prefix
   void* tmp_rec;          // pass-0 output records (2 passes)
-  uint32_t* tmp_leaf;     // pass-0 output leaf ids
+  uint32_t* tmp_leaf;     // leaf ids: input order (K_hist, pass 0) [+ sorted by digit 0]
 };
 constexpr int kRadixThreads = 512;
 constexpr int kRadixItems = 8;

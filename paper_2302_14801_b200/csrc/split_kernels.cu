@@ -23,6 +23,51 @@ __device__ __forceinline__ int ceil_log2_u64(uint64_t x) { return x <= 1 ? 0 : 6
 // ---------------------------------------------------------------------------
 // K1: bounds
 // ---------------------------------------------------------------------------
+// float32 records: min / max / finiteness in fp32 (exact; widened once at the end)
+__global__ void __launch_bounds__(kThreads) k_bounds_f32(const void* pts, uint64_t n, DevState* st) {
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  uint32_t expmax = 0;  // non-finite <=> exponent field all ones
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  const uint4* p = reinterpret_cast<const uint4*>(pts);
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = __ldg(p + min(i0 + u * stride, n - 1));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t w[3] = {r[u].x, r[u].y, r[u].z};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float f = __uint_as_float(w[a]);
+        expmax = max(expmax, w[a] & 0x7F800000u);
+        lo[a] = fminf(lo[a], f);
+        hi[a] = fmaxf(hi[a], f);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xFFFFFFFFu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xFFFFFFFFu, hi[a], o));
+    }
+  }
+  __shared__ float s_lo[kThreads / 32][3], s_hi[kThreads / 32][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int a = 0; a < 3; ++a) s_lo[warp][a] = lo[a], s_hi[warp][a] = hi[a];
+  if (__syncthreads_or(expmax == 0x7F800000u) && threadIdx.x == 0) raise_err(st, ERR_NONFINITE);
+  if (threadIdx.x < 3) {
+    int a = threadIdx.x;
+    float l = s_lo[0][a], h = s_hi[0][a];
+    for (int w = 1; w < kThreads / 32; ++w) l = fminf(l, s_lo[w][a]), h = fmaxf(h, s_hi[w][a]);
+    atomicMin(&st->lo_key[a], dkey((double)l));
+    atomicMax(&st->hi_key[a], dkey((double)h));
+  }
+}
+
 template <int FMT>
 __global__ void __launch_bounds__(kThreads) k_bounds(const void* pts, uint64_t n, DevState* st) {
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -91,7 +136,7 @@ int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const doub
   }
   uint32_t blocks = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, 148ull * 8);
   if (fmt == LOD_POINTS_F32)
-    k_bounds<LOD_POINTS_F32><<<blocks, kThreads, 0, s>>>(pts, n, st);
+    k_bounds_f32<<<blocks, kThreads, 0, s>>>(pts, n, st);
   else
     k_bounds<LOD_POINTS_F64><<<blocks, kThreads, 0, s>>>(pts, n, st);
   k_bounds_finalize<<<1, 32, 0, s>>>(st, 0, 0, 0, 0, 0);
@@ -122,7 +167,10 @@ __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
       uint64_t i = base + u * stride + threadIdx.x;
       bool valid = i < v.n;
       uint32_t key = 0;
-      if (valid) key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
+      if (valid) {
+        key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
+        v.pkey[i] = key;  // reused by extension counting and the distribute (no re-projection)
+      }
       // warp-uniform cell (coherent scans, dense clusters): one aggregated add;
       // otherwise one fire-and-forget RED per point (MATCH would saturate the ADU pipe)
       const uint32_t k0 = __shfl_sync(0xFFFFFFFFu, key, 0);
@@ -236,10 +284,11 @@ __global__ void __launch_bounds__(kThreads) k_ext_count(SplitView v, uint32_t ro
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < v.n; base += stride) {
     uint64_t i = base + threadIdx.x;
     uint64_t slot = ~0ull;
-    if (i < v.n) {
+    // only points inside an extension grid (target <= -2) re-project their record
+    const int32_t t = i < v.n ? __ldg(v.t8 + __ldg(v.pkey + i)) : -1;
+    if (t <= -2) {
       auto r = Rec<FMT>::load(v.pts, i);
       Cell16 c = cell16<FMT>(r, st, bad);
-      int32_t t = v.t8[level_key(c, v.D)];
       uint32_t e, rr;
       if (ext_descend(v, c, e, rr, t) && e >= round_first) {
         const ExtMeta& m = v.meta[e];

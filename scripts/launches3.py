@@ -11,7 +11,7 @@ per = collections.OrderedDict()
 for r in rows[hi + 1:]:
     per.setdefault(int(r[0]), {"k": r[ki].split("(")[0][-44:]})[r[mi]] = float(r[vi].replace(",", ""))
 items = list(per.items())
-start = max(i for i, (_, d) in enumerate(items) if "k_bounds<" in d["k"])
+start = max(i for i, (_, d) in enumerate(items) if "k_bounds" in d["k"] and "finalize" not in d["k"])
 agg = collections.OrderedDict()
 tot = [0.0, 0.0, 0.0]
 for _, d in items[start:]:
