@@ -133,6 +133,14 @@ int lod_tree_voxels(const lod_tree* tree, const void** d_ptr);
 int lod_tree_copy_leaf_points(const lod_tree* tree, void* host, void* stream);
 int lod_tree_copy_voxels(const lod_tree* tree, void* host, void* stream);
 
+/* VLPC payload (reference codec.py:28-47): for the n nodes h_order[i] (node ids, in the
+ * file's path order, codec.py:51) write each node's records at byte h_offsets[i] of the
+ * device buffer d_payload -- leaves 16-B {f32 offset from node min, rgb, pad}, inner nodes
+ * 6-B {cx, cy, cz, r, g, b} in stored order.  Header and node table are host bytes
+ * (paper_2302_14801_b200/codec.py). */
+int lod_tree_encode_payload(const lod_tree* tree, const int32_t* h_order, const uint64_t* h_offsets,
+                            uint32_t n, void* d_payload, void* stream);
+
 /* Device memory currently held by the tree, bytes. */
 uint64_t lod_tree_device_bytes(const lod_tree* tree);
 

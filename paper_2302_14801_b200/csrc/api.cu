@@ -940,6 +940,28 @@ int lod_tree_copy_voxels(const lod_tree* t, void* host, void* stream) {
   return LOD_OK;
 }
 
+int lod_tree_encode_payload(const lod_tree* tc, const int32_t* h_order, const uint64_t* h_offsets, uint32_t n,
+                            void* d_payload, void* stream) {
+  lod_tree* t = const_cast<lod_tree*>(tc);
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
+  if (t->voxel_mode < 0 && t->n_nodes > t->n_leaves)
+    return fail(LOD_EVALUE, "encode needs voxels: run lod_voxelize first");
+  if (n > t->n_nodes) return fail(LOD_EVALUE, "node order longer than the node table");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(t->device));
+  CK(ensure(t->export_buf, (size_t)n * 12 + 16));
+  int32_t* d_order = t->export_buf.as<int32_t>();
+  uint64_t* d_offs = reinterpret_cast<uint64_t*>(t->export_buf.as<uint8_t>() + (((size_t)n * 4 + 15) & ~(size_t)15));
+  CK(cudaMemcpyAsync(d_order, h_order, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_offs, h_offsets, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+  SplitView v = make_view(t, nullptr);
+  launch_encode(t->fmt, v, t->leaf_pts.p, reinterpret_cast<const uint2*>(stored_voxels(t)), d_order, d_offs, n,
+                reinterpret_cast<uint8_t*>(d_payload), s);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return LOD_OK;
+}
+
 uint64_t lod_tree_device_bytes(const lod_tree* t) {
   if (!t) return 0;
   const DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan,

@@ -198,6 +198,10 @@ int launch_local_leaf_counts(const SplitView& v, const uint32_t* local_main, con
 int launch_copy_segments(const void* src, void* dst, const uint64_t* seg_src, const uint64_t* seg_dst,
                          const uint32_t* seg_cnt, uint64_t nseg, int rec_bytes, cudaStream_t s);
 
+// --- VLPC payload (encode.cu) ---
+int launch_encode(int fmt, const SplitView& v, const void* leaf_pts, const uint2* vox, const int32_t* order,
+                  const uint64_t* offs, uint32_t n, uint8_t* out, cudaStream_t s);
+
 // --- generators (generate.cu) ---
 int launch_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, void* out, const double* table,
                     cudaStream_t s);

@@ -12,12 +12,14 @@ For every case in `cases.py` it
   3. writes tests/golden/<name>.json.gz: per-node digests in the format of
      `oracle/lod_oracle.split_digest` / `voxel_digest`, or the exception text
      when the reference raises (e.g. the 2^20 random-sampling limit).  "weighted" stores
-     sha1(coords) and the zlib+base64 colours (compared within +-1 per channel).
+     sha1(coords) and the zlib+base64 colours (compared within +-1 per channel);
+  4. records [length, sha1] of the reference's VLPC file (codec.encode) per mode.
 """
 from __future__ import annotations
 
 import base64
 import gzip
+import io
 import hashlib
 import json
 import multiprocessing as mp
@@ -50,6 +52,7 @@ def _ps(path):
 
 
 def run_case(case):
+    from lodforge.codec import encode
     from lodforge.errors import ConsistencyError
     from lodforge.ingest import GeneratorPreset, PointCloud, generate
     from lodforge.model import BuildConfig
@@ -78,11 +81,16 @@ def run_case(case):
             split[_ps(nd.path)] = ["I", 0, False, b, ""]
     out["world"] = [float(v).hex() for v in tree.world_bounds.min] + [float(tree.world_bounds.size).hex()]
     out["split"] = split
-    modes = {}
+    modes, vlpc = {}, {}
     for mode in case["modes"]:
         strat, _, seed = mode.partition(":")
         try:
             build_lod(tree, strat, int(seed or 0))
+            if strat != "weighted":   # the file of `lodforge build --strategy S --seed K` (cli.py:98-118)
+                tree.config.strategy, tree.config.seed = strat, int(seed or 0)
+                buf = io.BytesIO()
+                encode(tree, buf)
+                vlpc[mode] = [len(buf.getvalue()), hashlib.sha1(buf.getvalue()).hexdigest()]
             if strat == "weighted":   # +-1 tolerance: keep the colours themselves
                 modes[mode] = {_ps(nd.path): [nd.voxel_count, _sha(nd.voxel_coords),
                                               base64.b64encode(zlib.compress(
@@ -95,6 +103,7 @@ def run_case(case):
         except ConsistencyError as e:
             modes[mode] = {"error": str(e)}
     out["modes"] = modes
+    out["vlpc"] = vlpc
     out["seconds"] = round(time.time() - t0, 2)
     with gzip.open(os.path.join(HERE, case["name"] + ".json.gz"), "wt") as f:
         json.dump(out, f, separators=(",", ":"))
