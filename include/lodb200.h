@@ -141,6 +141,38 @@ int lod_tree_copy_voxels(const lod_tree* tree, void* host, void* stream);
 int lod_tree_encode_payload(const lod_tree* tree, const int32_t* h_order, const uint64_t* h_offsets,
                             uint32_t n, void* d_payload, void* stream);
 
+/* Ingest (reference ingest.py:59-198): decode raw file records already in device memory.
+ * LAS point formats 0-3 / 6-8: d_raw = n records of record_length bytes; x = X*scale+offset
+ * per axis in fp64 (no FMA), colour = 16-bit channel >> 8 at rgb_offset (-1: grey 128);
+ * output n LOD_POINTS_F64 records. */
+int lod_ingest_las(const void* d_raw, uint64_t n, uint32_t record_length, int32_t rgb_offset,
+                   const double* scale3, const double* offset3, void* d_records, void* stream);
+
+/* PLY scalar property types (ingest.py:122-131). */
+enum lod_ply_type { LOD_PLY_I8 = 0, LOD_PLY_U8 = 1, LOD_PLY_I16 = 2, LOD_PLY_U16 = 3, LOD_PLY_I32 = 4,
+                    LOD_PLY_U32 = 5, LOD_PLY_F32 = 6, LOD_PLY_F64 = 7 };
+
+/* binary_little_endian PLY vertex records (stride bytes each): types6/offsets6 give x, y, z,
+ * red, green, blue; has_rgb = 0 -> grey 128.  out_format LOD_POINTS_F32 only when x, y, z
+ * are float properties (exact), else LOD_POINTS_F64. */
+int lod_ingest_ply(const void* d_raw, uint64_t n, uint32_t stride, const int32_t* types6,
+                   const uint32_t* offsets6, int has_rgb, int out_format, void* d_records, void* stream);
+
+/* Structural checks (reference checks.py:18-92) on the built tree against the config's T
+ * and max_depth: per node (node-table order) a byte of LOD_CHECK_* failure bits in h_flags
+ * (n_nodes entries). */
+enum lod_check_bit {
+  LOD_CHECK_CAPACITY = 1,      /* non-oversized leaf with > T points */
+  LOD_CHECK_OVERSIZED = 2,     /* oversized leaf away from max_depth */
+  LOD_CHECK_MAXIMALITY = 4,    /* inner node whose children are all leaves with < T points */
+  LOD_CHECK_CONTAINMENT = 8,   /* empty leaf, or a point outside its node (+-size*1e-6) */
+  LOD_CHECK_VOXEL_BOUNDS = 16, /* voxel coordinate outside the 128^3 grid */
+  LOD_CHECK_UNIQUENESS = 32,   /* duplicate voxel cell */
+  LOD_CHECK_EMPTY_INNER = 64,  /* inner node without voxels (after lod_voxelize) */
+  LOD_CHECK_NO_CHILDREN = 128  /* inner node without children */
+};
+int lod_tree_checks(const lod_tree* tree, uint32_t T, int32_t max_depth, uint8_t* h_flags, void* stream);
+
 /* Device memory currently held by the tree, bytes. */
 uint64_t lod_tree_device_bytes(const lod_tree* tree);
 

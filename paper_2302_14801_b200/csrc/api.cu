@@ -962,6 +962,47 @@ int lod_tree_encode_payload(const lod_tree* tc, const int32_t* h_order, const ui
   return LOD_OK;
 }
 
+int lod_ingest_las(const void* d_raw, uint64_t n, uint32_t record_length, int32_t rgb_offset, const double* scale3,
+                   const double* offset3, void* d_records, void* stream) {
+  if (!scale3 || !offset3) return fail(LOD_EVALUE, "null scale / offset");
+  if (record_length < 12) return fail(LOD_EVALUE, "record length %u too short", record_length);
+  if (rgb_offset >= 0 && (uint32_t)rgb_offset + 6 > record_length)
+    return fail(LOD_EVALUE, "rgb offset %d outside the %u-byte record", rgb_offset, record_length);
+  launch_ingest_las(d_raw, n, record_length, rgb_offset, scale3, offset3, d_records, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return LOD_OK;
+}
+
+int lod_ingest_ply(const void* d_raw, uint64_t n, uint32_t stride, const int32_t* types6, const uint32_t* offsets6,
+                   int has_rgb, int out_format, void* d_records, void* stream) {
+  if (!types6 || !offsets6) return fail(LOD_EVALUE, "null property layout");
+  for (int i = 0; i < (has_rgb ? 6 : 3); ++i) {
+    if (types6[i] < LOD_PLY_I8 || types6[i] > LOD_PLY_F64) return fail(LOD_EVALUE, "bad PLY type %d", types6[i]);
+    const uint32_t w = types6[i] <= LOD_PLY_U8 ? 1 : types6[i] <= LOD_PLY_U16 ? 2 : types6[i] == LOD_PLY_F64 ? 8 : 4;
+    if (offsets6[i] + w > stride) return fail(LOD_EVALUE, "PLY property outside the %u-byte record", stride);
+  }
+  if (out_format != LOD_POINTS_F32 && out_format != LOD_POINTS_F64)
+    return fail(LOD_EVALUE, "unknown point format %d", out_format);
+  launch_ingest_ply(d_raw, n, stride, types6, offsets6, has_rgb, out_format, d_records, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return LOD_OK;
+}
+
+int lod_tree_checks(const lod_tree* tc, uint32_t T, int32_t max_depth, uint8_t* h_flags, void* stream) {
+  lod_tree* t = const_cast<lod_tree*>(tc);
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(t->device));
+  CK(ensure(t->export_buf, (size_t)t->n_nodes + 16));
+  SplitView v = make_view(t, nullptr);
+  // uniqueness is checked on the key-ordered arena (first-come's stored order is a permutation)
+  launch_checks(t->fmt, v, t->leaf_pts.p, t->vox.as<uint2>(), t->voxel_mode >= 0 ? 1 : 0, T, max_depth,
+                t->export_buf.as<uint8_t>(), s);
+  CK(cudaMemcpyAsync(h_flags, t->export_buf.p, t->n_nodes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return LOD_OK;
+}
+
 uint64_t lod_tree_device_bytes(const lod_tree* t) {
   if (!t) return 0;
   const DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan,

@@ -202,6 +202,14 @@ int launch_copy_segments(const void* src, void* dst, const uint64_t* seg_src, co
 int launch_encode(int fmt, const SplitView& v, const void* leaf_pts, const uint2* vox, const int32_t* order,
                   const uint64_t* offs, uint32_t n, uint8_t* out, cudaStream_t s);
 
+// --- ingest + structural checks (ingest_checks.cu) ---
+int launch_ingest_las(const void* raw, uint64_t n, uint32_t reclen, int32_t rgb_off, const double* scale,
+                      const double* offset, void* out, cudaStream_t s);
+int launch_ingest_ply(const void* raw, uint64_t n, uint32_t stride, const int32_t* types, const uint32_t* offs,
+                      int has_rgb, int fmt, void* out, cudaStream_t s);
+int launch_checks(int fmt, const SplitView& v, const void* leaf_pts, const uint2* vox, int voxels, uint32_t T,
+                  int max_depth, uint8_t* flags, cudaStream_t s);
+
 // --- generators (generate.cu) ---
 int launch_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, void* out, const double* table,
                     cudaStream_t s);
