@@ -592,6 +592,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
   const bool fc = mode == LOD_MODE_FIRST_COME;
   uint64_t acc_cap = std::max<uint64_t>(t->n / 2, 1ull << 21);
   if (t->vacc.cap / acc_stride > acc_cap) acc_cap = t->vacc.cap / acc_stride;
+  bool exact_sums = false;
   for (int attempt = 0; attempt < 8; ++attempt) {
     CK(ensure(t->vox, cap * 8, base_cursor * 8, s));
     cap = t->vox.cap / 8;
@@ -657,6 +658,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.acc = t->vacc.as<uint64_t>();
     L.acc_cap = acc_cap;
     L.mode = mode;
+    L.exact_sums = exact_sums ? 1 : 0;
     L.seed = seed;
     L.vpos = t->vpos.as<uint32_t>();
     L.vout = t->vout.as<uint2>();
@@ -695,6 +697,10 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
       uint64_t need = t->host_state->err_value;
       cap = std::max<uint64_t>(cap * 2, need + (need >> 2));
       acc_cap = std::max<uint64_t>(acc_cap * 2, need / 2);
+      continue;
+    }
+    if (t->host_state->err == ERR_F32_SUMS && !exact_sums) {  // >= 65794 samples in one voxel
+      exact_sums = true;
       continue;
     }
     if ((r = check_errors(t, s))) return r;

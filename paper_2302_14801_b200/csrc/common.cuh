@@ -37,6 +37,7 @@ enum : uint32_t {
   ERR_COUNT = 1u << 9,         // partition.py:268-269
   ERR_NO_ROOT = 1u << 10,      // partition.py:189-191
   ERR_ZERO_WEIGHT = 1u << 11,  // sampling.py:129-130
+  ERR_F32_SUMS = 1u << 12,     // internal: an f32 colour sum reached 2^24, re-run with u64 sums
 };
 
 // Device-resident scalars of one build; read back with a single small D2H copy.

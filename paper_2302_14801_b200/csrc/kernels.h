@@ -179,6 +179,7 @@ struct VoxLevel {
   uint32_t chunk;          // samples per K1/K3 chunk
   uint32_t vchunk;         // voxels per K4 chunk
   int mode;
+  int exact_sums;          // average: u64 sums (fallback) instead of f32 vector reductions
   uint64_t seed;
 };
 int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s);

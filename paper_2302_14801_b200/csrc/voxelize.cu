@@ -417,7 +417,14 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
           rank = __ldcg(pre + (key >> 5)) + __popc(__ldcg(bits + (key >> 5)) & mask);
         const uint64_t a = acc0 + rank;
         const uint32_t rgb = r[u].y;
-        if (L.mode == LOD_MODE_AVERAGE) {
+        if (L.mode == LOD_MODE_AVERAGE && !L.exact_sums) {
+          // one vector reduction per sample: {r, g, b, 1} as f32, exact while every sum
+          // stays below 2^24 (checked in K4; otherwise the build re-runs with u64 sums)
+          float* p = reinterpret_cast<float*>(L.acc) + 4 * a;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"((float)(rgb & 0xFF)),
+                       "f"((float)((rgb >> 8) & 0xFF)), "f"((float)((rgb >> 16) & 0xFF)), "f"(1.0f)
+                       : "memory");
+        } else if (L.mode == LOD_MODE_AVERAGE) {
           unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 2 * a;
           atomicAdd(p, (unsigned long long)(rgb & 0xFF) | ((unsigned long long)((rgb >> 8) & 0xFF) << 32));
           atomicAdd(p + 1, (unsigned long long)((rgb >> 16) & 0xFF) | (1ull << 32));
@@ -600,8 +607,14 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
         }
       }
       if (L.mode == LOD_MODE_AVERAGE) {
-        const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(L.acc) + acc0 + r);
-        sr += a.x & 0xFFFFFFFFull, sg += a.x >> 32, sb += a.y & 0xFFFFFFFFull, n += a.y >> 32;
+        if (L.exact_sums) {
+          const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(L.acc) + acc0 + r);
+          sr += a.x & 0xFFFFFFFFull, sg += a.x >> 32, sb += a.y & 0xFFFFFFFFull, n += a.y >> 32;
+        } else {
+          const float4 a = __ldcg(reinterpret_cast<const float4*>(L.acc) + acc0 + r);
+          if (fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)) >= 16777216.0f) raise_err(L.st, ERR_F32_SUMS, nd.node);
+          sr += (uint64_t)a.x, sg += (uint64_t)a.y, sb += (uint64_t)a.z, n += (uint64_t)a.w;
+        }
         L.vox[nd.vbase + r].y = mean_round(sr, n) | (mean_round(sg, n) << 8) | (mean_round(sb, n) << 16);
       } else if (L.mode == LOD_MODE_RANDOM) {
         const uint32_t e = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);

@@ -1,0 +1,53 @@
+"""GPU edge cases checked directly against the CPU oracle (oracle/lod_oracle.py, itself
+pinned to the reference's goldens):
+
+* a voxel with > 65793 samples of colour 255: its colour sum passes 2^24, so the f32
+  vector reductions of the average path must hand over to exact u64 sums;
+* duplicate points forming an oversized leaf at max depth, under every strategy."""
+import numpy as np
+import pytest
+
+from oracle import lod_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _cloud(n_dup, n_rest, seed=0):
+    rng = np.random.default_rng(seed)
+    dup = np.tile([[0.3125, 0.625, 0.8125]], (n_dup, 1))
+    rest = rng.random((n_rest, 3))
+    pos = np.concatenate([dup, rest]).astype(np.float32).astype(np.float64)
+    col = np.concatenate([np.full((n_dup, 3), 255, np.uint8), rng.integers(0, 256, (n_rest, 3)).astype(np.uint8)])
+    perm = rng.permutation(len(pos))
+    return pos[perm], col[perm]
+
+
+def _compare(pos, col, T, strategy, seed=0):
+    from paper_2302_14801_b200 import BuildConfig, PointCloud, build_lod, partition
+    tree = partition(PointCloud(pos, col), BuildConfig(T=T))
+    build_lod(tree, strategy, seed)
+    sp = O.split(pos, T=T)
+    vox = O.voxelize(sp, pos, col, strategy, seed)
+    got = {nd.path: nd for nd in tree.iter_nodes()}
+    assert set(got) == set(sp.nodes)
+    for path, (c, k) in vox.items():
+        g = got[path]
+        if strategy == "weighted":
+            assert np.array_equal(g.voxel_coords, c)
+            assert np.abs(g.voxel_colors.astype(int) - k.astype(int)).max(initial=0) <= 1
+        else:
+            assert np.array_equal(g.voxel_coords, c) and np.array_equal(g.voxel_colors, k), (strategy, path)
+    return tree
+
+
+def test_average_sum_overflow_falls_back_to_exact():
+    pos, col = _cloud(70_000, 30_000)
+    tree = _compare(pos, col, 1000, "average")
+    over = [nd for nd in tree.leaves() if nd.oversized]
+    assert over and max(nd.point_count for nd in over) == 70_000
+
+
+@pytest.mark.parametrize("strategy", ["first-come", "random", "weighted"])
+def test_oversized_duplicates_all_strategies(strategy):
+    pos, col = _cloud(3_000, 20_000, seed=1)
+    _compare(pos, col, 500, strategy, seed=4)
