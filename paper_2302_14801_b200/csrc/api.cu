@@ -89,7 +89,7 @@ struct lod_tree {
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
   DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
   DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
-  DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf, pkey;
+  DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf, pkey, pc16;
   DevBuf vox, scratch, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vleaf_chunks, vvchunks;
   DevBuf vpos, vout, obits, opre;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
@@ -204,6 +204,7 @@ SplitView make_view(lod_tree* t, const void* pts) {
   v.node_idx = t->node_idx.as<int32_t>();
   v.t8 = t->t8.as<int32_t>();
   v.pkey = t->pkey.as<uint32_t>();
+  v.pc16 = t->pc16.as<uint64_t>();
   v.te = t->te.as<int32_t>();
   v.meta = t->meta.as<ExtMeta>();
   v.n_ext = t->n_ext;
@@ -350,6 +351,7 @@ int phase_round(lod_tree* t, cudaStream_t s) {
   CK(ensure(t->meta, (size_t)(first + cur) * sizeof(ExtMeta), (size_t)first * sizeof(ExtMeta), s));
   CK(cudaMemsetAsync(t->pyr.as<uint32_t>() + pyr_base, 0, new_pyr * 4, s));
   CK(cudaMemsetAsync(t->te.as<int32_t>() + tgt_base, 0xFF, new_tgt * 4, s));
+  if (t->rounds.empty()) CK(ensure(t->pc16, std::max<uint64_t>(t->n, 1) * 8));  // depth-16 cells of ext points
   SplitView v = make_view(t, t->pts);
   RUN(launch_ext_create(v, (int)t->rounds.size(), first, cur, t->list.as<uint64_t>(), t->round_parent_first,
                         pyr_base, tgt_base, base, ext, s));
@@ -475,18 +477,25 @@ int phase_distribute(lod_tree* t, cudaStream_t s) {
   if (bits > 2 * kRadixMaxBits)
     return fail(LOD_EUNSUPPORTED, "%u leaves exceed the 2-pass distribute limit", t->n_leaves);
   p.passes = (t->n_nodes == 1 || n == 0) ? 0 : (bits <= kRadixMaxBits ? 1 : 2);
-  p.bits[0] = p.passes == 2 ? bits / 2 : bits;
-  p.bits[1] = p.passes == 2 ? bits - bits / 2 : 0;
+  p.bits[0] = bits;
+  p.bits[1] = 0;
+  if (p.passes == 2) {  // prefer a 2nd digit that fits the record pad (distribute.cu OUT_TAG)
+    const int tagb = t->fmt == LOD_POINTS_F32 ? 8 : kRadixMaxBits;
+    p.bits[1] = std::min(tagb, bits - bits / 2);
+    p.bits[0] = bits - p.bits[1];
+    if (p.bits[0] > kRadixMaxBits) p.bits[0] = bits / 2, p.bits[1] = bits - bits / 2;
+  }
   if (p.passes) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->device);
     plan_segments(p, n, sms);
     const int maxb = std::max(p.bits[0], p.bits[1]);
-    CK(ensure(t->status, ((size_t)p.segs << maxb) * 4));
+    CK(ensure(t->status, (((size_t)p.segs + 1024) << maxb) * 4));
     CK(ensure(t->digit_base, (size_t)(2 << kRadixMaxBits) * 8 * 2));
     if (p.passes == 2) CK(ensure(t->tmp_rec, n * rec));
     CK(ensure(t->tmp_leaf, n * 4 * p.passes));  // leaf ids in input order (+ sorted by the 1st digit)
     p.counts = t->status.as<uint32_t>();
+    p.scan_part = p.counts + ((size_t)p.segs << maxb);
     p.digit_base = t->digit_base.as<uint64_t>();
     p.tmp_rec = t->tmp_rec.p;
     p.tmp_leaf = t->tmp_leaf.as<uint32_t>();
@@ -586,11 +595,14 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
   uint64_t imp_total = 0;
   for (uint32_t i = 0; plan && i < plan->n_imp; ++i) imp_total += plan->imp_counts[i];
   const uint64_t base_cursor = keep ? t->n_voxels : 0;
-  uint64_t cap = std::max<uint64_t>(t->n + t->n / 2, 1ull << 21) + base_cursor + imp_total;
+  // first guess at the arena (grown and re-run on ERR_ARENA): surfaces give V/N ~ 0.3-1.0,
+  // volumes up to ~1.8; very large clouds start lean to leave HBM for the rest
+  const uint64_t guess = t->n <= (1ull << 27) ? t->n + t->n / 2 : t->n - t->n / 4;
+  uint64_t cap = std::max<uint64_t>(guess, 1ull << 21) + base_cursor + imp_total;
   if (t->vox.cap / 8 > cap) cap = t->vox.cap / 8;
   const uint32_t acc_stride = voxelize_acc_bytes(mode);
   const bool fc = mode == LOD_MODE_FIRST_COME;
-  uint64_t acc_cap = std::max<uint64_t>(t->n / 2, 1ull << 21);
+  uint64_t acc_cap = std::max<uint64_t>(t->n <= (1ull << 27) ? t->n / 2 : t->n / 4, 1ull << 21);
   if (t->vacc.cap / acc_stride > acc_cap) acc_cap = t->vacc.cap / acc_stride;
   bool exact_sums = false;
   for (int attempt = 0; attempt < 8; ++attempt) {
@@ -634,8 +646,14 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     CK(cudaMemsetAsync(t->vcount.p, 0, 64 * 4 * (kMaxDepth + 1), s));
     VoxLevel L{};
     L.st = t->state.as<DevState>();
-    CK(ensure(t->stash, std::max<uint64_t>(t->n, 1) * 8));
-    L.stash = t->stash.as<uint2>();
+    // the stash lives only during voxelize: reuse the 2-pass distribute's record scratch
+    // (dead after the split, 16-32 B/pt) instead of another 8 B/pt
+    if (t->tmp_rec.cap >= std::max<uint64_t>(t->n, 1) * 8) {
+      L.stash = t->tmp_rec.as<uint2>();
+    } else {
+      CK(ensure(t->stash, std::max<uint64_t>(t->n, 1) * 8));
+      L.stash = t->stash.as<uint2>();
+    }
     L.fmt = t->fmt;
     L.leaf_pts = t->leaf_pts.p;
     L.n_box = t->n_box.as<double4>();
@@ -854,7 +872,7 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
                    &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey};
+                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -1019,7 +1037,7 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->vox, &t->scratch, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
                          &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey};
+                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;

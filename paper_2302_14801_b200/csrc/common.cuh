@@ -95,10 +95,17 @@ struct Rec<LOD_POINTS_F32> {
   __device__ __forceinline__ static void store(void* base, uint64_t i, const Raw& r) {
     reinterpret_cast<uint4*>(base)[i] = r.a;
   }
+  __device__ __forceinline__ static float xf(const Raw& r) { return __uint_as_float(r.a.x); }
+  __device__ __forceinline__ static float yf(const Raw& r) { return __uint_as_float(r.a.y); }
+  __device__ __forceinline__ static float zf(const Raw& r) { return __uint_as_float(r.a.z); }
   __device__ __forceinline__ static double x(const Raw& r) { return (double)__uint_as_float(r.a.x); }
   __device__ __forceinline__ static double y(const Raw& r) { return (double)__uint_as_float(r.a.y); }
   __device__ __forceinline__ static double z(const Raw& r) { return (double)__uint_as_float(r.a.z); }
   __device__ __forceinline__ static uint32_t rgb(const Raw& r) { return r.a.w & 0xFFFFFFu; }
+  // the pad byte carries the 2nd-pass distribute digit between the two passes
+  static constexpr int kTagBits = 8;
+  __device__ __forceinline__ static uint32_t tag(const Raw& r) { return r.a.w >> 24; }
+  __device__ __forceinline__ static void set_tag(Raw& r, uint32_t t) { r.a.w = (r.a.w & 0xFFFFFFu) | (t << 24); }
 };
 
 template <>
@@ -118,6 +125,9 @@ struct Rec<LOD_POINTS_F64> {
     p[0] = r.a;
     p[1] = r.b;
   }
+  __device__ __forceinline__ static float xf(const Raw& r) { return (float)x(r); }
+  __device__ __forceinline__ static float yf(const Raw& r) { return (float)y(r); }
+  __device__ __forceinline__ static float zf(const Raw& r) { return (float)z(r); }
   __device__ __forceinline__ static double x(const Raw& r) {
     return __hiloint2double((int)r.a.y, (int)r.a.x);
   }
@@ -128,6 +138,9 @@ struct Rec<LOD_POINTS_F64> {
     return __hiloint2double((int)r.b.y, (int)r.b.x);
   }
   __device__ __forceinline__ static uint32_t rgb(const Raw& r) { return r.b.z & 0xFFFFFFu; }
+  static constexpr int kTagBits = 32;
+  __device__ __forceinline__ static uint32_t tag(const Raw& r) { return r.b.w; }
+  __device__ __forceinline__ static void set_tag(Raw& r, uint32_t t) { r.b.w = t; }
 };
 
 // ---------------------------------------------------------------------------
@@ -176,6 +189,44 @@ __device__ __forceinline__ Cell16 cell16(const typename Rec<FMT>::Raw& r, const 
 __device__ __forceinline__ uint32_t grid_cell128(double p, double lo, double size, double inv) {
   double f = exact_scaled_floor<7>(__dsub_rn(p, lo), size, inv);
   return (uint32_t)fmin(fmax(f, 0.0), 127.0);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 fast path for float32 coordinates (exactness kept by a certificate):
+//   v = fl32(fl32(p - lo32) * s32),  lo32 = fl32(lo), s32 = fl32(2^K / size)
+// differs from the reference's RN64(RN64(p - lo) / size) * 2^K by at most
+//   band = 2^-24 2^K (|lo| / size + 3) (1 + 1e-3) + 1e-12
+// (one rounding of lo, p - lo, s and the product; the fp64 roundings are ~2^-52).  When v
+// is farther than `band` from every integer and inside (0, 2^K), floor(v) IS the exact cell
+// and the point is inside the bounds; otherwise the caller takes the exact fp64 path.  At
+// K = 7..8 the band is ~1e-4 cells, so about 1e-4 of the axes fall back.
+// ---------------------------------------------------------------------------
+struct Frame32 {
+  float lo[3];
+  float s;       // fl32(2^K / size)
+  float band;
+};
+
+__host__ __device__ __forceinline__ Frame32 make_frame32(double lx, double ly, double lz, double size, int K) {
+  Frame32 f;
+  f.lo[0] = (float)lx, f.lo[1] = (float)ly, f.lo[2] = (float)lz;
+  const double scale = (double)(1u << K) / size;
+  f.s = (float)scale;
+  const double m = fmax(fabs(lx), fmax(fabs(ly), fabs(lz)));
+  const double band = 0x1p-24 * (double)(1u << K) * (m / size + 3.0) * 1.001 + 1e-12;
+  f.band = band < 0.25 && isfinite(scale) && scale < 1e30 ? (float)band : 1.0f;  // 1.0: never certain
+  return f;
+}
+
+__device__ __forceinline__ bool fast_cell(float p, float lo32, float s32, float band, float lim, uint32_t& cell) {
+  const float v = __fmul_rn(__fsub_rn(p, lo32), s32);
+  const float f = floorf(v);
+  const float fr = v - f;  // exact (Sterbenz)
+  if (fr > band && fr < 1.0f - band && f >= 0.0f && f < lim) {
+    cell = (uint32_t)f;
+    return true;
+  }
+  return false;
 }
 
 // linear x-major key of the cell at `depth` (partition.py:23-24)

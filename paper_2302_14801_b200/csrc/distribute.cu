@@ -32,24 +32,11 @@ namespace {
 constexpr int kW = kRadixThreads / 32;
 constexpr int K = kRadixItems;
 
-struct Proj {
-  double lo0, lo1, lo2, size, inv;
-};
 
-__device__ __forceinline__ Proj proj_of(const SplitView& v) {
-  return Proj{v.st->lo[0], v.st->lo[1], v.st->lo[2], v.st->size, v.st->inv_size};
-}
-
-// Leaf of point i from its stored finest main-grid key (K_count wrote pkey), descending
-// the extension grids from the record when the target says so; -1 if unresolved.
-template <int FMT>
-__device__ __forceinline__ int32_t leaf_from_record(const SplitView& v, const Proj& pj, uint64_t i, int32_t t,
-                                                 bool& bad) {
-  const auto r = Rec<FMT>::load(v.pts, i);
-  Cell16 c;
-  c.x = quant16(Rec<FMT>::x(r), pj.lo0, pj.size, pj.inv, bad);
-  c.y = quant16(Rec<FMT>::y(r), pj.lo1, pj.size, pj.inv, bad);
-  c.z = quant16(Rec<FMT>::z(r), pj.lo2, pj.size, pj.inv, bad);
+// Leaf of point i inside an extension grid (target t <= -2): descend from the depth-16 cell
+// the first extension round stored (pc16); -1 if unresolved.
+__device__ __forceinline__ int32_t leaf_from_c16(const SplitView& v, uint64_t i, int32_t t) {
+  const Cell16 c = unpack_c16(__ldg(v.pc16 + i));
   uint32_t e, rr;
   if (ext_descend(v, c, e, rr, t)) t = v.te[v.meta[e].tgt_off + rr];
   return t;
@@ -58,10 +45,9 @@ __device__ __forceinline__ int32_t leaf_from_record(const SplitView& v, const Pr
 // Leaf ids of one warp's K x 32 items starting at `base`.  FIRST: through the target table
 // from the point's finest main-grid key (no record read, no fp64 projection except for
 // points inside extension grids); else the ids of the previous pass.
-template <int FMT, bool FIRST>
-__device__ __forceinline__ void load_items(const SplitView& v, const Proj& pj, const uint32_t* in_leaf,
-                                           uint64_t base, int lane, uint32_t (&leaf)[K], bool& bad,
-                                           bool& unresolved) {
+template <int FMT, bool FIRST, bool TAGIN>
+__device__ __forceinline__ void load_items(const SplitView& v, const void* in_rec, const uint32_t* in_leaf,
+                                           uint64_t base, int lane, uint32_t (&leaf)[K], bool& unresolved) {
   const uint64_t last = v.n - 1;
   if (FIRST) {
     uint32_t key[K];
@@ -76,12 +62,18 @@ __device__ __forceinline__ void load_items(const SplitView& v, const Proj& pj, c
     for (int k = 0; k < K; ++k) {
       const uint64_t i = base + (uint64_t)k * 32 + lane;
       int32_t t = (int32_t)leaf[k];
-      if (t <= -2) t = leaf_from_record<FMT>(v, pj, i < last ? i : last, t, bad);
+      if (t <= -2) t = leaf_from_c16(v, i < last ? i : last, t);
       if (t < 0) {
         unresolved |= i < v.n;
         t = 0;
       }
       leaf[k] = (uint32_t)t;
+    }
+  } else if (TAGIN) {  // 2nd pass: the digit rides in the record's pad
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t i = base + (uint64_t)k * 32 + lane;
+      leaf[k] = Rec<FMT>::tag(Rec<FMT>::load(in_rec, i < last ? i : last));
     }
   } else {
 #pragma unroll
@@ -96,7 +88,7 @@ __device__ __forceinline__ void load_items(const SplitView& v, const Proj& pj, c
 // ---------------------------------------------------------------------------
 // K_hist: per-chunk digit counts
 // ---------------------------------------------------------------------------
-template <int FMT, bool FIRST>
+template <int FMT, bool FIRST, bool TAGIN>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_dist_hist(SplitView v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_out, int shift, int bits,
                 uint32_t seg_tiles, uint32_t tiles, uint32_t* counts) {
@@ -105,13 +97,12 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   for (int d = threadIdx.x; d < B; d += kRadixThreads) hist[d] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const Proj pj = proj_of(v);
-  bool bad = false, unresolved = false;
+  bool unresolved = false;
   const uint32_t t0 = blockIdx.x * seg_tiles, t1 = min(t0 + seg_tiles, tiles);
   for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
     uint32_t leaf[K];
-    load_items<FMT, FIRST>(v, pj, in_leaf, base, lane, leaf, bad, unresolved);
+    load_items<FMT, FIRST, TAGIN>(v, in_rec, in_leaf, base, lane, leaf, unresolved);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const bool valid = base + (uint64_t)k * 32 + lane < v.n;
@@ -131,29 +122,61 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   __syncthreads();
   for (int d = threadIdx.x; d < B; d += kRadixThreads) counts[(uint64_t)blockIdx.x * B + d] = hist[d];
   if (FIRST) {
-    if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) raise_err(v.st, ERR_OUTSIDE);
     if (__any_sync(0xFFFFFFFFu, unresolved) && lane == 0) raise_err(v.st, ERR_UNRESOLVED);
   }
 }
 
 // ---------------------------------------------------------------------------
-// K_scan: counts[g][d] -> digit_base[d] + sum_{g' < g} counts[g'][d]  (first slots)
-// 32 digits per block (lanes), the chunks split over the 32 warps.
+// K_scan: counts[g][d] -> digit_base[d] + sum_{g' < g} counts[g'][d]  (first slots), as
+// three parallel steps over (32-digit column, segment of rows) blocks:
+//   part  per segment and digit: the segment's column sums        -> part[seg][d]
+//   scan  per digit: exclusive prefix over the segments + base     (one small block)
+//   apply per segment: exclusive prefix of its rows from part[seg][d], in place
+// (one block per 32 digits walking every row serially took 2.7 ms at 500M points).
+// Inside a block the segment's rows are split over the 32 warps; lanes are digits.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_dist_scan(uint32_t* counts, uint32_t segs, int B,
-                                                    const uint64_t* digit_base) {
+__device__ __forceinline__ void rows_of(uint32_t rows, uint32_t seg_rows, uint32_t seg, int warp, uint32_t& g0,
+                                        uint32_t& g1) {
+  const uint32_t r0 = min(rows, seg * seg_rows), r1 = min(rows, r0 + seg_rows);
+  const uint32_t per = (r1 - r0 + 31) / 32;
+  g0 = min(r1, r0 + warp * per);
+  g1 = min(r1, g0 + per);
+}
+
+__global__ void __launch_bounds__(1024) k_dist_scan_part(const uint32_t* counts, uint32_t rows, uint32_t seg_rows,
+                                                         int B, uint32_t* part) {
+  __shared__ uint32_t sm[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = blockIdx.x * 32 + lane;
+  uint32_t g0, g1;
+  rows_of(rows, seg_rows, blockIdx.y, warp, g0, g1);
+  uint32_t sum = 0;
+  if (d < B)
+    for (uint32_t g = g0; g < g1; ++g) sum += __ldcg(counts + (uint64_t)g * B + d);
+  sm[warp][lane] = sum;
+  __syncthreads();
+  if (warp == 0 && d < B) {
+    uint32_t t = 0;
+    for (int w = 0; w < 32; ++w) t += sm[w][lane];
+    part[(uint64_t)blockIdx.y * B + d] = t;
+  }
+}
+
+// exclusive prefix of rows [0, rows) of a[g][d], plus base[d] (if any), in place
+__global__ void __launch_bounds__(1024) k_dist_scan_apply(uint32_t* a, uint32_t rows, uint32_t seg_rows, int B,
+                                                          const uint32_t* seg_base, const uint64_t* base) {
   __shared__ uint32_t part[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = blockIdx.x * 32 + lane;
-  const uint32_t per = (segs + 31) / 32;
-  const uint32_t g0 = min(segs, warp * per), g1 = min(segs, g0 + per);
-  uint32_t s = 0;
+  uint32_t g0, g1;
+  rows_of(rows, seg_rows, blockIdx.y, warp, g0, g1);
+  uint32_t sum = 0;
   if (d < B)
-    for (uint32_t g = g0; g < g1; ++g) s += counts[(uint64_t)g * B + d];
-  part[warp][lane] = s;
+    for (uint32_t g = g0; g < g1; ++g) sum += a[(uint64_t)g * B + d];
+  part[warp][lane] = sum;
   __syncthreads();
   if (warp == 0) {
-    uint32_t run = d < B ? (uint32_t)digit_base[d] : 0;
+    uint32_t run = d >= B ? 0 : seg_base ? seg_base[(uint64_t)blockIdx.y * B + d] : (uint32_t)base[d];
     for (int w = 0; w < 32; ++w) {
       const uint32_t c = part[w][lane];
       part[w][lane] = run;
@@ -164,20 +187,40 @@ __global__ void __launch_bounds__(1024) k_dist_scan(uint32_t* counts, uint32_t s
   if (d < B) {
     uint32_t run = part[warp][lane];
     for (uint32_t g = g0; g < g1; ++g) {
-      const uint32_t c = counts[(uint64_t)g * B + d];
-      counts[(uint64_t)g * B + d] = run;
+      const uint32_t c = a[(uint64_t)g * B + d];
+      a[(uint64_t)g * B + d] = run;
       run += c;
     }
   }
 }
 
+// first slots of every (tile, digit); part: >= 2 * kScanSegs * B words of scratch
+constexpr uint32_t kScanSegs = 512;
+int launch_dist_scan(uint32_t* counts, uint32_t rows, int B, const uint64_t* digit_base, uint32_t* part,
+                     cudaStream_t s) {
+  const uint32_t dcols = ceil_div_u32(B, 32);
+  const uint32_t seg_rows = std::max<uint32_t>(64, ceil_div_u32(rows, kScanSegs));
+  const uint32_t segs = ceil_div_u32(rows, seg_rows);
+  if (segs <= 1) {
+    k_dist_scan_apply<<<dim3(dcols, 1), 1024, 0, s>>>(counts, rows, rows, B, nullptr, digit_base);
+    return 1;
+  }
+  k_dist_scan_part<<<dim3(dcols, segs), 1024, 0, s>>>(counts, rows, seg_rows, B, part);
+  k_dist_scan_apply<<<dim3(dcols, 1), 1024, 0, s>>>(part, segs, segs, B, nullptr, digit_base);
+  k_dist_scan_apply<<<dim3(dcols, segs), 1024, 0, s>>>(counts, rows, seg_rows, B, part, nullptr);
+  return 3;
+}
+
 // ---------------------------------------------------------------------------
 // K_scatter: stable scatter; chunks in reverse launch order, sub-tiles in order
 // ---------------------------------------------------------------------------
-template <int FMT, bool FIRST, bool LAST>
+// OUT: what travels to the next pass with each record
+enum { OUT_FINAL = 0, OUT_LEAF = 1, OUT_TAG = 2 };
+
+template <int FMT, bool TAGIN, int OUT>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_dist_scatter(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
-                   int shift, int bits, uint32_t seg_tiles, uint32_t tiles, const uint32_t* firsts) {
+                   int shift, int bits, int tag_shift, uint32_t seg_tiles, uint32_t tiles, const uint32_t* firsts) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int B = 1 << bits;
   uint32_t* run = reinterpret_cast<uint32_t*>(smem);               // [B] first slot of the sub-tile
@@ -187,8 +230,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   for (int d = threadIdx.x; d < B; d += kRadixThreads) run[d] = firsts[(uint64_t)chunk * B + d];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1;
-  const Proj pj = proj_of(v);
-  bool bad = false, unresolved = false;
+  bool unresolved = false;
   const uint32_t t0 = chunk * seg_tiles, t1 = min(t0 + seg_tiles, tiles);
   for (uint32_t tile = t0; tile < t1; ++tile) {
     for (int i = threadIdx.x; i < kW * B / 2; i += kRadixThreads) reinterpret_cast<uint32_t*>(wh)[i] = 0;
@@ -196,7 +238,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
     uint32_t leaf[K];
     uint16_t rk[K];
-    load_items<FMT, FIRST>(v, pj, in_leaf, base, lane, leaf, bad, unresolved);
+    load_items<FMT, false, TAGIN>(v, in_rec, in_leaf, base, lane, leaf, unresolved);
     // stable in-warp ranks (item-major, lane order)
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -244,8 +286,11 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
       if (i < v.n) {
         const uint32_t d = (leaf[k] >> shift) & (B - 1);
         const uint64_t dest = (uint64_t)run[d] + wh[warp * B + d] + rk[k];
-        Rec<FMT>::store(out_rec, dest, Rec<FMT>::load(in_rec, i));
-        if (!LAST) out_leaf[dest] = leaf[k];
+        auto rec = Rec<FMT>::load(in_rec, i);
+        if (OUT == OUT_TAG) Rec<FMT>::set_tag(rec, leaf[k] >> tag_shift);  // the next pass's digit
+        if (OUT == OUT_FINAL && TAGIN) Rec<FMT>::set_tag(rec, 0);
+        Rec<FMT>::store(out_rec, dest, rec);
+        if (OUT == OUT_LEAF) out_leaf[dest] = leaf[k];
       }
     }
     __syncthreads();
@@ -272,13 +317,15 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
 }
 
 // One digit pass.  FIRST: the leaf ids are resolved once by K_hist, which stores them
-// (leaf_tmp) for K_scatter.
-template <int FMT, bool FIRST, bool LAST>
+// (leaf_tmp) for K_scatter.  TAGIN: the digit is read from the records' pad (written by the
+// previous pass with OUT_TAG); OUT_LEAF: the leaf ids travel in a separate array.
+template <int FMT, bool FIRST, bool TAGIN, int OUT>
 int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_tmp, void* out_rec,
-             uint32_t* out_leaf, int shift, int bits, const uint64_t* digit_base, const RadixPlan& p, cudaStream_t s) {
+             uint32_t* out_leaf, int shift, int bits, int tag_shift, const uint64_t* digit_base, const RadixPlan& p,
+             cudaStream_t s) {
   const int B = 1 << bits;
-  auto hist = k_dist_hist<FMT, FIRST>;
-  auto scat = k_dist_scatter<FMT, false, LAST>;
+  auto hist = k_dist_hist<FMT, FIRST, TAGIN>;
+  auto scat = k_dist_scatter<FMT, TAGIN, OUT>;
   const size_t hsm = (size_t)B * 4, ssm = (size_t)B * 8 + (size_t)kW * B * 2 + 4 * kW;
   static bool configured = false;
   if (!configured) {
@@ -289,10 +336,10 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   }
   const uint32_t* leaf_in = FIRST ? leaf_tmp : in_leaf;
   hist<<<p.segs, kRadixThreads, hsm, s>>>(v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
-  k_dist_scan<<<ceil_div_u32(B, 32), 1024, 0, s>>>(p.counts, p.segs, B, digit_base);
-  scat<<<p.segs, kRadixThreads, ssm, s>>>(v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, p.seg_tiles, p.tiles,
-                                          p.counts);
-  return 3;
+  const int nscan = launch_dist_scan(p.counts, p.segs, B, digit_base, p.scan_part, s);
+  scat<<<p.segs, kRadixThreads, ssm, s>>>(v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,
+                                          p.seg_tiles, p.tiles, p.counts);
+  return 2 + nscan;
 }
 
 template <int FMT>
@@ -309,18 +356,26 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
   k_digit_scan<<<1, 1024, 0, s>>>(base0, B0);
   launches += 2;
   if (p.passes == 1)
-    return launches + run_pass<FMT, true, true>(v, v.pts, nullptr, p.tmp_leaf, leaf_out, nullptr, 0, p.bits[0],
-                                                base0, p, s);
+    return launches + run_pass<FMT, true, false, OUT_FINAL>(v, v.pts, nullptr, p.tmp_leaf, leaf_out, nullptr, 0,
+                                                           p.bits[0], 0, base0, p, s);
   k_digit_hist<<<lb, 256, 0, s>>>(v.leaf_count, v.n_leaves, p.bits[0], p.bits[1],
                                   reinterpret_cast<unsigned long long*>(base1));
   k_digit_scan<<<1, 1024, 0, s>>>(base1, B1);
   launches += 2;
+  if (p.bits[1] <= Rec<FMT>::kTagBits) {
+    // the 2nd digit rides in the record pad: no scattered 4-B leaf-id stream (its partial
+    // sectors cost read-modify-writes), the 2nd pass reads digits from the records
+    launches += run_pass<FMT, true, false, OUT_TAG>(v, v.pts, nullptr, p.tmp_leaf, p.tmp_rec, nullptr, 0,
+                                                    p.bits[0], p.bits[0], base0, p, s);
+    launches += run_pass<FMT, false, true, OUT_FINAL>(v, p.tmp_rec, nullptr, nullptr, leaf_out, nullptr, 0,
+                                                      p.bits[1], 0, base1, p, s);
+    return launches;
+  }
   uint32_t* sorted_leaf = p.tmp_leaf + v.n;
-  launches += run_pass<FMT, true, false>(v, v.pts, nullptr, p.tmp_leaf, p.tmp_rec, sorted_leaf, 0, p.bits[0], base0,
-                                         p, s);
-  launches += run_pass<FMT, false, true>(v, p.tmp_rec, sorted_leaf, nullptr, leaf_out, nullptr, p.bits[0], p.bits[1],
-                                         base1,
-                                         p, s);
+  launches += run_pass<FMT, true, false, OUT_LEAF>(v, v.pts, nullptr, p.tmp_leaf, p.tmp_rec, sorted_leaf, 0,
+                                                   p.bits[0], 0, base0, p, s);
+  launches += run_pass<FMT, false, false, OUT_FINAL>(v, p.tmp_rec, sorted_leaf, nullptr, leaf_out, nullptr,
+                                                     p.bits[0], p.bits[1], 0, base1, p, s);
   return launches;
 }
 

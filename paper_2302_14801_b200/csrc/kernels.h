@@ -23,6 +23,8 @@ struct SplitView {
   int32_t* node_idx;      // slot -> node id (valid at non-zero slots)
   int32_t* t8;            // main finest level: leaf id, -(ext+2), or -1
   uint32_t* pkey;         // per point: its main finest-level key (written by K_count)
+  uint64_t* pc16;         // per point inside an extension grid: packed depth-16 cell
+                          // (x | y << 16 | z << 32), written by the first extension round
   int32_t* te;            // ext finest levels: same encoding
   ExtMeta* meta;
   uint32_t n_ext;
@@ -91,6 +93,10 @@ int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_
                       const uint64_t* list, uint32_t parent_first, uint64_t pyr_base, uint64_t tgt_base,
                       int base_depth, int ext_levels, cudaStream_t s);
 int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first_ext, cudaStream_t s);
+
+__device__ __forceinline__ Cell16 unpack_c16(uint64_t p) {
+  return Cell16{(uint32_t)p & 0xFFFF, (uint32_t)(p >> 16) & 0xFFFF, (uint32_t)(p >> 32) & 0xFFFF};
+}
 int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint32_t* round_count,
                      const int* round_ext, const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s);
 int launch_count_nodes(const SplitView& v, uint64_t total_slots, uint64_t* slots_out, ScanScratch& scr,
@@ -115,6 +121,7 @@ struct RadixPlan {
   uint32_t segs;          // chunks (one CTA each)
   uint32_t seg_tiles;     // sub-tiles per chunk
   uint32_t* counts;       // [segs][2^bits] digit counts -> first slots (reused per pass)
+  uint32_t* scan_part;    // 2 x 512 x 2^bits words: per-segment column sums of the counts
   uint64_t* digit_base;   // per pass: 2^bits global exclusive prefix
   void* tmp_rec;          // pass-0 output records (2 passes)
   uint32_t* tmp_leaf;     // leaf ids: input order (K_hist, pass 0) [+ sorted by digit 0]

@@ -151,6 +151,8 @@ constexpr int kCountUnroll = 4;
 template <int FMT>
 __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
   const DevState st = *v.st;
+  const Frame32 fr = make_frame32(st.lo[0], st.lo[1], st.lo[2], st.size, v.D);
+  const float lim = (float)(1u << v.D);
   uint32_t* grid = v.pyr + level_off(v.D);
   const int lane = threadIdx.x & 31;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -168,7 +170,14 @@ __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
       bool valid = i < v.n;
       uint32_t key = 0;
       if (valid) {
-        key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
+        uint32_t cx, cy, cz;
+        if (FMT == LOD_POINTS_F32 &&
+            fast_cell(Rec<FMT>::xf(r[u]), fr.lo[0], fr.s, fr.band, lim, cx) &&
+            fast_cell(Rec<FMT>::yf(r[u]), fr.lo[1], fr.s, fr.band, lim, cy) &&
+            fast_cell(Rec<FMT>::zf(r[u]), fr.lo[2], fr.s, fr.band, lim, cz))
+          key = (cx << (2 * v.D)) | (cy << v.D) | cz;
+        else
+          key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
         v.pkey[i] = key;  // reused by extension counting and the distribute (no re-projection)
       }
       // warp-uniform cell (coherent scans, dense clusters): one aggregated add;
@@ -284,11 +293,19 @@ __global__ void __launch_bounds__(kThreads) k_ext_count(SplitView v, uint32_t ro
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < v.n; base += stride) {
     uint64_t i = base + threadIdx.x;
     uint64_t slot = ~0ull;
-    // only points inside an extension grid (target <= -2) re-project their record
+    // only points inside an extension grid (target <= -2) need their depth-16 cell: the
+    // first round projects the record once and keeps it (pc16) for the later rounds and
+    // the distribute
     const int32_t t = i < v.n ? __ldg(v.t8 + __ldg(v.pkey + i)) : -1;
     if (t <= -2) {
-      auto r = Rec<FMT>::load(v.pts, i);
-      Cell16 c = cell16<FMT>(r, st, bad);
+      Cell16 c;
+      if (round_first == 0) {
+        auto r = Rec<FMT>::load(v.pts, i);
+        c = cell16<FMT>(r, st, bad);
+        v.pc16[i] = (uint64_t)c.x | ((uint64_t)c.y << 16) | ((uint64_t)c.z << 32);
+      } else {
+        c = unpack_c16(__ldg(v.pc16 + i));
+      }
       uint32_t e, rr;
       if (ext_descend(v, c, e, rr, t) && e >= round_first) {
         const ExtMeta& m = v.meta[e];

@@ -11,7 +11,8 @@
 //
 //   K0 setup     one thread per node: children, ordinals, sample chunks (sampling.py:21-47)
 //   K1 occupy    all samples, test-and-set their bit (L2 atomics only on first touch)
-//   K2 words     per 4096-word block: popcount sums; node offsets; prefix + key emission
+//   K2 words     per 4096-word block: popcount sums; node offsets; word prefixes, voxel
+//                keys, the block's accumulators zeroed (one coalesced sweep of its ranks)
 //   K3 scatter   LEAF-point samples only: integer channel sums + counts (average,
 //                sampling.py:88-97) or atomicMax of (rand12 | ordinal20) (random,
 //                sampling.py:69-85 / PAPER Listing 1)
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
   if (L.st->err & ERR_ARENA) return;
   __shared__ uint32_t rb[kRegionWords];
   const uint32_t nch = L.counters[0];
-  constexpr int U = 8;
+  constexpr int U = FMT == LOD_POINTS_F32 ? 8 : 4;  // records in flight per thread
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const uint4 ch = L.chunks[c];
     const VoxNode& nd = L.info[ch.x];
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
     if (nd.cslot[o] == -1) {
       const double4 b = nd.box;
       const double inv = nd.inv;
+      const Frame32 fr = make_frame32(b.x, b.y, b.z, b.w, 7);  // certified fp32 first (common.cuh)
       for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kRT) {
         typename Rec<FMT>::Raw r[U];
 #pragma unroll
@@ -213,9 +215,14 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
         for (int u = 0; u < U; ++u) {
           const uint32_t j = j0 + u * kRT;
           if (j >= ch.w) continue;
-          const uint32_t key = (grid_cell128(Rec<FMT>::x(r[u]), b.x, b.w, inv) << 14) |
-                               (grid_cell128(Rec<FMT>::y(r[u]), b.y, b.w, inv) << 7) |
-                               grid_cell128(Rec<FMT>::z(r[u]), b.z, b.w, inv);
+          uint32_t cx, cy, cz, key;
+          if (FMT == LOD_POINTS_F32 && fast_cell(Rec<FMT>::xf(r[u]), fr.lo[0], fr.s, fr.band, 128.f, cx) &&
+              fast_cell(Rec<FMT>::yf(r[u]), fr.lo[1], fr.s, fr.band, 128.f, cy) &&
+              fast_cell(Rec<FMT>::zf(r[u]), fr.lo[2], fr.s, fr.band, 128.f, cz))
+            key = (cx << 14) | (cy << 7) | cz;
+          else
+            key = (grid_cell128(Rec<FMT>::x(r[u]), b.x, b.w, inv) << 14) |
+                  (grid_cell128(Rec<FMT>::y(r[u]), b.y, b.w, inv) << 7) | grid_cell128(Rec<FMT>::z(r[u]), b.z, b.w, inv);
           L.stash[first + j] = make_uint2(key, Rec<FMT>::rgb(r[u]));
           mark(key);
         }
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
 }
 
 // ---------------------------------------------------------------------------
-// K2: popcount sums per 4096-word block, node offsets, prefix + key emission
+// K2: popcount sums per 4096-word block, node offsets, word prefixes
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kT) k_block_sums(VoxLevel L) {
   const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
@@ -317,53 +324,68 @@ __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
   }
 }
 
-__global__ void __launch_bounds__(kT) k_prefix_emit(VoxLevel L) {
-  const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
-  const VoxNode& nd = L.info[s];
-  if (nd.skip || L.st->err & ERR_ARENA) return;
-  __shared__ uint32_t sm[kT / 32 + 1];
-  __shared__ __align__(16) uint32_t sbits[kBlkWords];
-  __shared__ __align__(16) uint32_t spre[kBlkWords];
+// Stage one 4096-word block of a node's bitmap in shared memory and compute every word's
+// exclusive popcount prefix (= voxel rank of its first set bit) into spre; returns the
+// block's voxel count.
+__device__ __forceinline__ uint32_t stage_block(const VoxLevel& L, uint32_t s, uint32_t blk, uint32_t* sbits,
+                                                uint32_t* spre, uint32_t* sm) {
   const uint32_t* bits = bits_of(L, L.parity, s) + blk * kBlkWords;
-  uint32_t* pre = pre_of(L, L.parity, s) + blk * kBlkWords;
-  // coalesced stage of the block's words
   for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT)
     reinterpret_cast<uint4*>(sbits)[i] = __ldcg(reinterpret_cast<const uint4*>(bits) + i);
   __syncthreads();
-  // prefix over 16 consecutive words per thread
-  constexpr uint32_t per = kBlkWords / kT;
+  constexpr uint32_t per = kBlkWords / kT;  // 16 consecutive words per thread
   uint32_t c = 0;
 #pragma unroll
   for (uint32_t q = 0; q < per; ++q) c += __popc(sbits[threadIdx.x * per + ((q + threadIdx.x) & (per - 1))]);
   uint32_t tot;
-  uint32_t r = block_excl_scan<uint32_t, kT>(c, &tot, sm) + L.blk_sum[blockIdx.x];
+  uint32_t r = block_excl_scan<uint32_t, kT>(c, &tot, sm) + L.blk_sum[s * kBlksPerNode + blk];
 #pragma unroll
   for (uint32_t q = 0; q < per; ++q) {
     spre[threadIdx.x * per + q] = r;
     r += __popc(sbits[threadIdx.x * per + q]);
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT)
-    reinterpret_cast<uint4*>(pre)[i] = reinterpret_cast<const uint4*>(spre)[i];
-  // emission: lanes own consecutive words, so their voxel ranks are adjacent
-  const uint64_t acc0 = nd.vbase - L.level_start[0];
+  return tot;
+}
+
+// K2b: word prefixes to HBM (for rank lookups by K3 and the parent level's gathers), the
+// voxel keys, and the block's accumulators zeroed -- its voxels are the contiguous rank
+// range [blk_sum, blk_sum + tot), so the zeroing is one coalesced sweep.
+__global__ void __launch_bounds__(kT) k_prefix(VoxLevel L) {
+  const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
+  const VoxNode& nd = L.info[s];
+  if (nd.skip || L.st->err & ERR_ARENA) return;
+  __shared__ uint32_t sm[kT / 32 + 1];
+  __shared__ __align__(16) uint32_t sbits[kBlkWords];
+  __shared__ __align__(16) uint32_t spre[kBlkWords];
+  const uint32_t tot = stage_block(L, s, blk, sbits, spre, sm);
+  uint32_t* pre = pre_of(L, L.parity, s) + blk * kBlkWords;
+  // a prefix is only ever read for a word with a set bit (rank of an occupied key), so the
+  // prefixes of empty 4-word groups are not written: sparse (surface) nodes skip most of it
+  for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT) {
+    const uint4 b4 = reinterpret_cast<const uint4*>(sbits)[i];
+    if (b4.x | b4.y | b4.z | b4.w) reinterpret_cast<uint4*>(pre)[i] = reinterpret_cast<const uint4*>(spre)[i];
+  }
+  // voxel keys in rank order (K4 reads them back voxel-parallel)
   for (uint32_t wi = threadIdx.x; wi < kBlkWords; wi += kT) {
     uint32_t bw = sbits[wi];
     uint32_t rr = spre[wi];
     const uint32_t key0 = (blk * kBlkWords + wi) << 5;
     while (bw) {
-      uint32_t bit = __ffs(bw) - 1;
+      const uint32_t bit = __ffs(bw) - 1;
       bw &= bw - 1;
-      L.vox[nd.vbase + rr] = make_uint2(key0 + bit, 0);
-      if (L.mode == LOD_MODE_AVERAGE) {
-        reinterpret_cast<ulonglong2*>(L.acc)[acc0 + rr] = make_ulonglong2(0, 0);
-      } else if (L.mode == LOD_MODE_WEIGHTED) {
-        reinterpret_cast<ulonglong2*>(L.acc)[2 * (acc0 + rr)] = make_ulonglong2(0, 0);
-        reinterpret_cast<ulonglong2*>(L.acc)[2 * (acc0 + rr) + 1] = make_ulonglong2(0, 0);
-      } else {
-        reinterpret_cast<uint32_t*>(L.acc)[acc0 + rr] = 0;
-      }
-      ++rr;
+      L.vox[nd.vbase + rr++].x = key0 + bit;
+    }
+  }
+  const uint64_t a0 = nd.vbase - L.level_start[0] + L.blk_sum[blockIdx.x];
+  for (uint32_t i = threadIdx.x; i < tot; i += kT) {
+    if (L.mode == LOD_MODE_AVERAGE) {
+      reinterpret_cast<uint4*>(L.acc)[a0 + i] = make_uint4(0, 0, 0, 0);
+    } else if (L.mode == LOD_MODE_WEIGHTED) {
+      reinterpret_cast<uint4*>(L.acc)[2 * (a0 + i)] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4*>(L.acc)[2 * (a0 + i) + 1] = make_uint4(0, 0, 0, 0);
+    } else {
+      reinterpret_cast<uint32_t*>(L.acc)[a0 + i] = 0;
     }
   }
 }
@@ -393,8 +415,9 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
     const int o = (int)ch.y;
     for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) {
       const uint32_t gw = region_to_global(i, o);
-      rbits[i] = __ldcg(bits + gw);
-      rpre[i] = __ldcg(pre + gw);
+      const uint32_t w = __ldcg(bits + gw);
+      rbits[i] = w;
+      if (w) rpre[i] = __ldcg(pre + gw);  // empty words' prefixes are never read (nor written)
     }
     __syncthreads();
     const uint2* src = L.stash + nd.cfirst[o];
@@ -467,8 +490,9 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter_w(VoxLevel L) {
     const int o = (int)ch.y;
     for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) {
       const uint32_t gw = region_to_global(i, o);
-      rbits[i] = __ldcg(bits + gw);
-      rpre[i] = __ldcg(pre + gw);
+      const uint32_t w = __ldcg(bits + gw);
+      rbits[i] = w;
+      if (w) rpre[i] = __ldcg(pre + gw);  // empty words' prefixes are never read (nor written)
     }
     __syncthreads();
     const bool leaf = nd.cslot[o] == -1;
@@ -545,90 +569,97 @@ __device__ __forceinline__ uint32_t leaf_winner_rgb(const VoxLevel& L, const Vox
   return __ldg(&L.stash[nd.cfirst[oo] + (ord - nd.cbase[oo])].y);
 }
 
+// Colour of voxel `r` (key `key`) of node `nd`: children's samples gathered / accumulated
+// per mode; writes the record's colour (and, first-come, the winning ordinal).
+__device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode& nd, uint64_t acc0, uint32_t key,
+                                               uint32_t r) {
+  const int cpar = L.parity ^ 1;
+  if (L.mode == LOD_MODE_WEIGHTED) {
+    const unsigned long long* a = reinterpret_cast<const unsigned long long*>(L.acc) + 4 * (acc0 + r);
+    const double W = (double)__ldcg(a);
+    uint32_t rgb = 0;
+    if (!(W > 0.0)) raise_err(L.st, ERR_ZERO_WEIGHT, nd.node);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double m = floor(__dadd_rn(__ddiv_rn((double)__ldcg(a + 1 + k), W), 0.5));
+      rgb |= (uint32_t)fmin(fmax(m, 0.0), 255.0) << (8 * k);
+    }
+    L.vox[nd.vbase + r].y = rgb;
+    return;
+  }
+  const uint32_t X = key >> 14, Y = (key >> 7) & 127, Z = key & 127;
+  const int o = (int)((X >> 6) | ((Y >> 6) << 1) | ((Z >> 6) << 2));
+  const int32_t cs = nd.cslot[o];
+  uint64_t sr = 0, sg = 0, sb = 0, n = 0;
+  uint32_t best = 0, best_rgb = 0;
+  bool have = false;
+  if (cs >= 0) {
+    // gather the child's 2x2x2 block: each (cx, cy) row holds both z cells in one word
+    const uint32_t* cb = bits_of(L, cpar, (uint32_t)cs);
+    const uint32_t* cp = pre_of(L, cpar, (uint32_t)cs);
+    const VoxNode& ci = L.cinfo[cs];
+    const uint32_t cx0 = (X & 63) << 1, cy0 = (Y & 63) << 1, cz0 = (Z & 63) << 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t ck = ((cx0 + (q & 1)) << 14) | ((cy0 + (q >> 1)) << 7) | cz0;
+      const uint32_t w = ck >> 5, b = ck & 31;
+      const uint32_t bw = __ldcg(cb + w);
+      const uint32_t two = (bw >> b) & 3u;
+      if (!two) continue;
+      uint32_t cr = __ldcg(cp + w) + __popc(bw & ((1u << b) - 1));
+#pragma unroll
+      for (int dz = 0; dz < 2; ++dz) {
+        if (!((two >> dz) & 1)) continue;
+        const uint32_t rgb = __ldcg(&L.vox[ci.vbase + cr].y);
+        if (L.mode == LOD_MODE_AVERAGE) {
+          sr += rgb & 0xFF, sg += (rgb >> 8) & 0xFF, sb += (rgb >> 16) & 0xFF, ++n;
+        } else if (L.mode == LOD_MODE_RANDOM) {
+          uint32_t e = rand_enc(nd.hash, nd.cbase[o] + cr);
+          if (!have || e > best) best = e, best_rgb = rgb, have = true;
+        } else {  // first-come: ordinal = octant base + the child's stored position
+          const uint32_t ord = nd.cbase[o] + __ldcg(L.vpos + ci.vbase + cr);
+          if (!have || ord < best) best = ord, best_rgb = rgb, have = true;
+        }
+        ++cr;
+      }
+    }
+  }
+  uint32_t rgb;
+  if (L.mode == LOD_MODE_AVERAGE) {
+    if (L.exact_sums) {
+      const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(L.acc) + acc0 + r);
+      sr += a.x & 0xFFFFFFFFull, sg += a.x >> 32, sb += a.y & 0xFFFFFFFFull, n += a.y >> 32;
+    } else {
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(L.acc) + acc0 + r);
+      if (fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)) >= 16777216.0f) raise_err(L.st, ERR_F32_SUMS, nd.node);
+      sr += (uint64_t)a.x, sg += (uint64_t)a.y, sb += (uint64_t)a.z, n += (uint64_t)a.w;
+    }
+    rgb = mean_round(sr, n) | (mean_round(sg, n) << 8) | (mean_round(sb, n) << 16);
+  } else if (L.mode == LOD_MODE_RANDOM) {
+    const uint32_t e = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
+    // the winner is a leaf point: its ordinal names (child, index) directly
+    rgb = (!have || e > best) ? leaf_winner_rgb(L, nd, e & 0xFFFFFu) : best_rgb;
+  } else {
+    uint32_t* a = reinterpret_cast<uint32_t*>(L.acc) + acc0 + r;
+    const uint32_t e = __ldcg(a);
+    if (e != 0 && (!have || ~e < best)) best = ~e, best_rgb = leaf_winner_rgb(L, nd, ~e);
+    rgb = best_rgb;
+    *a = best;  // winning ordinal, ranked by K5
+  }
+  L.vox[nd.vbase + r].y = rgb;
+}
+
+// K4: finalize every voxel of the level, one thread per voxel (rank chunks): a word-walk
+// per block serialised each thread's gathers and ran 5x slower (measured).
 __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
   if (L.st->err & ERR_ARENA) return;
   const uint32_t nch = L.counters[2];
-  const int cpar = L.parity ^ 1;
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const uint2 ch = L.vchunks[c];
     const VoxNode& nd = L.info[ch.x];
     const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
     const uint64_t acc0 = nd.vbase - L.level_start[0];
-    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
-      if (L.mode == LOD_MODE_WEIGHTED) {
-        const unsigned long long* a = reinterpret_cast<const unsigned long long*>(L.acc) + 4 * (acc0 + r);
-        const double W = (double)__ldcg(a);
-        uint32_t rgb = 0;
-        if (!(W > 0.0)) raise_err(L.st, ERR_ZERO_WEIGHT, nd.node);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const double m = floor(__dadd_rn(__ddiv_rn((double)__ldcg(a + 1 + k), W), 0.5));
-          rgb |= (uint32_t)fmin(fmax(m, 0.0), 255.0) << (8 * k);
-        }
-        L.vox[nd.vbase + r].y = rgb;
-        continue;
-      }
-      const uint32_t key = L.vox[nd.vbase + r].x;
-      const uint32_t X = key >> 14, Y = (key >> 7) & 127, Z = key & 127;
-      const int o = (int)((X >> 6) | ((Y >> 6) << 1) | ((Z >> 6) << 2));
-      const int32_t cs = nd.cslot[o];
-      uint64_t sr = 0, sg = 0, sb = 0, n = 0;
-      uint32_t best = 0, best_rgb = 0;
-      bool have = false;
-      if (cs >= 0) {
-        // gather the child's 2x2x2 block: each (cx, cy) row holds both z cells in one word
-        const uint32_t* cb = bits_of(L, cpar, (uint32_t)cs);
-        const uint32_t* cp = pre_of(L, cpar, (uint32_t)cs);
-        const VoxNode& ci = L.cinfo[cs];
-        const uint32_t cx0 = (X & 63) << 1, cy0 = (Y & 63) << 1, cz0 = (Z & 63) << 1;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t ck = ((cx0 + (q & 1)) << 14) | ((cy0 + (q >> 1)) << 7) | cz0;
-          const uint32_t w = ck >> 5, b = ck & 31;
-          const uint32_t bw = __ldcg(cb + w);
-          const uint32_t two = (bw >> b) & 3u;
-          if (!two) continue;
-          uint32_t cr = __ldcg(cp + w) + __popc(bw & ((1u << b) - 1));
-#pragma unroll
-          for (int dz = 0; dz < 2; ++dz) {
-            if (!((two >> dz) & 1)) continue;
-            const uint32_t rgb = __ldcg(&L.vox[ci.vbase + cr].y);
-            if (L.mode == LOD_MODE_AVERAGE) {
-              sr += rgb & 0xFF, sg += (rgb >> 8) & 0xFF, sb += (rgb >> 16) & 0xFF, ++n;
-            } else if (L.mode == LOD_MODE_RANDOM) {
-              uint32_t e = rand_enc(nd.hash, nd.cbase[o] + cr);
-              if (!have || e > best) best = e, best_rgb = rgb, have = true;
-            } else {  // first-come: ordinal = octant base + the child's stored position
-              const uint32_t ord = nd.cbase[o] + __ldcg(L.vpos + ci.vbase + cr);
-              if (!have || ord < best) best = ord, best_rgb = rgb, have = true;
-            }
-            ++cr;
-          }
-        }
-      }
-      if (L.mode == LOD_MODE_AVERAGE) {
-        if (L.exact_sums) {
-          const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(L.acc) + acc0 + r);
-          sr += a.x & 0xFFFFFFFFull, sg += a.x >> 32, sb += a.y & 0xFFFFFFFFull, n += a.y >> 32;
-        } else {
-          const float4 a = __ldcg(reinterpret_cast<const float4*>(L.acc) + acc0 + r);
-          if (fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)) >= 16777216.0f) raise_err(L.st, ERR_F32_SUMS, nd.node);
-          sr += (uint64_t)a.x, sg += (uint64_t)a.y, sb += (uint64_t)a.z, n += (uint64_t)a.w;
-        }
-        L.vox[nd.vbase + r].y = mean_round(sr, n) | (mean_round(sg, n) << 8) | (mean_round(sb, n) << 16);
-      } else if (L.mode == LOD_MODE_RANDOM) {
-        const uint32_t e = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
-        // the winner is a leaf point: its ordinal names (child, index) directly
-        if (!have || e > best) best_rgb = leaf_winner_rgb(L, nd, e & 0xFFFFFu);
-        L.vox[nd.vbase + r].y = best_rgb;
-      } else {
-        uint32_t* a = reinterpret_cast<uint32_t*>(L.acc) + acc0 + r;
-        const uint32_t e = __ldcg(a);
-        if (e != 0 && (!have || ~e < best)) best = ~e, best_rgb = leaf_winner_rgb(L, nd, ~e);
-        L.vox[nd.vbase + r].y = best_rgb;
-        *a = best;  // winning ordinal, ranked by K5
-      }
-    }
+    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) finalize_voxel(L, nd, acc0, __ldcg(&L.vox[nd.vbase + r].x), r);
   }
 }
 
@@ -798,7 +829,7 @@ int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStre
     k_occupy<LOD_POINTS_F64><<<sms * 2, kRT, 0, s>>>(L);
   k_block_sums<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
   k_alloc<<<1, 1024, 0, s>>>(L);
-  k_prefix_emit<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
+  k_prefix<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);

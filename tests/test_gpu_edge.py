@@ -51,3 +51,23 @@ def test_average_sum_overflow_falls_back_to_exact():
 def test_oversized_duplicates_all_strategies(strategy):
     pos, col = _cloud(3_000, 20_000, seed=1)
     _compare(pos, col, 500, strategy, seed=4)
+
+
+def test_distribute_two_pass_leaf_id_path():
+    """> 2^19 leaves: the 2nd radix digit no longer fits the f32 record pad, so the
+    distribute carries leaf ids in a separate array (distribute.cu OUT_LEAF)."""
+    from paper_2302_14801_b200 import BuildConfig, PointCloud, partition
+    rng = np.random.default_rng(11)
+    pos = rng.random((2_500_000, 3)).astype(np.float32).astype(np.float64)
+    col = rng.integers(0, 256, (len(pos), 3)).astype(np.uint8)
+    tree = partition(PointCloud(pos, col), BuildConfig(T=3))
+    info = tree.device_tree.info()
+    assert info.n_leaves > (1 << 19) and info.radix_passes == 2
+    sp = O.split(pos, T=3)
+    got = {nd.path: nd for nd in tree.leaves()}
+    exp = {p: nd for p, nd in sp.nodes.items() if nd.kind == "leaf"}
+    assert set(got) == set(exp)
+    rng2 = np.random.default_rng(0)
+    for path in rng2.choice(len(exp), 2000, replace=False):
+        p = list(exp)[path]
+        assert np.array_equal(got[p].point_positions, pos[exp[p].idx]), p
