@@ -92,6 +92,11 @@ struct Rec<LOD_POINTS_F32> {
   __device__ __forceinline__ static Raw load_cg(const void* base, uint64_t i) {
     return Raw{__ldcg(reinterpret_cast<const uint4*>(base) + i)};
   }
+  // streaming (evict-first): for the last read of a record stream, so the L2 keeps the
+  // lookup tables / counting grids / partially written output lines instead
+  __device__ __forceinline__ static Raw load_cs(const void* base, uint64_t i) {
+    return Raw{__ldcs(reinterpret_cast<const uint4*>(base) + i)};
+  }
   __device__ __forceinline__ static void store(void* base, uint64_t i, const Raw& r) {
     reinterpret_cast<uint4*>(base)[i] = r.a;
   }
@@ -119,6 +124,10 @@ struct Rec<LOD_POINTS_F64> {
   __device__ __forceinline__ static Raw load_cg(const void* base, uint64_t i) {
     const uint4* p = reinterpret_cast<const uint4*>(base) + 2 * i;
     return Raw{__ldcg(p), __ldcg(p + 1)};
+  }
+  __device__ __forceinline__ static Raw load_cs(const void* base, uint64_t i) {
+    const uint4* p = reinterpret_cast<const uint4*>(base) + 2 * i;
+    return Raw{__ldcs(p), __ldcs(p + 1)};
   }
   __device__ __forceinline__ static void store(void* base, uint64_t i, const Raw& r) {
     uint4* p = reinterpret_cast<uint4*>(base) + 2 * i;

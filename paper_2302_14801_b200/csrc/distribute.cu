@@ -73,7 +73,7 @@ __device__ __forceinline__ void load_items(const SplitView& v, const void* in_re
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t i = base + (uint64_t)k * 32 + lane;
-      leaf[k] = Rec<FMT>::tag(Rec<FMT>::load(in_rec, i < last ? i : last));
+      leaf[k] = Rec<FMT>::tag(Rec<FMT>::load(in_rec, i < last ? i : last));  // re-read at the store
     }
   } else {
 #pragma unroll

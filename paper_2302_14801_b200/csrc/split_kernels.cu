@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds_f32(const void* pts, uint64
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
     uint4 r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = __ldg(p + min(i0 + u * stride, n - 1));
+    for (int u = 0; u < U; ++u) r[u] = __ldcs(p + min(i0 + u * stride, n - 1));
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t w[3] = {r[u].x, r[u].y, r[u].z};
@@ -284,48 +284,69 @@ int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_
   return 1;
 }
 
-template <int FMT>
+// Count one point into the extension grids of this round (if it reaches one).
+__device__ __forceinline__ void ext_count_point(const SplitView& v, const Cell16& c, int32_t t, uint32_t round_first,
+                                                bool live) {
+  uint64_t slot = ~0ull;
+  uint32_t e, rr;
+  if (live && ext_descend(v, c, e, rr, t) && e >= round_first) {
+    const ExtMeta& m = v.meta[e];
+    slot = m.pyr_off + level_off(m.ext) + rr;
+  }
+  // dense clusters put whole warps into one cell: aggregate
+  const unsigned act = __ballot_sync(0xFFFFFFFFu, slot != ~0ull);
+  if (slot != ~0ull) {
+    const unsigned peers = __match_any_sync(act, slot);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(v.pyr + slot, (uint32_t)__popc(peers));
+  }
+}
+
+// Every extension round scans all points, four per thread per trip so the key -> target
+// loads stay in flight.  Points inside an extension grid (target <= -2) need their depth-16
+// cell: the first round projects the record once and keeps it (pc16) for the later rounds
+// and the distribute.  (Listing those points for the later rounds cost more in the
+// single-counter append than the full scan it saved.)
+template <int FMT, bool FIRST>
 __global__ void __launch_bounds__(kThreads) k_ext_count(SplitView v, uint32_t round_first) {
   const DevState st = *v.st;
-  const int lane = threadIdx.x & 31;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int U = 4;
   bool bad = false;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < v.n; base += stride) {
-    uint64_t i = base + threadIdx.x;
-    uint64_t slot = ~0ull;
-    // only points inside an extension grid (target <= -2) need their depth-16 cell: the
-    // first round projects the record once and keeps it (pc16) for the later rounds and
-    // the distribute
-    const int32_t t = i < v.n ? __ldg(v.t8 + __ldg(v.pkey + i)) : -1;
-    if (t <= -2) {
-      Cell16 c;
-      if (round_first == 0) {
-        auto r = Rec<FMT>::load(v.pts, i);
-        c = cell16<FMT>(r, st, bad);
-        v.pc16[i] = (uint64_t)c.x | ((uint64_t)c.y << 16) | ((uint64_t)c.z << 32);
-      } else {
-        c = unpack_c16(__ldg(v.pc16 + i));
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < v.n; i0 += U * stride) {
+    uint32_t key[U];
+    int32_t t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) key[u] = __ldg(v.pkey + min(i0 + u * stride, v.n - 1));
+#pragma unroll
+    for (int u = 0; u < U; ++u) t[u] = __ldg(v.t8 + key[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      const bool ext = i < v.n && t[u] <= -2;
+      Cell16 c{0, 0, 0};
+      if (ext) {
+        if (FIRST) {
+          c = cell16<FMT>(Rec<FMT>::load(v.pts, i), st, bad);
+          v.pc16[i] = (uint64_t)c.x | ((uint64_t)c.y << 16) | ((uint64_t)c.z << 32);
+        } else {
+          c = unpack_c16(__ldg(v.pc16 + i));
+        }
       }
-      uint32_t e, rr;
-      if (ext_descend(v, c, e, rr, t) && e >= round_first) {
-        const ExtMeta& m = v.meta[e];
-        slot = m.pyr_off + level_off(m.ext) + rr;
-      }
-    }
-    unsigned act = __ballot_sync(0xFFFFFFFFu, slot != ~0ull);
-    if (slot != ~0ull) {
-      unsigned peers = __match_any_sync(act, slot);
-      if (lane == __ffs(peers) - 1) atomicAdd(v.pyr + slot, (uint32_t)__popc(peers));
+      ext_count_point(v, c, t[u], round_first, ext);
     }
   }
 }
 
 int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStream_t s) {
   uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
-  if (fmt == LOD_POINTS_F32)
-    k_ext_count<LOD_POINTS_F32><<<blocks, kThreads, 0, s>>>(v, round_first);
-  else
-    k_ext_count<LOD_POINTS_F64><<<blocks, kThreads, 0, s>>>(v, round_first);
+  const bool first = round_first == 0;
+  if (fmt == LOD_POINTS_F32) {
+    if (first) k_ext_count<LOD_POINTS_F32, true><<<blocks, kThreads, 0, s>>>(v, round_first);
+    else k_ext_count<LOD_POINTS_F32, false><<<blocks, kThreads, 0, s>>>(v, round_first);
+  } else {
+    if (first) k_ext_count<LOD_POINTS_F64, true><<<blocks, kThreads, 0, s>>>(v, round_first);
+    else k_ext_count<LOD_POINTS_F64, false><<<blocks, kThreads, 0, s>>>(v, round_first);
+  }
   return 1;
 }
 

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
       for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kRT) {
         typename Rec<FMT>::Raw r[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) r[u] = Rec<FMT>::load(L.leaf_pts, first + min(j0 + u * kRT, ch.w - 1));
+        for (int u = 0; u < U; ++u) r[u] = Rec<FMT>::load_cs(L.leaf_pts, first + min(j0 + u * kRT, ch.w - 1));
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t j = j0 + u * kRT;
