@@ -142,6 +142,18 @@ def make_input_device(torch, kind, n, seed, start=0):
     return buf
 
 
+def measured_traffic(config, mode, n, stage):
+    """DRAM bytes (read + write) per build of `stage`'s kernels, from the committed ncu launch
+    list of this config (profiles/traffic.json, scripts/traffic.py); None if not profiled."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t[f"{config}:{mode}"]
+        return e["stages"][stage] if e["points"] == n else None
+    except Exception:
+        return None
+
+
 def cpu_reference_rate(kind, seed, sample, mode, steps=1):
     """The reference algorithm on the host (oracle port, numpy, 1 core): points/s on a sample."""
     from oracle import lod_oracle as O
@@ -236,25 +248,26 @@ def main():
     info = dev.info()
     launches_per_step = dev.launches()
 
-    # stage breakdown (one extra instrumented build, outside the timed region)
-    dev.set_timing(True)
-    step()
-    torch.cuda.synchronize()
-    stages = dev.stage_ms()
-    dev.set_timing(False)
-
     # ---- timed region: K builds, inputs resident in HBM ----
+    # Per-stage CUDA events (recorded by the library on the build's stream between its
+    # stages) are read after every step, so the stage times -- and the roofline below --
+    # are averages over exactly the timed builds.
+    dev.set_timing(True)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    stage_sum = [0.0] * 5
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             step()
+            stage_sum = [a + b for a, b in zip(stage_sum, dev.stage_ms())]
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
+    stages = [x / args.steps for x in stage_sum]
+    dev.set_timing(False)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -301,16 +314,26 @@ def main():
                "d2h_bytes_per_step": rec_bytes + vox_bytes + 88 * info.n_nodes, "ms_per_step": ems}
 
     # ---- roofline of the dominant stage (algorithmic bytes) ----
+    # bounds 16N + count 16N, extension 16E, distribute 32N (read + write each record),
+    # voxelize 16N (leaf points) + 12V (each voxel written and read once as a 6-B record);
+    # the skeleton (merge / nodes / targets) is N-independent and has no per-point bytes.
     peak, peak_kind = hbm_peak()
     V = info.n_voxels
     stage_names = ["bounds+count", "extension", "merge+nodes+targets", "distribute", "voxelize"]
-    stage_bytes = [32 * n, 16 * n if info.n_ext_grids else 0, 0,
-                   (32 if info.radix_passes <= 1 else 72) * n, 16 * n + 16 * V]
+    stage_kernels = ["k_bounds_f32, k_count", "k_ext_count", "k_merge, compactions, k_target_*",
+                     "k_dist_hist, k_dist_scan_*, k_dist_scatter",
+                     "per level: k_setup, k_occupy, k_block_sums, k_alloc, k_prefix, k_scatter, k_finalize"]
+    stage_bytes = [32 * n, 16 * n if info.n_ext_grids else 0, 0, 32 * n, 16 * n + 12 * V]
     dom = max(range(5), key=lambda i: stages[i] if stage_bytes[i] else -1)
     achieved = stage_bytes[dom] / (stages[dom] / 1000.0) / 1e9
     whole_bytes = 80 * n + 12 * V
+    traffic = measured_traffic(args.config, args.mode, n, stage_names[dom])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": stage_names[dom], "peak_source": peak_kind,
+                "traffic": traffic, "kernel": f"{stage_names[dom]} stage ({stage_kernels[dom]})",
+                "algorithmic_bytes": stage_bytes[dom], "ms_per_build": stages[dom], "peak_source": peak_kind,
+                "stages": {nm: {"ms": st, "algorithmic_bytes": b,
+                                "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st > 0 else None}
+                           for nm, st, b in zip(stage_names, stages, stage_bytes)},
                 "whole_build": {"algorithmic_bytes": whole_bytes,
                                 "achieved_gbs": whole_bytes / (ms / 1000.0) / 1e9,
                                 "frac": whole_bytes / (ms / 1000.0) / 1e9 / peak}}
