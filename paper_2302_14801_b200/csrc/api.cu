@@ -89,8 +89,8 @@ struct lod_tree {
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
   DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
   DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
-  DevBuf leaf_pts, status, digit_base, ticket, tmp_rec, tmp_leaf, pkey, pc16;
-  DevBuf vox, scratch, export_buf, stash;
+  DevBuf leaf_pts, status, digit_base, tmp_rec, tmp_leaf, pkey, pc16;
+  DevBuf vox, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vleaf_chunks, vvchunks;
   DevBuf vpos, vout, obits, opre;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
   DevState* host_state = nullptr;  // pinned mirror
@@ -869,7 +869,7 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid, &t->n_lvl,
                    &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node, &t->leaf_first, &t->leaf_count,
                    &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
-                   &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->scratch, &t->export_buf,
+                   &t->digit_base, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
                    &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
                    &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
@@ -1033,8 +1033,8 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->slots, &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid,
                          &t->n_lvl, &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node,
                          &t->leaf_first, &t->leaf_count, &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists,
-                         &t->leaf_pts, &t->status, &t->digit_base, &t->ticket, &t->tmp_rec, &t->tmp_leaf,
-                         &t->vox, &t->scratch, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
+                         &t->leaf_pts, &t->status, &t->digit_base, &t->tmp_rec, &t->tmp_leaf,
+                         &t->vox, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
                          &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
                    &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
