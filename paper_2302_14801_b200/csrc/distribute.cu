@@ -199,9 +199,9 @@ constexpr uint32_t kScanSegs = 512;
 int launch_dist_scan(uint32_t* counts, uint32_t rows, int B, const uint64_t* digit_base, uint32_t* part,
                      cudaStream_t s) {
   const uint32_t dcols = ceil_div_u32(B, 32);
-  const uint32_t seg_rows = std::max<uint32_t>(64, ceil_div_u32(rows, kScanSegs));
+  const uint32_t seg_rows = std::max<uint32_t>(768, ceil_div_u32(rows, kScanSegs));  // ~24 rows per warp
   const uint32_t segs = ceil_div_u32(rows, seg_rows);
-  if (segs <= 1) {
+  if (segs <= 1 || rows <= 16384) {  // small: one pass per 32-digit column is faster
     k_dist_scan_apply<<<dim3(dcols, 1), 1024, 0, s>>>(counts, rows, rows, B, nullptr, digit_base);
     return 1;
   }

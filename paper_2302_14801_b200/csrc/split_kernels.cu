@@ -358,40 +358,53 @@ __global__ void k_mark_anchors(SplitView v) {
   if (e < v.n_ext) v.pyr[v.meta[e].anchor_slot] = UNMERGEABLE;
 }
 
+// One parent cell (pyramid p, cell c of level lp): the 2x2x2 merge rule.
+__device__ __forceinline__ void merge_cell(uint32_t* pyr, uint64_t first, uint64_t stride, int lp, uint32_t T,
+                                         uint64_t p, uint64_t c) {
+  const uint32_t dp = 1u << lp, dc = dp << 1, msk = dp - 1;
+  uint32_t px = (uint32_t)(c >> (2 * lp)), py = (uint32_t)(c >> lp) & msk, pz = (uint32_t)c & msk;
+  uint32_t* base = pyr + first + p * stride;
+  uint32_t* ch = base + level_off(lp + 1);
+  uint64_t sum = 0;
+  bool flag = false;
+  uint64_t at[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint32_t x = 2 * px + (k & 1), y = 2 * py + ((k >> 1) & 1), z = 2 * pz + (k >> 2);
+    at[k] = ((uint64_t)x * dc + y) * dc + z;
+    uint32_t val = ch[at[k]];
+    if (val == UNMERGEABLE)
+      flag = true;
+    else
+      sum += val;
+  }
+  uint32_t parent;
+  if (!flag && sum > 0 && sum < T) {
+    parent = (uint32_t)sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ch[at[k]] = 0;
+  } else {
+    parent = (flag || sum > 0) ? UNMERGEABLE : 0u;
+  }
+  base[level_off(lp) + c] = parent;
+}
+
 // One parent level `lp` of `n_pyr` equally shaped pyramids starting at `first`, stride `stride`.
 __global__ void __launch_bounds__(kThreads) k_merge(uint32_t* pyr, uint64_t first, uint64_t stride, uint32_t n_pyr,
                                                      int lp, uint32_t T) {
   const uint64_t cells = 1ull << (3 * lp);
   const uint64_t total = cells * n_pyr;
-  const uint32_t dp = 1u << lp, dc = dp << 1, msk = dp - 1;
   for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t p = idx / cells, c = idx % cells;
-    uint32_t px = (uint32_t)(c >> (2 * lp)), py = (uint32_t)(c >> lp) & msk, pz = (uint32_t)c & msk;
-    uint32_t* base = pyr + first + p * stride;
-    uint32_t* ch = base + level_off(lp + 1);
-    uint64_t sum = 0;
-    bool flag = false;
-    uint64_t at[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      uint32_t x = 2 * px + (k & 1), y = 2 * py + ((k >> 1) & 1), z = 2 * pz + (k >> 2);
-      at[k] = ((uint64_t)x * dc + y) * dc + z;
-      uint32_t val = ch[at[k]];
-      if (val == UNMERGEABLE)
-        flag = true;
-      else
-        sum += val;
-    }
-    uint32_t parent;
-    if (!flag && sum > 0 && sum < T) {
-      parent = (uint32_t)sum;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) ch[at[k]] = 0;
-    } else {
-      parent = (flag || sum > 0) ? UNMERGEABLE : 0u;
-    }
-    base[level_off(lp) + c] = parent;
+       idx += (uint64_t)gridDim.x * blockDim.x)
+    merge_cell(pyr, first, stride, lp, T, idx / cells, idx % cells);
+}
+
+// The main pyramid's small levels top..0 in one block (barriers between levels): they are
+// a few thousand cells, where separate launches cost more than the work.
+__global__ void __launch_bounds__(1024) k_merge_small(uint32_t* pyr, int top, uint32_t T) {
+  for (int lp = top; lp >= 0; --lp) {
+    for (uint64_t c = threadIdx.x; c < (1ull << (3 * lp)); c += blockDim.x) merge_cell(pyr, 0, 0, lp, T, 0, c);
+    __syncthreads();
   }
 }
 
@@ -429,8 +442,13 @@ int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint
     k_ext_roots<<<ceil_div_u32(v.n_ext, kThreads), kThreads, 0, s>>>(v);
     ++launches;
   }
-  for (int lp = v.D - 1; lp >= 0; --lp) {
+  const int small = std::min(v.D - 1, 4);
+  for (int lp = v.D - 1; lp > small; --lp) {
     k_merge<<<merge_blocks(1ull << (3 * lp)), kThreads, 0, s>>>(v.pyr, 0, 0, 1, lp, v.T);
+    ++launches;
+  }
+  if (small >= 0) {
+    k_merge_small<<<1, 1024, 0, s>>>(v.pyr, small, v.T);
     ++launches;
   }
   return launches;
@@ -725,7 +743,7 @@ __global__ void __launch_bounds__(kThreads) k_target_ext(SplitView v, uint32_t f
 }
 
 int launch_targets(const SplitView& v, cudaStream_t s) {
-  const int small = std::min(v.D, 3);
+  const int small = std::min(v.D, 3);  // one block for levels 0..3 (a block for 0..5 took 46 us)
   k_target_small<<<1, 1024, 0, s>>>(v, small);
   int launches = 1;
   for (int l = small + 1; l <= v.D; ++l, ++launches)
