@@ -201,7 +201,7 @@ int launch_dist_scan(uint32_t* counts, uint32_t rows, int B, const uint64_t* dig
   const uint32_t dcols = ceil_div_u32(B, 32);
   const uint32_t seg_rows = std::max<uint32_t>(768, ceil_div_u32(rows, kScanSegs));  // ~24 rows per warp
   const uint32_t segs = ceil_div_u32(rows, seg_rows);
-  if (segs <= 1 || rows <= 16384) {  // small: one pass per 32-digit column is faster
+  if (segs <= 1) {
     k_dist_scan_apply<<<dim3(dcols, 1), 1024, 0, s>>>(counts, rows, rows, B, nullptr, digit_base);
     return 1;
   }
