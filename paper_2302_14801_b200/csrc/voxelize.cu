@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
         if (region_word(key, o, lw))
           rank = rpre[lw] + __popc(rbits[lw] & mask);
         else
-          rank = __ldcg(pre + (key >> 5)) + __popc(__ldcg(bits + (key >> 5)) & mask);
+          rank = __ldg(pre + (key >> 5)) + __popc(__ldg(bits + (key >> 5)) & mask);
         const uint64_t a = acc0 + rank;
         const uint32_t rgb = r[u].y;
         if (L.mode == LOD_MODE_AVERAGE && !L.exact_sums) {
@@ -603,21 +603,21 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
     for (int q = 0; q < 4; ++q) {
       const uint32_t ck = ((cx0 + (q & 1)) << 14) | ((cy0 + (q >> 1)) << 7) | cz0;
       const uint32_t w = ck >> 5, b = ck & 31;
-      const uint32_t bw = __ldcg(cb + w);
+      const uint32_t bw = __ldg(cb + w);  // child level: read-only here, neighbours share words (L1)
       const uint32_t two = (bw >> b) & 3u;
       if (!two) continue;
-      uint32_t cr = __ldcg(cp + w) + __popc(bw & ((1u << b) - 1));
+      uint32_t cr = __ldg(cp + w) + __popc(bw & ((1u << b) - 1));
 #pragma unroll
       for (int dz = 0; dz < 2; ++dz) {
         if (!((two >> dz) & 1)) continue;
-        const uint32_t rgb = __ldcg(&L.vox[ci.vbase + cr].y);
+        const uint32_t rgb = __ldg(&L.vox[ci.vbase + cr].y);
         if (L.mode == LOD_MODE_AVERAGE) {
           sr += rgb & 0xFF, sg += (rgb >> 8) & 0xFF, sb += (rgb >> 16) & 0xFF, ++n;
         } else if (L.mode == LOD_MODE_RANDOM) {
           uint32_t e = rand_enc(nd.hash, nd.cbase[o] + cr);
           if (!have || e > best) best = e, best_rgb = rgb, have = true;
         } else {  // first-come: ordinal = octant base + the child's stored position
-          const uint32_t ord = nd.cbase[o] + __ldcg(L.vpos + ci.vbase + cr);
+          const uint32_t ord = nd.cbase[o] + __ldg(L.vpos + ci.vbase + cr);
           if (!have || ord < best) best = ord, best_rgb = rgb, have = true;
         }
         ++cr;
