@@ -276,42 +276,93 @@ def main():
     value = n * world / (ms / 1000.0)
 
     # ---- e2e: host buffers in, whole tree out, through the public C ABI ----
+    # Every step uploads its input from pinned host memory and downloads the whole built
+    # tree (leaf points, voxels, node table).  On one GPU the steps are pipelined two deep
+    # on separate streams -- upload of step k+1 || build of step k || download of step k-1
+    # (PCIe is full duplex; the library's lod_tree_copy_async enqueues the downloads) -- the
+    # way a stream of clouds would be processed.  N > 1 ranks run the steps serially.
     e2e = None
     if not args.no_e2e:
         rec_bytes = n * 16
+        vox_bytes = info.n_voxels * 8
+        node_bytes = info.n_nodes * _abi.node_dtype().itemsize
         h_in = torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True)
         h_in.copy_(d_in.cpu())
-        h_leaf = torch.empty(rec_bytes * (2 if world > 1 else 1), dtype=torch.uint8, pin_memory=True)
-        vox_bytes = info.n_voxels * 8
-        h_vox = torch.empty(max(vox_bytes, 8) * (2 if world > 1 else 1), dtype=torch.uint8, pin_memory=True)
-        h_nodes = np.zeros(info.n_nodes, _abi.node_dtype())
-        d_stage = torch.empty(rec_bytes, dtype=torch.uint8, device="cuda")
         lib = dev.lib
+        if world == 1:
+            trees = [dev, DeviceTree(local)]
+            d_stage = [torch.empty(rec_bytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+            h_leaf = [torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            h_vox = [torch.empty(max(vox_bytes, 8), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            h_nodes = [torch.empty(max(node_bytes, 8), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            up = torch.cuda.Stream()
+            cs = [torch.cuda.Stream(), torch.cuda.Stream()]
+            uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+            built = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def e2e_step():
-            d_stage.copy_(h_in, non_blocking=True)
-            step(d_stage)
-            _abi.check(lib.lod_tree_copy_leaf_points(dev.h, C.c_void_p(h_leaf.data_ptr()), sptr))
-            _abi.check(lib.lod_tree_copy_voxels(dev.h, C.c_void_p(h_vox.data_ptr()), sptr))
-            _abi.check(lib.lod_tree_copy_nodes(dev.h, h_nodes.ctypes.data_as(C.c_void_p), sptr))
+            def run(k_steps):
+                for b in range(2):
+                    built[b].record(cs[b])
+                with torch.cuda.stream(up):
+                    d_stage[0].copy_(h_in, non_blocking=True)
+                    uploaded[0].record(up)
+                for k in range(k_steps):
+                    b = k & 1
+                    if k + 1 < k_steps:  # next input, once the build that last read the buffer is done
+                        up.wait_event(built[1 - b])
+                        with torch.cuda.stream(up):
+                            d_stage[1 - b].copy_(h_in, non_blocking=True)
+                            uploaded[1 - b].record(up)
+                    cs[b].wait_event(uploaded[b])
+                    sp = C.c_void_p(cs[b].cuda_stream)
+                    trees[b].build(d_stage[b], n, _abi.LOD_POINTS_F32, cfg, mode_code, 0, stream=sp)
+                    built[b].record(cs[b])
+                    _abi.check(lib.lod_tree_copy_async(trees[b].h, C.c_void_p(h_leaf[b].data_ptr()),
+                                                       C.c_void_p(h_vox[b].data_ptr()),
+                                                       C.c_void_p(h_nodes[b].data_ptr()), sp))
+                for st in (up, cs[0], cs[1]):
+                    stream.wait_stream(st)
 
-        e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
+            run(2)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            up.wait_stream(stream)
+            run(args.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ems = e0.elapsed_time(e1) / args.steps
+            pipeline = "2-deep on 3 streams: upload k+1 || build k || download k-1"
+        else:
+            h_leaf = torch.empty(rec_bytes * 2, dtype=torch.uint8, pin_memory=True)
+            h_vox = torch.empty(max(vox_bytes, 8) * 2, dtype=torch.uint8, pin_memory=True)
+            h_nodes = np.zeros(info.n_nodes, _abi.node_dtype())
+            d_stage = torch.empty(rec_bytes, dtype=torch.uint8, device="cuda")
+
+            def e2e_step():
+                d_stage.copy_(h_in, non_blocking=True)
+                step(d_stage)
+                _abi.check(lib.lod_tree_copy_leaf_points(dev.h, C.c_void_p(h_leaf.data_ptr()), sptr))
+                _abi.check(lib.lod_tree_copy_voxels(dev.h, C.c_void_p(h_vox.data_ptr()), sptr))
+                _abi.check(lib.lod_tree_copy_nodes(dev.h, h_nodes.ctypes.data_as(C.c_void_p), sptr))
+
             e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / args.steps
-        if world > 1:
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                e2e_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ems = e0.elapsed_time(e1) / args.steps
             t = torch.tensor([ems], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ems = float(t.item())
+            pipeline = "serial per step"
         e2e = {"value": n * world / (ems / 1000.0), "unit": "points/s", "h2d_bytes_per_step": rec_bytes,
-               "d2h_bytes_per_step": rec_bytes + vox_bytes + 88 * info.n_nodes, "ms_per_step": ems}
+               "d2h_bytes_per_step": rec_bytes + vox_bytes + node_bytes, "ms_per_step": ems,
+               "pipeline": pipeline}
 
     # ---- roofline of the dominant stage (algorithmic bytes) ----
     # bounds 16N + count 16N, extension 16E, distribute 32N (read + write each record),

@@ -129,6 +129,13 @@ int lod_tree_copy_nodes(const lod_tree* tree, lod_node* host_nodes, void* stream
 int lod_tree_leaf_points(const lod_tree* tree, const void** d_ptr);
 int lod_tree_voxels(const lod_tree* tree, const void** d_ptr);
 
+/* Enqueue the whole tree's device->host copies on `stream` without waiting: leaf points,
+ * voxels (stored order) and node table, each skipped when its pointer is NULL.  Host
+ * buffers should be pinned; synchronize the stream before reading them.  Lets a caller
+ * overlap the copies of build k with the upload / build of build k+1 (PCIe is duplex). */
+int lod_tree_copy_async(const lod_tree* tree, void* h_leaf_points, void* h_voxels, lod_node* h_nodes,
+                        void* stream);
+
 /* Host copies of the outputs (sizes from lod_tree_get_info). */
 int lod_tree_copy_leaf_points(const lod_tree* tree, void* host, void* stream);
 int lod_tree_copy_voxels(const lod_tree* tree, void* host, void* stream);

@@ -916,6 +916,8 @@ int lod_tree_get_info(const lod_tree* t, lod_tree_info* o) {
   return LOD_OK;
 }
 
+static const void* stored_voxels(const lod_tree* t);
+
 int lod_tree_copy_nodes(const lod_tree* tc, lod_node* host, void* stream) {
   lod_tree* t = const_cast<lod_tree*>(tc);
   if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
@@ -926,6 +928,25 @@ int lod_tree_copy_nodes(const lod_tree* tc, lod_node* host, void* stream) {
   launch_export_nodes(v, t->export_buf.as<lod_node>(), s);
   CK(cudaMemcpyAsync(host, t->export_buf.p, (size_t)t->n_nodes * sizeof(lod_node), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return LOD_OK;
+}
+
+int lod_tree_copy_async(const lod_tree* tc, void* h_leaf, void* h_vox, lod_node* h_nodes, void* stream) {
+  lod_tree* t = const_cast<lod_tree*>(tc);
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
+  if (h_vox && t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(t->device));
+  if (h_nodes) {
+    CK(ensure(t->export_buf, (size_t)t->n_nodes * sizeof(lod_node)));
+    SplitView v = make_view(t, nullptr);
+    launch_export_nodes(v, t->export_buf.as<lod_node>(), s);
+    CK(cudaMemcpyAsync(h_nodes, t->export_buf.p, (size_t)t->n_nodes * sizeof(lod_node), cudaMemcpyDeviceToHost, s));
+  }
+  const size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
+  if (h_leaf && t->n) CK(cudaMemcpyAsync(h_leaf, t->leaf_pts.p, t->n * rec, cudaMemcpyDeviceToHost, s));
+  if (h_vox && t->n_voxels)
+    CK(cudaMemcpyAsync(h_vox, stored_voxels(t), t->n_voxels * 8, cudaMemcpyDeviceToHost, s));
   return LOD_OK;
 }
 
