@@ -44,7 +44,7 @@ def parse():
                     choices=["color_filter", "average", "random", "first-come", "weighted"])
     ap.add_argument("--points", type=int, default=0, help="override the config's point count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=500_000)
+    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--stages", action="store_true", help="also print per-stage device times to stderr")

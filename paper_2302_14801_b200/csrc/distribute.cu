@@ -89,7 +89,7 @@ __device__ __forceinline__ void load_items(const SplitView& v, const void* in_re
 // K_hist: per-chunk digit counts
 // ---------------------------------------------------------------------------
 template <int FMT, bool FIRST, bool TAGIN>
-__global__ void __launch_bounds__(kRadixThreads, 2)
+__global__ void __launch_bounds__(kRadixThreads, 3)
     k_dist_hist(SplitView v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_out, int shift, int bits,
                 uint32_t seg_tiles, uint32_t tiles, uint32_t* counts) {
   extern __shared__ __align__(16) uint32_t hist[];
