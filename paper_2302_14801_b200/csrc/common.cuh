@@ -271,6 +271,31 @@ __host__ __device__ __forceinline__ uint32_t ceil_div_u32(uint64_t a, uint64_t b
   return (uint32_t)((a + b - 1) / b);
 }
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: every kernel is launched with programmatic stream
+// serialization and begins with griddepcontrol.wait, so the next grid's launch and block
+// scheduling overlap the previous grid's tail while memory ordering stays exactly that of
+// plain stream order (the wait returns once the preceding grid has completed and flushed).
+// A build is ~75 dependent launches, many of them short.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 #define LOD_CUDA_CHECK(expr)                                  \
   do {                                                        \
     cudaError_t _e = (expr);                                  \

@@ -9,6 +9,7 @@ namespace {
 constexpr int kT = 256;
 
 __global__ void k_local_main(SplitView v, const uint32_t* local_main) {
+  pdl_wait();
   const uint64_t cells = 1ull << (3 * v.D);
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells; c += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t n = local_main[c];
@@ -20,6 +21,7 @@ __global__ void k_local_main(SplitView v, const uint32_t* local_main) {
 
 __global__ void k_local_ext(SplitView v, const uint32_t* local_ext, uint32_t first, uint32_t count, int ext,
                             uint64_t pyr_base, uint64_t main_cells) {
+  pdl_wait();
   const uint64_t cells = 1ull << (3 * ext);
   const uint64_t total = cells * count;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -36,6 +38,7 @@ __global__ void k_local_ext(SplitView v, const uint32_t* local_ext, uint32_t fir
 
 __global__ void k_copy_segments(const uint4* src, uint4* dst, const uint64_t* seg_src, const uint64_t* seg_dst,
                                 const uint32_t* seg_cnt, uint64_t nseg, int vec) {
+  pdl_wait();
   for (uint64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
     const uint64_t a = seg_src[g] * vec, b = seg_dst[g] * vec, n = (uint64_t)seg_cnt[g] * vec;
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[b + i] = __ldg(src + a + i);
@@ -49,13 +52,13 @@ int launch_local_leaf_counts(const SplitView& v, const uint32_t* local_main, con
                              const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s) {
   cudaMemsetAsync(v.leaf_count, 0, (size_t)v.n_leaves * 4, s);
   const uint64_t cells = 1ull << (3 * v.D);
-  k_local_main<<<(uint32_t)std::min<uint64_t>((cells + kT - 1) / kT, 148ull * 16), kT, 0, s>>>(v, local_main);
+  launch_pdl(k_local_main, (uint32_t)std::min<uint64_t>((cells + kT - 1) / kT, 148ull * 16), kT, 0, s, v, local_main);
   int launches = 1;
   const uint64_t main_cells = level_off(v.D + 1);
   for (int r = 0; r < n_rounds; ++r) {
     if (!round_count[r]) continue;
     const uint64_t total = (uint64_t)round_count[r] << (3 * round_ext[r]);
-    k_local_ext<<<(uint32_t)std::min<uint64_t>((total + kT - 1) / kT, 148ull * 16), kT, 0, s>>>(
+    launch_pdl(k_local_ext, (uint32_t)std::min<uint64_t>((total + kT - 1) / kT, 148ull * 16), kT, 0, s, 
         v, local_ext, round_first[r], round_count[r], round_ext[r], round_pyr_base[r], main_cells);
     ++launches;
   }
@@ -66,7 +69,7 @@ int launch_copy_segments(const void* src, void* dst, const uint64_t* seg_src, co
                          const uint32_t* seg_cnt, uint64_t nseg, int rec_bytes, cudaStream_t s) {
   if (!nseg) return 0;
   const uint32_t blocks = (uint32_t)std::min<uint64_t>(nseg, 148ull * 16);
-  k_copy_segments<<<blocks, kT, 0, s>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), seg_src,
+  launch_pdl(k_copy_segments, blocks, kT, 0, s, reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), seg_src,
                                         seg_dst, seg_cnt, nseg, rec_bytes / 16);
   return 1;
 }

@@ -92,6 +92,7 @@ template <int FMT, bool FIRST, bool TAGIN>
 __global__ void __launch_bounds__(kRadixThreads, 3)
     k_dist_hist(SplitView v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_out, int shift, int bits,
                 uint32_t seg_tiles, uint32_t tiles, uint32_t* counts) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t hist[];
   const int B = 1 << bits;
   for (int d = threadIdx.x; d < B; d += kRadixThreads) hist[d] = 0;
@@ -145,6 +146,7 @@ __device__ __forceinline__ void rows_of(uint32_t rows, uint32_t seg_rows, uint32
 
 __global__ void __launch_bounds__(1024) k_dist_scan_part(const uint32_t* counts, uint32_t rows, uint32_t seg_rows,
                                                          int B, uint32_t* part) {
+  pdl_wait();
   __shared__ uint32_t sm[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = blockIdx.x * 32 + lane;
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(1024) k_dist_scan_part(const uint32_t* counts,
 // exclusive prefix of rows [0, rows) of a[g][d], plus base[d] (if any), in place
 __global__ void __launch_bounds__(1024) k_dist_scan_apply(uint32_t* a, uint32_t rows, uint32_t seg_rows, int B,
                                                           const uint32_t* seg_base, const uint64_t* base) {
+  pdl_wait();
   __shared__ uint32_t part[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = blockIdx.x * 32 + lane;
@@ -202,12 +205,12 @@ int launch_dist_scan(uint32_t* counts, uint32_t rows, int B, const uint64_t* dig
   const uint32_t seg_rows = std::max<uint32_t>(768, ceil_div_u32(rows, kScanSegs));  // ~24 rows per warp
   const uint32_t segs = ceil_div_u32(rows, seg_rows);
   if (segs <= 1) {
-    k_dist_scan_apply<<<dim3(dcols, 1), 1024, 0, s>>>(counts, rows, rows, B, nullptr, digit_base);
+    launch_pdl(k_dist_scan_apply, dim3(dcols, 1), 1024, 0, s, counts, rows, rows, B, nullptr, digit_base);
     return 1;
   }
-  k_dist_scan_part<<<dim3(dcols, segs), 1024, 0, s>>>(counts, rows, seg_rows, B, part);
-  k_dist_scan_apply<<<dim3(dcols, 1), 1024, 0, s>>>(part, segs, segs, B, nullptr, digit_base);
-  k_dist_scan_apply<<<dim3(dcols, segs), 1024, 0, s>>>(counts, rows, seg_rows, B, part, nullptr);
+  launch_pdl(k_dist_scan_part, dim3(dcols, segs), 1024, 0, s, counts, rows, seg_rows, B, part);
+  launch_pdl(k_dist_scan_apply, dim3(dcols, 1), 1024, 0, s, part, segs, segs, B, nullptr, digit_base);
+  launch_pdl(k_dist_scan_apply, dim3(dcols, segs), 1024, 0, s, counts, rows, seg_rows, B, part, nullptr);
   return 3;
 }
 
@@ -221,6 +224,7 @@ template <int FMT, bool TAGIN, int OUT>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_dist_scatter(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, uint32_t* out_leaf,
                    int shift, int bits, int tag_shift, uint32_t seg_tiles, uint32_t tiles, const uint32_t* firsts) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t smem[];
   const int B = 1 << bits;
   uint32_t* run = reinterpret_cast<uint32_t*>(smem);               // [B] first slot of the sub-tile
@@ -301,12 +305,14 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
 // Global exclusive prefix per digit, from the leaf counts (leaf ids are the sort keys).
 __global__ void k_digit_hist(const uint32_t* leaf_count, uint32_t n_leaves, int shift, int bits,
                              unsigned long long* hist) {
+  pdl_wait();
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_leaves) return;
   atomicAdd(hist + ((j >> shift) & ((1u << bits) - 1)), (unsigned long long)leaf_count[j]);
 }
 
 __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
+  pdl_wait();
   __shared__ uint64_t sm[1024 / 32 + 1];
   uint64_t a = (2 * threadIdx.x < (unsigned)B) ? hist[2 * threadIdx.x] : 0;
   uint64_t b = (2 * threadIdx.x + 1 < (unsigned)B) ? hist[2 * threadIdx.x + 1] : 0;
@@ -335,9 +341,9 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
     configured = true;
   }
   const uint32_t* leaf_in = FIRST ? leaf_tmp : in_leaf;
-  hist<<<p.segs, kRadixThreads, hsm, s>>>(v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
+  launch_pdl(hist, p.segs, kRadixThreads, hsm, s, v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
   const int nscan = launch_dist_scan(p.counts, p.segs, B, digit_base, p.scan_part, s);
-  scat<<<p.segs, kRadixThreads, ssm, s>>>(v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,
+  launch_pdl(scat, p.segs, kRadixThreads, ssm, s, v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,
                                           p.seg_tiles, p.tiles, p.counts);
   return 2 + nscan;
 }
@@ -351,16 +357,16 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
   uint64_t* base1 = p.digit_base + B0;
   cudaMemsetAsync(p.digit_base, 0, (size_t)(B0 + B1) * 8, s);
   uint32_t lb = ceil_div_u32(v.n_leaves, 256);
-  k_digit_hist<<<lb, 256, 0, s>>>(v.leaf_count, v.n_leaves, 0, p.bits[0],
+  launch_pdl(k_digit_hist, lb, 256, 0, s, v.leaf_count, v.n_leaves, 0, p.bits[0],
                                   reinterpret_cast<unsigned long long*>(base0));
-  k_digit_scan<<<1, 1024, 0, s>>>(base0, B0);
+  launch_pdl(k_digit_scan, 1, 1024, 0, s, base0, B0);
   launches += 2;
   if (p.passes == 1)
     return launches + run_pass<FMT, true, false, OUT_FINAL>(v, v.pts, nullptr, p.tmp_leaf, leaf_out, nullptr, 0,
                                                            p.bits[0], 0, base0, p, s);
-  k_digit_hist<<<lb, 256, 0, s>>>(v.leaf_count, v.n_leaves, p.bits[0], p.bits[1],
+  launch_pdl(k_digit_hist, lb, 256, 0, s, v.leaf_count, v.n_leaves, p.bits[0], p.bits[1],
                                   reinterpret_cast<unsigned long long*>(base1));
-  k_digit_scan<<<1, 1024, 0, s>>>(base1, B1);
+  launch_pdl(k_digit_scan, 1, 1024, 0, s, base1, B1);
   launches += 2;
   if (p.bits[1] <= Rec<FMT>::kTagBits) {
     // the 2nd digit rides in the record pad: no scattered 4-B leaf-id stream (its partial

@@ -17,6 +17,7 @@ template <int FMT>
 __global__ void __launch_bounds__(256) k_encode(SplitView v, const void* leaf_pts, const uint2* vox,
                                                 const int32_t* order, const uint64_t* offs, uint32_t n,
                                                 uint8_t* out) {
+  pdl_wait();
   for (uint32_t q = blockIdx.x; q < n; q += gridDim.x) {
     const int32_t node = order[q];
     const uint64_t off = offs[q];
@@ -66,9 +67,9 @@ int launch_encode(int fmt, const SplitView& v, const void* leaf_pts, const uint2
   if (!n) return 0;
   const uint32_t grid = std::min<uint32_t>(n, 148u * 16);
   if (fmt == LOD_POINTS_F32)
-    k_encode<LOD_POINTS_F32><<<grid, 256, 0, s>>>(v, leaf_pts, vox, order, offs, n, out);
+    launch_pdl(k_encode<LOD_POINTS_F32>, grid, 256, 0, s, v, leaf_pts, vox, order, offs, n, out);
   else
-    k_encode<LOD_POINTS_F64><<<grid, 256, 0, s>>>(v, leaf_pts, vox, order, offs, n, out);
+    launch_pdl(k_encode<LOD_POINTS_F64>, grid, 256, 0, s, v, leaf_pts, vox, order, offs, n, out);
   return 1;
 }
 

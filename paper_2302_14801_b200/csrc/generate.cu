@@ -84,6 +84,7 @@ __device__ __forceinline__ void terrain_row(uint64_t seed, double x, double y, d
 
 // kind: 0 sphere, 1 terrain, 2 scene, 3 cluster, 4 surface
 __global__ void k_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, uint4* out, const double* table) {
+  pdl_wait();
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = start + t;
     double x, y, z;
@@ -160,7 +161,7 @@ int launch_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, void* o
                     cudaStream_t s) {
   uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
   if (blocks == 0) return 0;
-  k_generate<<<blocks, 256, 0, s>>>(kind, seed, start, n, reinterpret_cast<uint4*>(out), table);
+  launch_pdl(k_generate, blocks, 256, 0, s, kind, seed, start, n, reinterpret_cast<uint4*>(out), table);
   return 1;
 }
 

@@ -23,6 +23,7 @@ __device__ __forceinline__ T ld_unaligned(const uint8_t* p) {
 
 __global__ void k_ingest_las(const uint8_t* raw, uint64_t n, uint32_t reclen, int32_t rgb_off, double sx, double sy,
                              double sz, double ox, double oy, double oz, uint4* out) {
+  pdl_wait();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint8_t* r = raw + i * reclen;
     const double x = __dadd_rn(__dmul_rn((double)ld_unaligned<int32_t>(r), sx), ox);
@@ -73,6 +74,7 @@ struct PlyLayout {
 
 __global__ void k_ingest_ply(const uint8_t* raw, uint64_t n, uint32_t stride, PlyLayout L, int has_rgb, int fmt,
                              uint4* out) {
+  pdl_wait();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint8_t* r = raw + i * stride;
     uint32_t rgb = 0x808080u;
@@ -97,6 +99,7 @@ __global__ void k_ingest_ply(const uint8_t* raw, uint64_t n, uint32_t stride, Pl
 template <int FMT>
 __global__ void __launch_bounds__(256) k_checks(SplitView v, const void* leaf_pts, const uint2* vox, int voxels,
                                                 uint32_t T, int max_depth, uint8_t* flags) {
+  pdl_wait();
   __shared__ int s_bad;
   for (uint32_t k = blockIdx.x; k < v.n_nodes; k += gridDim.x) {
     if (threadIdx.x == 0) s_bad = 0;
@@ -163,7 +166,7 @@ int launch_ingest_las(const void* raw, uint64_t n, uint32_t reclen, int32_t rgb_
                       const double* of, void* out, cudaStream_t s) {
   if (!n) return 0;
   const uint32_t grid = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-  k_ingest_las<<<grid, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(raw), n, reclen, rgb_off, sc[0], sc[1], sc[2],
+  launch_pdl(k_ingest_las, grid, 256, 0, s, reinterpret_cast<const uint8_t*>(raw), n, reclen, rgb_off, sc[0], sc[1], sc[2],
                                     of[0], of[1], of[2], reinterpret_cast<uint4*>(out));
   return 1;
 }
@@ -174,7 +177,7 @@ int launch_ingest_ply(const void* raw, uint64_t n, uint32_t stride, const int32_
   PlyLayout L;
   for (int i = 0; i < 6; ++i) L.type[i] = types[i], L.off[i] = offs[i];
   const uint32_t grid = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-  k_ingest_ply<<<grid, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(raw), n, stride, L, has_rgb, fmt,
+  launch_pdl(k_ingest_ply, grid, 256, 0, s, reinterpret_cast<const uint8_t*>(raw), n, stride, L, has_rgb, fmt,
                                     reinterpret_cast<uint4*>(out));
   return 1;
 }
@@ -183,9 +186,9 @@ int launch_checks(int fmt, const SplitView& v, const void* leaf_pts, const uint2
                   int max_depth, uint8_t* flags, cudaStream_t s) {
   const uint32_t grid = std::min<uint32_t>(v.n_nodes, 148u * 16);
   if (fmt == LOD_POINTS_F32)
-    k_checks<LOD_POINTS_F32><<<grid, 256, 0, s>>>(v, leaf_pts, vox, voxels, T, max_depth, flags);
+    launch_pdl(k_checks<LOD_POINTS_F32>, grid, 256, 0, s, v, leaf_pts, vox, voxels, T, max_depth, flags);
   else
-    k_checks<LOD_POINTS_F64><<<grid, 256, 0, s>>>(v, leaf_pts, vox, voxels, T, max_depth, flags);
+    launch_pdl(k_checks<LOD_POINTS_F64>, grid, 256, 0, s, v, leaf_pts, vox, voxels, T, max_depth, flags);
   return 1;
 }
 

@@ -4,6 +4,7 @@ namespace lod {
 
 __global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* sums, uint32_t nb, const uint64_t* base_in,
                                                     uint64_t* total_out) {
+  pdl_wait();
   __shared__ uint64_t sm[1024 / 32 + 1];
   __shared__ uint64_t carry;
   if (threadIdx.x == 0) carry = base_in ? *base_in : 0;

@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace lod {
 
 constexpr int kScanThreads = 256;
@@ -47,6 +49,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T* total, T* smem /* >= NT/32 
 
 template <class F>
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(uint64_t n, F f, uint64_t* block_sums) {
+  pdl_wait();
   __shared__ uint64_t sm[kScanThreads / 32 + 1];
   uint64_t base = (uint64_t)blockIdx.x * kScanTile;
   uint64_t s = 0;
@@ -67,6 +70,7 @@ __global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* sums, uint32_t nb,
 
 template <class F>
 __global__ void __launch_bounds__(kScanThreads) k_scan_store(uint64_t n, F f, const uint64_t* block_sums) {
+  pdl_wait();
   // 16 coalesced trips of 256 consecutive items; a block-wide scan per trip keeps the order
   __shared__ uint64_t warp_tot[kScanThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -98,6 +102,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_store(uint64_t n, F f, co
 // ---------------------------------------------------------------------------
 template <class F>
 __global__ void __launch_bounds__(kScanThreads) k_compact_count(uint64_t n, F f, uint64_t* block_sums) {
+  pdl_wait();
   __shared__ uint32_t wc[kScanThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)warp * 32 * kScanItems;
@@ -118,6 +123,7 @@ __global__ void __launch_bounds__(kScanThreads) k_compact_count(uint64_t n, F f,
 
 template <class F>
 __global__ void __launch_bounds__(kScanThreads) k_compact_store(uint64_t n, F f, const uint64_t* block_sums) {
+  pdl_wait();
   __shared__ uint32_t wc[kScanThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)warp * 32 * kScanItems;
@@ -155,9 +161,9 @@ int device_scan(uint64_t n, F f, ScanScratch& scr, const uint64_t* base_in, uint
   uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
   if (nb == 0) nb = 1;
   if (scr.cap < nb + 1) return -1;
-  k_scan_reduce<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
-  k_scan_sums<<<1, 1024, 0, st>>>(scr.sums, nb, base_in, total_out);
-  k_scan_store<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
+  launch_pdl(k_scan_reduce<F>, nb, kScanThreads, 0, st, n, f, scr.sums);
+  launch_pdl(k_scan_sums, 1, 1024, 0, st, scr.sums, nb, base_in, total_out);
+  launch_pdl(k_scan_store<F>, nb, kScanThreads, 0, st, n, f, scr.sums);
   return 3;
 }
 
@@ -167,9 +173,9 @@ int device_compact(uint64_t n, F f, ScanScratch& scr, uint64_t* total_out, cudaS
   uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
   if (nb == 0) nb = 1;
   if (scr.cap < nb + 1) return -1;
-  k_compact_count<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
-  k_scan_sums<<<1, 1024, 0, st>>>(scr.sums, nb, nullptr, total_out);
-  k_compact_store<F><<<nb, kScanThreads, 0, st>>>(n, f, scr.sums);
+  launch_pdl(k_compact_count<F>, nb, kScanThreads, 0, st, n, f, scr.sums);
+  launch_pdl(k_scan_sums, 1, 1024, 0, st, scr.sums, nb, nullptr, total_out);
+  launch_pdl(k_compact_store<F>, nb, kScanThreads, 0, st, n, f, scr.sums);
   return 3;
 }
 

@@ -25,6 +25,7 @@ __device__ __forceinline__ int ceil_log2_u64(uint64_t x) { return x <= 1 ? 0 : 6
 // ---------------------------------------------------------------------------
 // float32 records: min / max / finiteness in fp32 (exact; widened once at the end)
 __global__ void __launch_bounds__(kThreads) k_bounds_f32(const void* pts, uint64_t n, DevState* st) {
+  pdl_wait();
   float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   uint32_t expmax = 0;  // non-finite <=> exponent field all ones
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds_f32(const void* pts, uint64
 
 template <int FMT>
 __global__ void __launch_bounds__(kThreads) k_bounds(const void* pts, uint64_t n, DevState* st) {
+  pdl_wait();
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   bool bad = false;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(kThreads) k_bounds(const void* pts, uint64_t n
 
 // size = max_axis(max - min), 1.0 when degenerate (model.py:206-209)
 __global__ void k_bounds_finalize(DevState* st, int user, double ux, double uy, double uz, double us) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   if (user) {
     st->lo[0] = ux, st->lo[1] = uy, st->lo[2] = uz, st->size = us;
@@ -131,15 +134,15 @@ __global__ void k_bounds_finalize(DevState* st, int user, double ux, double uy, 
 
 int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const double* ub, cudaStream_t s) {
   if (ub) {
-    k_bounds_finalize<<<1, 32, 0, s>>>(st, 1, ub[0], ub[1], ub[2], ub[3]);
+    launch_pdl(k_bounds_finalize, 1, 32, 0, s, st, 1, ub[0], ub[1], ub[2], ub[3]);
     return 1;
   }
   uint32_t blocks = (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, 148ull * 8);
   if (fmt == LOD_POINTS_F32)
-    k_bounds_f32<<<blocks, kThreads, 0, s>>>(pts, n, st);
+    launch_pdl(k_bounds_f32, blocks, kThreads, 0, s, pts, n, st);
   else
-    k_bounds<LOD_POINTS_F64><<<blocks, kThreads, 0, s>>>(pts, n, st);
-  k_bounds_finalize<<<1, 32, 0, s>>>(st, 0, 0, 0, 0, 0);
+    launch_pdl(k_bounds<LOD_POINTS_F64>, blocks, kThreads, 0, s, pts, n, st);
+  launch_pdl(k_bounds_finalize, 1, 32, 0, s, st, 0, 0, 0, 0, 0);
   return 2;
 }
 
@@ -150,6 +153,7 @@ constexpr int kCountUnroll = 4;
 
 template <int FMT>
 __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
+  pdl_wait();
   const DevState st = *v.st;
   const Frame32 fr = make_frame32(st.lo[0], st.lo[1], st.lo[2], st.size, v.D);
   const float lim = (float)(1u << v.D);
@@ -197,9 +201,9 @@ __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
 int launch_count(int fmt, const SplitView& v, cudaStream_t s) {
   uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
   if (fmt == LOD_POINTS_F32)
-    k_count<LOD_POINTS_F32><<<blocks, kThreads, 0, s>>>(v);
+    launch_pdl(k_count<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
   else
-    k_count<LOD_POINTS_F64><<<blocks, kThreads, 0, s>>>(v);
+    launch_pdl(k_count<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
   return 1;
 }
 
@@ -243,6 +247,7 @@ int launch_find_subanchors(const SplitView& v, uint32_t first_ext, uint32_t n_ex
 __global__ void k_ext_create(SplitView v, int round, uint32_t first, uint32_t count, const uint64_t* list,
                              uint32_t parent_first, uint64_t pyr_base, uint64_t tgt_base, int base_depth,
                              int ext) {
+  pdl_wait();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   uint32_t e = first + i;
@@ -279,7 +284,7 @@ int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_
                       uint32_t parent_first, uint64_t pyr_base, uint64_t tgt_base, int base_depth,
                       int ext_levels, cudaStream_t s) {
   if (!count) return 0;
-  k_ext_create<<<ceil_div_u32(count, kThreads), kThreads, 0, s>>>(v, round, first_ext, count, list, parent_first,
+  launch_pdl(k_ext_create, ceil_div_u32(count, kThreads), kThreads, 0, s, v, round, first_ext, count, list, parent_first,
                                                                    pyr_base, tgt_base, base_depth, ext_levels);
   return 1;
 }
@@ -308,6 +313,7 @@ __device__ __forceinline__ void ext_count_point(const SplitView& v, const Cell16
 // single-counter append than the full scan it saved.)
 template <int FMT, bool FIRST>
 __global__ void __launch_bounds__(kThreads) k_ext_count(SplitView v, uint32_t round_first) {
+  pdl_wait();
   const DevState st = *v.st;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   constexpr int U = 4;
@@ -341,11 +347,11 @@ int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStre
   uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
   const bool first = round_first == 0;
   if (fmt == LOD_POINTS_F32) {
-    if (first) k_ext_count<LOD_POINTS_F32, true><<<blocks, kThreads, 0, s>>>(v, round_first);
-    else k_ext_count<LOD_POINTS_F32, false><<<blocks, kThreads, 0, s>>>(v, round_first);
+    if (first) launch_pdl(k_ext_count<LOD_POINTS_F32, true>, blocks, kThreads, 0, s, v, round_first);
+    else launch_pdl(k_ext_count<LOD_POINTS_F32, false>, blocks, kThreads, 0, s, v, round_first);
   } else {
-    if (first) k_ext_count<LOD_POINTS_F64, true><<<blocks, kThreads, 0, s>>>(v, round_first);
-    else k_ext_count<LOD_POINTS_F64, false><<<blocks, kThreads, 0, s>>>(v, round_first);
+    if (first) launch_pdl(k_ext_count<LOD_POINTS_F64, true>, blocks, kThreads, 0, s, v, round_first);
+    else launch_pdl(k_ext_count<LOD_POINTS_F64, false>, blocks, kThreads, 0, s, v, round_first);
   }
   return 1;
 }
@@ -354,6 +360,7 @@ int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStre
 // K4: merge (partition.py:36-61 rule; anchors pre-flagged, partition.py:157-159,165-167)
 // ---------------------------------------------------------------------------
 __global__ void k_mark_anchors(SplitView v) {
+  pdl_wait();
   uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < v.n_ext) v.pyr[v.meta[e].anchor_slot] = UNMERGEABLE;
 }
@@ -392,6 +399,7 @@ __device__ __forceinline__ void merge_cell(uint32_t* pyr, uint64_t first, uint64
 // One parent level `lp` of `n_pyr` equally shaped pyramids starting at `first`, stride `stride`.
 __global__ void __launch_bounds__(kThreads) k_merge(uint32_t* pyr, uint64_t first, uint64_t stride, uint32_t n_pyr,
                                                      int lp, uint32_t T) {
+  pdl_wait();
   const uint64_t cells = 1ull << (3 * lp);
   const uint64_t total = cells * n_pyr;
   for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -402,6 +410,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(uint32_t* pyr, uint64_t firs
 // The main pyramid's small levels top..0 in one block (barriers between levels): they are
 // a few thousand cells, where separate launches cost more than the work.
 __global__ void __launch_bounds__(1024) k_merge_small(uint32_t* pyr, int top, uint32_t T) {
+  pdl_wait();
   for (int lp = top; lp >= 0; --lp) {
     for (uint64_t c = threadIdx.x; c < (1ull << (3 * lp)); c += blockDim.x) merge_cell(pyr, 0, 0, lp, T, 0, c);
     __syncthreads();
@@ -411,6 +420,7 @@ __global__ void __launch_bounds__(1024) k_merge_small(uint32_t* pyr, int top, ui
 // Extension roots must come out UNMERGEABLE (partition.py:169-170); the root slot then
 // duplicates the anchor node and is cleared so node enumeration skips it (partition.py:216).
 __global__ void k_ext_roots(SplitView v) {
+  pdl_wait();
   uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= v.n_ext) return;
   uint64_t s = v.meta[e].pyr_off;
@@ -426,29 +436,29 @@ int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint
                      const int* round_ext, const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s) {
   int launches = 0;
   if (v.n_ext) {
-    k_mark_anchors<<<ceil_div_u32(v.n_ext, kThreads), kThreads, 0, s>>>(v);
+    launch_pdl(k_mark_anchors, ceil_div_u32(v.n_ext, kThreads), kThreads, 0, s, v);
     ++launches;
   }
   for (int r = n_rounds - 1; r >= 0; --r) {
     if (!round_count[r]) continue;
     int e = round_ext[r];
     for (int lp = e - 1; lp >= 0; --lp) {
-      k_merge<<<merge_blocks((uint64_t)round_count[r] << (3 * lp)), kThreads, 0, s>>>(
+      launch_pdl(k_merge, merge_blocks((uint64_t)round_count[r] << (3 * lp)), kThreads, 0, s,
           v.pyr, round_pyr_base[r], level_off(e + 1), round_count[r], lp, v.T);
       ++launches;
     }
   }
   if (v.n_ext) {
-    k_ext_roots<<<ceil_div_u32(v.n_ext, kThreads), kThreads, 0, s>>>(v);
+    launch_pdl(k_ext_roots, ceil_div_u32(v.n_ext, kThreads), kThreads, 0, s, v);
     ++launches;
   }
   const int small = std::min(v.D - 1, 4);
   for (int lp = v.D - 1; lp > small; --lp) {
-    k_merge<<<merge_blocks(1ull << (3 * lp)), kThreads, 0, s>>>(v.pyr, 0, 0, 1, lp, v.T);
+    launch_pdl(k_merge, merge_blocks(1ull << (3 * lp)), kThreads, 0, s, v.pyr, 0, 0, 1, lp, v.T);
     ++launches;
   }
   if (small >= 0) {
-    k_merge_small<<<1, 1024, 0, s>>>(v.pyr, small, v.T);
+    launch_pdl(k_merge_small, 1, 1024, 0, s, v.pyr, small, v.T);
     ++launches;
   }
   return launches;
@@ -506,6 +516,7 @@ __device__ __forceinline__ SlotInfo decode_slot(const SplitView& v, uint64_t s) 
 }
 
 __global__ void __launch_bounds__(kThreads) k_build_nodes(SplitView v, const uint64_t* slots) {
+  pdl_wait();
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= v.n_nodes) return;
   uint64_t s = slots[k];
@@ -548,6 +559,7 @@ __global__ void __launch_bounds__(kThreads) k_build_nodes(SplitView v, const uin
 }
 
 __global__ void __launch_bounds__(kThreads) k_link(SplitView v) {
+  pdl_wait();
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= v.n_nodes) return;
   uint64_t cell = v.n_cell[k];
@@ -583,6 +595,7 @@ __global__ void __launch_bounds__(kThreads) k_link(SplitView v) {
 
 // bounds_at(world, path): sequential child_bounds fold (model.py:62-81, hazard H2)
 __global__ void __launch_bounds__(kThreads) k_node_bounds(SplitView v) {
+  pdl_wait();
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= v.n_nodes) return;
   uint64_t cell = v.n_cell[k];
@@ -601,9 +614,9 @@ __global__ void __launch_bounds__(kThreads) k_node_bounds(SplitView v) {
 
 int launch_build_nodes(const SplitView& v, const uint64_t* slots, cudaStream_t s) {
   uint32_t b = ceil_div_u32(v.n_nodes, kThreads);
-  k_build_nodes<<<b, kThreads, 0, s>>>(v, slots);
-  k_link<<<b, kThreads, 0, s>>>(v);
-  k_node_bounds<<<b, kThreads, 0, s>>>(v);
+  launch_pdl(k_build_nodes, b, kThreads, 0, s, v, slots);
+  launch_pdl(k_link, b, kThreads, 0, s, v);
+  launch_pdl(k_node_bounds, b, kThreads, 0, s, v);
   return 3;
 }
 
@@ -645,6 +658,7 @@ struct LeafOffF {
 // Per leaf, the bounds of its parent (the node whose 128^3 grid its points are sampled
 // into, sampling.py:29-38) and RN(1/size) = RN(1/world_size) * 2^depth (exact scaling).
 __global__ void k_leaf_parent_boxes(SplitView v) {
+  pdl_wait();
   uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= v.n_leaves) return;
   int32_t par = v.n_parent[v.leaf_node[j]];
@@ -659,7 +673,7 @@ __global__ void k_leaf_parent_boxes(SplitView v) {
 }
 
 int launch_leaf_parent_boxes(const SplitView& v, cudaStream_t s) {
-  k_leaf_parent_boxes<<<ceil_div_u32(v.n_leaves, kThreads), kThreads, 0, s>>>(v);
+  launch_pdl(k_leaf_parent_boxes, ceil_div_u32(v.n_leaves, kThreads), kThreads, 0, s, v);
   return 1;
 }
 
@@ -704,6 +718,7 @@ __device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t 
 
 // levels 0..top in one block (small levels, block barriers between them)
 __global__ void __launch_bounds__(1024) k_target_small(SplitView v, int top) {
+  pdl_wait();
   for (int l = 0; l <= top; ++l) {
     for (uint64_t c = threadIdx.x; c < (1ull << (3 * l)); c += blockDim.x) target_cell(v, l, c);
     __syncthreads();
@@ -711,6 +726,7 @@ __global__ void __launch_bounds__(1024) k_target_small(SplitView v, int top) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_target_level(SplitView v, int l) {
+  pdl_wait();
   const uint64_t cells = 1ull << (3 * l);
   for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
        c += (uint64_t)gridDim.x * blockDim.x)
@@ -718,6 +734,7 @@ __global__ void __launch_bounds__(kThreads) k_target_level(SplitView v, int l) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_target_ext(SplitView v, uint32_t first, uint32_t count, int ext) {
+  pdl_wait();
   const uint64_t cells = 1ull << (3 * ext);
   const uint64_t total = cells * count;
   const uint32_t msk = (1u << ext) - 1;
@@ -744,20 +761,21 @@ __global__ void __launch_bounds__(kThreads) k_target_ext(SplitView v, uint32_t f
 
 int launch_targets(const SplitView& v, cudaStream_t s) {
   const int small = std::min(v.D, 3);  // one block for levels 0..3 (a block for 0..5 took 46 us)
-  k_target_small<<<1, 1024, 0, s>>>(v, small);
+  launch_pdl(k_target_small, 1, 1024, 0, s, v, small);
   int launches = 1;
   for (int l = small + 1; l <= v.D; ++l, ++launches)
-    k_target_level<<<merge_blocks(1ull << (3 * l)), kThreads, 0, s>>>(v, l);
+    launch_pdl(k_target_level, merge_blocks(1ull << (3 * l)), kThreads, 0, s, v, l);
   return launches;
 }
 
 int launch_targets_ext(const SplitView& v, uint32_t first, uint32_t count, int ext, cudaStream_t s) {
   if (!count) return 0;
-  k_target_ext<<<merge_blocks((uint64_t)count << (3 * ext)), kThreads, 0, s>>>(v, first, count, ext);
+  launch_pdl(k_target_ext, merge_blocks((uint64_t)count << (3 * ext)), kThreads, 0, s, v, first, count, ext);
   return 1;
 }
 
 __global__ void k_depth_hist(SplitView v, uint32_t* depth_count) {
+  pdl_wait();
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= v.n_nodes) return;
   uint64_t cell = v.n_cell[k];
@@ -767,11 +785,12 @@ __global__ void k_depth_hist(SplitView v, uint32_t* depth_count) {
 }
 
 int launch_depth_lists(const SplitView& v, uint32_t* depth_count, cudaStream_t s) {
-  k_depth_hist<<<ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s>>>(v, depth_count);
+  launch_pdl(k_depth_hist, ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s, v, depth_count);
   return 1;
 }
 
 __global__ void k_depth_scatter(SplitView v, const uint32_t* depth_off, uint32_t* cursor, uint32_t* lists) {
+  pdl_wait();
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= v.n_nodes || v.n_val[k] != UNMERGEABLE) return;
   uint32_t depth = (uint32_t)(v.n_cell[k] >> 48) & 0xFF;
@@ -780,11 +799,12 @@ __global__ void k_depth_scatter(SplitView v, const uint32_t* depth_off, uint32_t
 
 int launch_depth_scatter(const SplitView& v, const uint32_t* depth_off, uint32_t* depth_cursor, uint32_t* lists,
                          cudaStream_t s) {
-  k_depth_scatter<<<ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s>>>(v, depth_off, depth_cursor, lists);
+  launch_pdl(k_depth_scatter, ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s, v, depth_off, depth_cursor, lists);
   return 1;
 }
 
 __global__ void k_export_nodes(SplitView v, lod_node* out) {
+  pdl_wait();
   uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= v.n_nodes) return;
   lod_node o;
@@ -802,7 +822,7 @@ __global__ void k_export_nodes(SplitView v, lod_node* out) {
 }
 
 int launch_export_nodes(const SplitView& v, lod_node* out, cudaStream_t s) {
-  k_export_nodes<<<ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s>>>(v, out);
+  launch_pdl(k_export_nodes, ceil_div_u32(v.n_nodes, kThreads), kThreads, 0, s, v, out);
   return 1;
 }
 

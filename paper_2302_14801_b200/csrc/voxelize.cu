@@ -88,6 +88,7 @@ __device__ __forceinline__ uint32_t* pre_of(const VoxLevel& L, int parity, uint3
 // K0: per-node setup; eight lanes per node, one per child octant
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
+  pdl_wait();
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t s = g >> 3;
   const int o = (int)(g & 7);
@@ -182,6 +183,7 @@ __device__ __forceinline__ uint32_t region_to_global(uint32_t lw, int o) {
 
 template <int FMT>
 __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
+  pdl_wait();
   if (L.st->err & ERR_ARENA) return;
   __shared__ uint32_t rb[kRegionWords];
   const uint32_t nch = L.counters[0];
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
 // K2: popcount sums per 4096-word block, node offsets, word prefixes
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kT) k_block_sums(VoxLevel L) {
+  pdl_wait();
   const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
   __shared__ uint32_t red[kT / 32];
   uint32_t c = 0;
@@ -274,6 +277,7 @@ __global__ void __launch_bounds__(kT) k_block_sums(VoxLevel L) {
 
 // one block: per-node voxel counts -> arena offsets (bump pointer), K4 voxel chunks
 __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
+  pdl_wait();
   if (L.st->err & ERR_ARENA) return;
   __shared__ uint64_t sm[1024 / 32 + 1];
   __shared__ uint64_t carry, ocarry;
@@ -352,6 +356,7 @@ __device__ __forceinline__ uint32_t stage_block(const VoxLevel& L, uint32_t s, u
 // voxel keys, and the block's accumulators zeroed -- its voxels are the contiguous rank
 // range [blk_sum, blk_sum + tot), so the zeroing is one coalesced sweep.
 __global__ void __launch_bounds__(kT) k_prefix(VoxLevel L) {
+  pdl_wait();
   const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
   const VoxNode& nd = L.info[s];
   if (nd.skip || L.st->err & ERR_ARENA) return;
@@ -401,6 +406,7 @@ __device__ __forceinline__ uint32_t rank_of(const uint32_t* bits, const uint32_t
 // atomics reach L2.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
+  pdl_wait();
   if (L.st->err & ERR_ARENA) return;
   extern __shared__ __align__(16) uint32_t rsm[];
   uint32_t* rbits = rsm;
@@ -476,6 +482,7 @@ __device__ __forceinline__ double wdist_axis(double g, uint32_t c) {
 }
 
 __global__ void __launch_bounds__(kRT, 2) k_scatter_w(VoxLevel L) {
+  pdl_wait();
   if (L.st->err & ERR_ARENA) return;
   extern __shared__ __align__(16) uint32_t rsm[];
   uint32_t* rbits = rsm;
@@ -652,6 +659,7 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
 // K4: finalize every voxel of the level, one thread per voxel (rank chunks): a word-walk
 // per block serialised each thread's gathers and ran 5x slower (measured).
 __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
+  pdl_wait();
   if (L.st->err & ERR_ARENA) return;
   const uint32_t nch = L.counters[2];
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
@@ -667,6 +675,7 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
 // K5 (first-come): stored order = ascending winning ordinal (sampling.py:64-66)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kT) k_fc_mark(VoxLevel L) {
+  pdl_wait();
   if (L.st->err & ERR_ARENA) return;
   const uint32_t nch = L.counters[2];
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
@@ -689,6 +698,7 @@ struct OrdScanF {  // exclusive popcount prefix over the level's ordinal bitmaps
 };
 
 __global__ void __launch_bounds__(kT) k_fc_pos(VoxLevel L) {
+  pdl_wait();
   if (L.st->err & ERR_ARENA) return;
   const uint32_t nch = L.counters[2];
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
@@ -716,6 +726,7 @@ __global__ void __launch_bounds__(kT) k_fc_pos(VoxLevel L) {
 // gather from them exactly like from locally voxelized children.
 // ---------------------------------------------------------------------------
 __global__ void k_import_setup(VoxLevel L, uint32_t slot_base) {
+  pdl_wait();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.list_n) return;
   const uint32_t node = L.list[i], s = slot_base + i;
@@ -728,6 +739,7 @@ __global__ void k_import_setup(VoxLevel L, uint32_t slot_base) {
 }
 
 __global__ void __launch_bounds__(kT) k_import_bits(VoxLevel L, uint32_t slot_base) {
+  pdl_wait();
   const uint32_t i = blockIdx.x / kBlksPerNode, part = blockIdx.x % kBlksPerNode;
   const VoxNode& nd = L.info[slot_base + i];
   uint32_t* bits = bits_of(L, L.parity, slot_base + i);
@@ -740,6 +752,7 @@ __global__ void __launch_bounds__(kT) k_import_bits(VoxLevel L, uint32_t slot_ba
 }
 
 __global__ void __launch_bounds__(kT) k_import_block_sums(VoxLevel L, uint32_t slot_base) {
+  pdl_wait();
   const uint32_t s = slot_base + blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
   __shared__ uint32_t red[kT / 32];
   const uint4* b = reinterpret_cast<const uint4*>(bits_of(L, L.parity, s) + blk * kBlkWords);
@@ -760,6 +773,7 @@ __global__ void __launch_bounds__(kT) k_import_block_sums(VoxLevel L, uint32_t s
 }
 
 __global__ void k_import_block_prefix(VoxLevel L) {
+  pdl_wait();
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.list_n) return;
   uint32_t run = 0;
@@ -771,6 +785,7 @@ __global__ void k_import_block_prefix(VoxLevel L) {
 }
 
 __global__ void __launch_bounds__(kT) k_import_prefix(VoxLevel L, uint32_t slot_base) {
+  pdl_wait();
   const uint32_t s = slot_base + blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
   __shared__ uint32_t sm[kT / 32 + 1];
   const uint32_t* bits = bits_of(L, L.parity, s) + blk * kBlkWords;
@@ -791,6 +806,7 @@ __global__ void __launch_bounds__(kT) k_import_prefix(VoxLevel L, uint32_t slot_
 // first-come imports arrive in stored order (in vout): put the arena in key order and
 // record each voxel's stored position for the parent's gather
 __global__ void __launch_bounds__(kT) k_import_fc(VoxLevel L, uint32_t slot_base) {
+  pdl_wait();
   const uint32_t i = blockIdx.x / kBlksPerNode, part = blockIdx.x % kBlksPerNode;
   const VoxNode& nd = L.info[slot_base + i];
   const uint32_t* bits = bits_of(L, L.parity, slot_base + i);
@@ -807,13 +823,13 @@ __global__ void __launch_bounds__(kT) k_import_fc(VoxLevel L, uint32_t slot_base
 
 int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s) {
   if (!L.list_n) return 0;
-  k_import_setup<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L, slot_base);
-  k_import_bits<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
-  k_import_block_sums<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
-  k_import_block_prefix<<<ceil_div_u32(L.list_n, kT), kT, 0, s>>>(L);
-  k_import_prefix<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
+  launch_pdl(k_import_setup, ceil_div_u32(L.list_n, kT), kT, 0, s, L, slot_base);
+  launch_pdl(k_import_bits, L.list_n * kBlksPerNode, kT, 0, s, L, slot_base);
+  launch_pdl(k_import_block_sums, L.list_n * kBlksPerNode, kT, 0, s, L, slot_base);
+  launch_pdl(k_import_block_prefix, ceil_div_u32(L.list_n, kT), kT, 0, s, L);
+  launch_pdl(k_import_prefix, L.list_n * kBlksPerNode, kT, 0, s, L, slot_base);
   if (L.mode != LOD_MODE_FIRST_COME) return 5;
-  k_import_fc<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L, slot_base);
+  launch_pdl(k_import_fc, L.list_n * kBlksPerNode, kT, 0, s, L, slot_base);
   return 6;
 }
 
@@ -822,14 +838,14 @@ int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s
 int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s) {
   const int grid = sms * 8;
   int launches = 7;
-  k_setup<<<ceil_div_u32(8ull * L.list_n, kT), kT, 0, s>>>(L);
+  launch_pdl(k_setup, ceil_div_u32(8ull * L.list_n, kT), kT, 0, s, L);
   if (L.fmt == LOD_POINTS_F32)
-    k_occupy<LOD_POINTS_F32><<<sms * 2, kRT, 0, s>>>(L);
+    launch_pdl(k_occupy<LOD_POINTS_F32>, sms * 2, kRT, 0, s, L);
   else
-    k_occupy<LOD_POINTS_F64><<<sms * 2, kRT, 0, s>>>(L);
-  k_block_sums<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
-  k_alloc<<<1, 1024, 0, s>>>(L);
-  k_prefix<<<L.list_n * kBlksPerNode, kT, 0, s>>>(L);
+    launch_pdl(k_occupy<LOD_POINTS_F64>, sms * 2, kRT, 0, s, L);
+  launch_pdl(k_block_sums, L.list_n * kBlksPerNode, kT, 0, s, L);
+  launch_pdl(k_alloc, 1, 1024, 0, s, L);
+  launch_pdl(k_prefix, L.list_n * kBlksPerNode, kT, 0, s, L);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);
@@ -837,16 +853,16 @@ int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStre
     configured = true;
   }
   if (L.mode == LOD_MODE_WEIGHTED)
-    k_scatter_w<<<sms * 2, kRT, 2 * kRegionWords * 4, s>>>(L);
+    launch_pdl(k_scatter_w, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
   else
-    k_scatter<<<sms * 2, kRT, 2 * kRegionWords * 4, s>>>(L);
-  k_finalize<<<grid, kT, 0, s>>>(L);
+    launch_pdl(k_scatter, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
+  launch_pdl(k_finalize, grid, kT, 0, s, L);
   if (L.mode == LOD_MODE_FIRST_COME) {
     cudaMemsetAsync(L.obits, 0, L.ocap * 4, s);
-    k_fc_mark<<<grid, kT, 0, s>>>(L);
+    launch_pdl(k_fc_mark, grid, kT, 0, s, L);
     const int r = device_scan(L.ocap, OrdScanF{L.obits, L.opre}, scr, nullptr, nullptr, s);
     if (r < 0) return r;
-    k_fc_pos<<<grid, kT, 0, s>>>(L);
+    launch_pdl(k_fc_pos, grid, kT, 0, s, L);
     launches += 2 + r;
   }
   return launches;
