@@ -468,7 +468,7 @@ int phase_skeleton(lod_tree* t, cudaStream_t s) {
 
 // Stable distribute of the local points into their leaves (partition.py:244-271).  Uses
 // t->leaf_count (per leaf, this process's points) for the digit bases and offsets.
-int phase_distribute(lod_tree* t, cudaStream_t s) {
+int phase_distribute(lod_tree* t, cudaStream_t s, bool sync = true) {
   const uint64_t n = t->n;
   const size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
   CK(ensure(t->leaf_pts, std::max<uint64_t>(n, 1) * rec));
@@ -503,15 +503,21 @@ int phase_distribute(lod_tree* t, cudaStream_t s) {
   SplitView v = make_view(t, t->pts);
   RUN(launch_distribute(t->fmt, v, p, t->leaf_pts.p, s));
   mark(t, 4, s);
+  if (!sync) {  // lod_build: the leaf-count invariant is checked on the device, reported after voxelize
+    RUN(launch_check_count(v.st, n, s));
+    CK(cudaGetLastError());
+    return LOD_OK;
+  }
   int r = read_state(t, s);
   if (r) return r;
   if ((r = check_errors(t, s))) return r;
+  if (t->host_state->count_b != n) return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
   CK(cudaGetLastError());
   return LOD_OK;
 }
 
 int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub, const lod_config* cfg,
-             cudaStream_t s) {
+             cudaStream_t s, bool final_sync = true) {
   if (t) t->dist = false;
   int r = phase_init(t, pts, n, fmt, ub, cfg, s);
   if (r) return r;
@@ -522,8 +528,7 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   while (cur > 0) {
     if ((r = phase_round(t, s)) || (r = phase_subanchors(t, &cur, s))) return r;
   }
-  if ((r = phase_skeleton(t, s)) || (r = phase_distribute(t, s))) return r;
-  if (t->host_state->count_b != n) return fail(LOD_ECONSISTENCY, "leaf received a different count than allocated");
+  if ((r = phase_skeleton(t, s)) || (r = phase_distribute(t, s, final_sync))) return r;
   t->split_done = true;
   return LOD_OK;
 }
@@ -540,7 +545,8 @@ struct VoxPlan {
   const void* d_imp_vox = nullptr;    // their voxels, concatenated (device)
 };
 
-int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxPlan* plan = nullptr) {
+int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxPlan* plan = nullptr,
+                bool split_errors_pending = false) {
   if (!t || !t->split_done) return fail(LOD_EVALUE, "lod_voxelize before a successful lod_split");
   if (mode < LOD_MODE_RANDOM || mode > LOD_MODE_WEIGHTED) return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
   CK(cudaSetDevice(t->device));
@@ -624,8 +630,12 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     CK(ensure(t->vchunks, chunk_cap * 16));
     CK(ensure(t->vleaf_chunks, chunk_cap * 16));
     CK(ensure(t->vvchunks, vchunk_cap * 8));
-    CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
-                       sizeof(DevState) - offsetof(DevState, err), s));
+    if (!(split_errors_pending && attempt == 0))  // else the split's device checks report with ours
+      CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
+                         sizeof(DevState) - offsetof(DevState, err), s));
+    else
+      CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, vox_cursor), 0,
+                         sizeof(DevState) - offsetof(DevState, vox_cursor), s));
     // arena: [earlier results][imports][this call's voxels]
     uint64_t cursor = base_cursor;
     if (plan && plan->n_imp) {
@@ -641,8 +651,12 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         cursor += c;
       }
     }
-    CK(cudaMemcpyAsync((char*)t->state.p + offsetof(DevState, vox_cursor), &cursor, 8, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
+    if (cursor) {  // host source on the stack: wait for the copy
+      CK(cudaMemcpyAsync((char*)t->state.p + offsetof(DevState, vox_cursor), &cursor, 8, cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    } else {
+      CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, vox_cursor), 0, 8, s));
+    }
     CK(cudaMemsetAsync(t->vcount.p, 0, 64 * 4 * (kMaxDepth + 1), s));
     VoxLevel L{};
     L.st = t->state.as<DevState>();
@@ -893,9 +907,11 @@ int lod_voxelize(lod_tree* t, int mode, uint64_t seed, void* stream) {
 int lod_build(lod_tree* t, const void* d_points, uint64_t n, int format, const lod_config* config, int mode,
               uint64_t seed, void* stream) {
   if (mode < LOD_MODE_RANDOM || mode > LOD_MODE_WEIGHTED) return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
-  int r = do_split(t, d_points, n, format, nullptr, config, (cudaStream_t)stream);
+  // one host round trip fewer: the split's last invariants are checked on the device and
+  // reported together with the voxelizer's
+  int r = do_split(t, d_points, n, format, nullptr, config, (cudaStream_t)stream, false);
   if (r) return r;
-  return do_voxelize(t, mode, seed, (cudaStream_t)stream);
+  return do_voxelize(t, mode, seed, (cudaStream_t)stream, nullptr, true);
 }
 
 int lod_tree_get_info(const lod_tree* t, lod_tree_info* o) {

@@ -390,6 +390,16 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
 // Chunking of n points: one sub-tile per chunk.  Larger chunks shrink the counts matrix
 // but spread each leaf's write front over many half-written lines (measured: 4 sub-tiles
 // per chunk -> +35% DRAM writes, +75% reads from read-modify-write of partial sectors).
+__global__ void k_check_count(DevState* st, uint64_t n) {
+  pdl_wait();
+  if (st->count_b != n) raise_err(st, ERR_COUNT);  // partition.py:268-269
+}
+
+int launch_check_count(DevState* st, uint64_t n, cudaStream_t s) {
+  launch_pdl(k_check_count, 1, 1, 0, s, st, n);
+  return 1;
+}
+
 void plan_segments(RadixPlan& p, uint64_t n, int sms) {
   (void)sms;
   p.tiles = (uint32_t)((n + kRadixTile - 1) / kRadixTile);

@@ -131,6 +131,7 @@ constexpr int kRadixItems = 8;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;
 constexpr int kRadixMaxBits = 11;
 void plan_segments(RadixPlan& plan, uint64_t n, int sms);
+int launch_check_count(DevState* st, uint64_t n, cudaStream_t s);
 int launch_distribute(int fmt, const SplitView& v, RadixPlan& plan, void* leaf_out, cudaStream_t s);
 
 // --- voxelize (voxelize.cu) ---
