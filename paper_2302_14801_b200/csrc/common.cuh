@@ -272,6 +272,32 @@ __host__ __device__ __forceinline__ uint32_t ceil_div_u32(uint64_t a, uint64_t b
 }
 
 // ---------------------------------------------------------------------------
+// L2 residency hints for lookup tables read at random while a large array streams past:
+// the table (targets, pyramid) is loaded evict-last, the stream (per-point keys)
+// evict-first, so the stream does not push the table out of L2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t ld_hint(const int32_t* a, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_hint(const uint32_t* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
+// ---------------------------------------------------------------------------
 // Programmatic dependent launch: every kernel is launched with programmatic stream
 // serialization and begins with griddepcontrol.wait, so the next grid's launch and block
 // scheduling overlap the previous grid's tail while memory ordering stays exactly that of

@@ -51,13 +51,14 @@ __device__ __forceinline__ void load_items(const SplitView& v, const void* in_re
   const uint64_t last = v.n - 1;
   if (FIRST) {
     uint32_t key[K];
+    const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t i = base + (uint64_t)k * 32 + lane;
-      key[k] = __ldg(v.pkey + (i < last ? i : last));
+      key[k] = ld_hint(v.pkey + (i < last ? i : last), stream);
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k) leaf[k] = (uint32_t)__ldg(v.t8 + key[k]);
+    for (int k = 0; k < K; ++k) leaf[k] = (uint32_t)ld_hint(v.t8 + key[k], keep);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t i = base + (uint64_t)k * 32 + lane;

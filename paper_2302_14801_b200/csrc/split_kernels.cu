@@ -318,13 +318,14 @@ __global__ void __launch_bounds__(kThreads) k_ext_count(SplitView v, uint32_t ro
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   constexpr int U = 4;
   bool bad = false;
+  const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < v.n; i0 += U * stride) {
     uint32_t key[U];
     int32_t t[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) key[u] = __ldg(v.pkey + min(i0 + u * stride, v.n - 1));
+    for (int u = 0; u < U; ++u) key[u] = ld_hint(v.pkey + min(i0 + u * stride, v.n - 1), stream);
 #pragma unroll
-    for (int u = 0; u < U; ++u) t[u] = __ldg(v.t8 + key[u]);
+    for (int u = 0; u < U; ++u) t[u] = ld_hint(v.t8 + key[u], keep);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t i = i0 + u * stride;
