@@ -378,7 +378,7 @@ def main():
     dom = max(range(5), key=lambda i: stages[i] if stage_bytes[i] else -1)
     achieved = stage_bytes[dom] / (stages[dom] / 1000.0) / 1e9
     whole_bytes = 80 * n + 12 * V
-    traffic = measured_traffic(args.config, args.mode, n, stage_names[dom])
+    traffic = measured_traffic(args.config, args.mode, n, stage_names[dom]) if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": f"{stage_names[dom]} stage ({stage_kernels[dom]})",
                 "algorithmic_bytes": stage_bytes[dom], "ms_per_build": stages[dom], "peak_source": peak_kind,
@@ -405,7 +405,7 @@ def main():
             "dtype": "f64-geometry/u32-counts", "data": "synthetic",
             "config": {"workload": args.config, "points_per_gpu": n, "mode": args.mode, "T": 50_000,
                        "grid": 128, "l2": "input 16 B/pt x points > 126 MB L2, no flush",
-                       "parallelism": f"subtree-sharded x{world} (NCCL all-reduce + all-to-all + rank-0 merge)"
+                       "parallelism": f"subtree-sharded x{world} ({args.backend} all-reduce + all-to-all + rank-0 merge)"
                        if world > 1 else "single"},
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
