@@ -324,11 +324,12 @@ int phase_anchors(lod_tree* t, uint32_t* cur, cudaStream_t s) {
   CK(ensure(t->list, max_anchor * 8 + 8));
   ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
   SplitView v = make_view(t, t->pts);
-  RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s));
+  RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s, false));
   int r = read_state(t, s);
   if (r) return r;
   if ((r = check_errors(t, s))) return r;
   *cur = (uint32_t)t->host_state->count_a;
+  if (*cur) RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s, true));  // none: no store pass
   t->round_base = D;
   t->round_first = 0;
   t->round_parent_first = 0;

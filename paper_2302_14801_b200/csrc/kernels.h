@@ -86,7 +86,8 @@ __device__ __forceinline__ int32_t leaf_of_point(const SplitView& v, const Cell1
 int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const double* user_bounds,
                   cudaStream_t s);
 int launch_count(int fmt, const SplitView& v, cudaStream_t s);
-int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s);
+// count pass (store = false; hit count -> st->count_a), then, if any, the store pass
+int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s, bool store);
 int launch_find_subanchors(const SplitView& v, uint32_t first_ext, uint32_t n_ext_round, int ext_levels,
                            uint64_t* list, ScanScratch& scr, cudaStream_t s);
 int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_t count,

@@ -167,6 +167,25 @@ int device_scan(uint64_t n, F f, ScanScratch& scr, const uint64_t* base_in, uint
   return 3;
 }
 
+// Two halves of device_compact, for callers that read the count on the host in between and
+// skip the store when there is nothing to store.
+template <class F>
+int device_compact_count(uint64_t n, F f, ScanScratch& scr, uint64_t* total_out, cudaStream_t st) {
+  uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
+  if (nb == 0) nb = 1;
+  if (scr.cap < nb + 1) return -1;
+  launch_pdl(k_compact_count<F>, nb, kScanThreads, 0, st, n, f, scr.sums);
+  launch_pdl(k_scan_sums, 1, 1024, 0, st, scr.sums, nb, nullptr, total_out);
+  return 2;
+}
+template <class F>
+int device_compact_store(uint64_t n, F f, ScanScratch& scr, cudaStream_t st) {
+  uint32_t nb = (uint32_t)((n + kScanTile - 1) / kScanTile);
+  if (nb == 0) nb = 1;
+  launch_pdl(k_compact_store<F>, nb, kScanThreads, 0, st, n, f, scr.sums);
+  return 1;
+}
+
 // Compaction of f.pred hits over [0, n); writes the hit count to *total_out (device).
 template <class F>
 int device_compact(uint64_t n, F f, ScanScratch& scr, uint64_t* total_out, cudaStream_t st) {

@@ -218,9 +218,10 @@ struct AnchorF {  // main finest cells with count > T (partition.py:111)
   __device__ void emit(uint64_t i, uint64_t pos) const { out[pos] = i; }
 };
 
-int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s) {
+int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s, bool store) {
   AnchorF f{v.pyr + level_off(v.D), v.T, list};
-  return device_compact(1ull << (3 * v.D), f, scr, &v.st->count_a, s);
+  if (!store) return device_compact_count(1ull << (3 * v.D), f, scr, &v.st->count_a, s);
+  return device_compact_store(1ull << (3 * v.D), f, scr, s);
 }
 
 struct SubAnchorF {  // extension finest cells with count > T (partition.py:140-143)
@@ -711,7 +712,9 @@ __device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t 
     t = v.node_idx[level_off(l - 1) + ((uint64_t)x * dp + y) * dp + z];
   }
   if (l == v.D) {
-    if (val != UNMERGEABLE) v.t8[c] = t;  // anchors keep -(ext+2); t8 was cleared to -1
+    // anchors keep -(ext+2); t8 was cleared to -1, so cells without an owning leaf
+    // (most of the grid for surfaces) need no write
+    if (val != UNMERGEABLE && t != -1) v.t8[c] = t;
   } else {
     v.node_idx[s] = t;
   }
