@@ -401,9 +401,9 @@ __device__ __forceinline__ uint32_t rank_of(const uint32_t* bits, const uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// K3: leaf-point samples -> accumulators.  The octant region's bits + prefixes are staged
-// in shared memory, so a sample's rank costs two shared loads; only the accumulator
-// atomics reach L2.
+// K3: leaf-point samples (average: and child voxels) -> accumulators.  The octant region's
+// bits + prefixes are staged in shared memory, so a sample's rank costs two shared loads;
+// only the accumulator atomics reach L2.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
   pdl_wait();
@@ -411,9 +411,14 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
   extern __shared__ __align__(16) uint32_t rsm[];
   uint32_t* rbits = rsm;
   uint32_t* rpre = rsm + kRegionWords;
-  const uint32_t nch = L.counters[1];
+  // average: child VOXELS are pushed here too (one reduction each into the level's
+  // accumulators, L2-resident) -- cheaper than K4 gathering every parent voxel's 2x2x2 block
+  // through the child's rank structure (~7 scattered sectors per voxel); the other modes
+  // need the winner's identity and keep the gather
+  const bool all = L.mode == LOD_MODE_AVERAGE;
+  const uint32_t nch = all ? L.counters[0] : L.counters[1];
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    const uint4 ch = L.leaf_chunks[c];
+    const uint4 ch = all ? L.chunks[c] : L.leaf_chunks[c];
     const VoxNode& nd = L.info[ch.x];
     const uint32_t* bits = bits_of(L, L.parity, ch.x);
     const uint32_t* pre = pre_of(L, L.parity, ch.x);
@@ -426,7 +431,8 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
       if (w) rpre[i] = __ldcg(pre + gw);  // empty words' prefixes are never read (nor written)
     }
     __syncthreads();
-    const uint2* src = L.stash + nd.cfirst[o];
+    const bool leafc = nd.cslot[o] == -1;
+    const uint2* src = (leafc ? L.stash : L.vox) + nd.cfirst[o];
     const uint32_t ob = nd.cbase[o];
     constexpr int U = 4;
     for (uint32_t j0 = ch.z + threadIdx.x; j0 < ch.w; j0 += U * kRT) {
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
       for (int u = 0; u < U; ++u) {
         const uint32_t j = j0 + u * kRT;
         if (j >= ch.w) continue;
-        const uint32_t key = r[u].x;
+        const uint32_t key = leafc ? r[u].x : voxel_to_parent(o, r[u].x);
         const uint32_t mask = (1u << (key & 31)) - 1;
         uint32_t lw, rank;
         if (region_word(key, o, lw))
@@ -600,7 +606,7 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
   uint64_t sr = 0, sg = 0, sb = 0, n = 0;
   uint32_t best = 0, best_rgb = 0;
   bool have = false;
-  if (cs >= 0) {
+  if (cs >= 0 && L.mode != LOD_MODE_AVERAGE) {  // (average: pushed by K3)
     // gather the child's 2x2x2 block: each (cx, cy) row holds both z cells in one word
     const uint32_t* cb = bits_of(L, cpar, (uint32_t)cs);
     const uint32_t* cp = pre_of(L, cpar, (uint32_t)cs);
