@@ -13,30 +13,32 @@
 //   K1 occupy    all samples, test-and-set their bit (L2 atomics only on first touch)
 //   K2 words     per 4096-word block: popcount sums; node offsets; word prefixes, voxel
 //                keys, the block's accumulators zeroed (one coalesced sweep of its ranks)
-//   K3 scatter   LEAF-point samples only: integer channel sums + counts (average,
-//                sampling.py:88-97) or atomicMax of (rand12 | ordinal20) (random,
-//                sampling.py:69-85 / PAPER Listing 1)
-//   K4 finalize  per voxel.  A voxel in an octant whose child is an inner node takes its
-//                samples from that child's 2x2x2 block of voxels (off + c/2, sampling.py:
-//                41-44): they are GATHERED through the child's kept bitmap + prefix, so
-//                voxel children need no atomics at all; leaf-point contributions (incl.
-//                the rare boundary spill into a neighbouring octant) come from K3.
+//   K3 scatter   every sample of the level -- leaf points (projected once by K1, stashed)
+//                and child voxels (key c in octant o -> off + c/2, sampling.py:41-44) --
+//                into its voxel's accumulator: integer channel sums + count as one f32x4
+//                reduction (average, sampling.py:88-97), atomicMax of (rand12 | ordinal20)
+//                (random, sampling.py:69-85 / PAPER Listing 1), atomicMax of ~ordinal
+//                (first-come).  The octant region's bits + prefixes sit in shared memory.
+//   K4 finalize  per voxel, from its accumulator alone (no gather from the child level:
+//                pushing child voxels was ~2x cheaper than pulling each parent voxel's
+//                2x2x2 block through the child's rank structure).
 //   Average: (2*sum + n) // (2*n) per channel over the children's ROUNDED colours (H5).
 //   Random : max (rand12 | ordinal20); the winning ordinal names the sample directly.
-//   First-come (sampling.py:61-66): min ordinal per cell (max of ~ordinal for leaf points;
-//            child voxels gathered with ordinal = octant base + the child's STORED position).
-//            The node's voxels are then listed by winning ordinal: K5 marks the winners in
-//            an ordinal bitmap (S bits per node), one level-wide popcount scan gives every
-//            winner its stored position p (vpos, used by the parent's gather) and the voxel
-//            is written to vout[vbase + p].  The arena itself stays in key order.
+//   First-come (sampling.py:61-66): min ordinal per cell, where a child voxel's ordinal is
+//            octant base + its STORED position in the child (vpos).  The node's voxels are
+//            then listed by winning ordinal: K5 marks the winners in an ordinal bitmap (S
+//            bits per node), one level-wide popcount scan gives every winner its stored
+//            position p (vpos, used by the parent) and the voxel is written to
+//            vout[vbase + p].  The arena itself stays in key order.
 //   Weighted (sampling.py:100-133): every sample (leaf points AND child voxels) adds
 //            w = clamp(1 - |g - centre|, 0, 1) to the occupied cells of its 2x2x2
 //            neighbourhood, as exact 2^-24 fixed-point u64 sums (order-independent, so
 //            repeated builds are bit-identical); colour = floor(sum(w c) / sum(w) + 0.5),
 //            within +-1 of the reference's sequential fp64 sums.
 //
-// Bitmaps/prefixes of a level are kept until the next (coarser) level has gathered from
-// them: two buffers alternate by depth parity.
+// Bitmaps/prefixes of a level are kept while the next (coarser) level runs (the
+// multi-GPU import path rebuilds them for imported subtree roots): two buffers alternate by
+// depth parity.
 #include "kernels.h"
 
 namespace lod {
@@ -411,14 +413,13 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
   extern __shared__ __align__(16) uint32_t rsm[];
   uint32_t* rbits = rsm;
   uint32_t* rpre = rsm + kRegionWords;
-  // average: child VOXELS are pushed here too (one reduction each into the level's
+  // child VOXELS are pushed here too (one reduction / atomicMax each into the level's
   // accumulators, L2-resident) -- cheaper than K4 gathering every parent voxel's 2x2x2 block
-  // through the child's rank structure (~7 scattered sectors per voxel); the other modes
-  // need the winner's identity and keep the gather
-  const bool all = L.mode == LOD_MODE_AVERAGE;
-  const uint32_t nch = all ? L.counters[0] : L.counters[1];
+  // through the child's rank structure (~7 scattered sectors per voxel); random and
+  // first-come keep the winner's ordinal, which names the sample for K4
+  const uint32_t nch = L.counters[0];
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    const uint4 ch = all ? L.chunks[c] : L.leaf_chunks[c];
+    const uint4 ch = L.chunks[c];
     const VoxNode& nd = L.info[ch.x];
     const uint32_t* bits = bits_of(L, L.parity, ch.x);
     const uint32_t* pre = pre_of(L, L.parity, ch.x);
@@ -463,10 +464,12 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
           unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 2 * a;
           atomicAdd(p, (unsigned long long)(rgb & 0xFF) | ((unsigned long long)((rgb >> 8) & 0xFF) << 32));
           atomicAdd(p + 1, (unsigned long long)((rgb >> 16) & 0xFF) | (1ull << 32));
-        } else if (L.mode == LOD_MODE_RANDOM) {
+        } else if (L.mode == LOD_MODE_RANDOM) {  // a child voxel's ordinal is its index in the child
           atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, rand_enc(nd.hash, ob + j));
-        } else {  // first-come: the smallest ordinal is the largest complement
-          atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, ~(ob + j));
+        } else {  // first-come: the smallest ordinal is the largest complement; a child voxel's
+                  // ordinal is its STORED position in the child (sampling.py:5-6, 64-66)
+          const uint32_t ord = ob + (leafc ? j : __ldg(L.vpos + nd.cfirst[o] + j));
+          atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, ~ord);
         }
       }
     }
@@ -576,17 +579,21 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter_w(VoxLevel L) {
 // ---------------------------------------------------------------------------
 // K4: finalize every voxel of the level
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t leaf_winner_rgb(const VoxLevel& L, const VoxNode& nd, uint32_t ord) {
-  int oo = 7;  // the leaf octant holding ordinal `ord`
-  while (oo > 0 && (nd.cslot[oo] != -1 || nd.cbase[oo] > ord)) --oo;
-  return __ldg(&L.stash[nd.cfirst[oo] + (ord - nd.cbase[oo])].y);
+// Colour of the sample with node ordinal `ord`: octant o = the child holding it, index =
+// ord - cbase[o] in the child's stored order (leaf: stash; inner: arena, or the stored-order
+// copy for first-come).
+__device__ __forceinline__ uint32_t winner_rgb(const VoxLevel& L, const VoxNode& nd, uint32_t ord) {
+  int oo = 7;
+  while (oo > 0 && (nd.ccount[oo] == 0 || nd.cbase[oo] > ord)) --oo;
+  const uint64_t at = nd.cfirst[oo] + (ord - nd.cbase[oo]);
+  if (nd.cslot[oo] == -1) return __ldg(&L.stash[at].y);
+  return __ldg(L.mode == LOD_MODE_FIRST_COME ? &L.vout[at].y : &L.vox[at].y);
 }
 
-// Colour of voxel `r` (key `key`) of node `nd`: children's samples gathered / accumulated
-// per mode; writes the record's colour (and, first-come, the winning ordinal).
+// Colour of voxel `r` of node `nd` from its accumulator (every sample was pushed by K3):
+// writes the record's colour (and, first-come, the winning ordinal).
 __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode& nd, uint64_t acc0, uint32_t key,
                                                uint32_t r) {
-  const int cpar = L.parity ^ 1;
   if (L.mode == LOD_MODE_WEIGHTED) {
     const unsigned long long* a = reinterpret_cast<const unsigned long long*>(L.acc) + 4 * (acc0 + r);
     const double W = (double)__ldcg(a);
@@ -600,43 +607,8 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
     L.vox[nd.vbase + r].y = rgb;
     return;
   }
-  const uint32_t X = key >> 14, Y = (key >> 7) & 127, Z = key & 127;
-  const int o = (int)((X >> 6) | ((Y >> 6) << 1) | ((Z >> 6) << 2));
-  const int32_t cs = nd.cslot[o];
+  (void)key;
   uint64_t sr = 0, sg = 0, sb = 0, n = 0;
-  uint32_t best = 0, best_rgb = 0;
-  bool have = false;
-  if (cs >= 0 && L.mode != LOD_MODE_AVERAGE) {  // (average: pushed by K3)
-    // gather the child's 2x2x2 block: each (cx, cy) row holds both z cells in one word
-    const uint32_t* cb = bits_of(L, cpar, (uint32_t)cs);
-    const uint32_t* cp = pre_of(L, cpar, (uint32_t)cs);
-    const VoxNode& ci = L.cinfo[cs];
-    const uint32_t cx0 = (X & 63) << 1, cy0 = (Y & 63) << 1, cz0 = (Z & 63) << 1;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t ck = ((cx0 + (q & 1)) << 14) | ((cy0 + (q >> 1)) << 7) | cz0;
-      const uint32_t w = ck >> 5, b = ck & 31;
-      const uint32_t bw = __ldg(cb + w);  // child level: read-only here, neighbours share words (L1)
-      const uint32_t two = (bw >> b) & 3u;
-      if (!two) continue;
-      uint32_t cr = __ldg(cp + w) + __popc(bw & ((1u << b) - 1));
-#pragma unroll
-      for (int dz = 0; dz < 2; ++dz) {
-        if (!((two >> dz) & 1)) continue;
-        const uint32_t rgb = __ldg(&L.vox[ci.vbase + cr].y);
-        if (L.mode == LOD_MODE_AVERAGE) {
-          sr += rgb & 0xFF, sg += (rgb >> 8) & 0xFF, sb += (rgb >> 16) & 0xFF, ++n;
-        } else if (L.mode == LOD_MODE_RANDOM) {
-          uint32_t e = rand_enc(nd.hash, nd.cbase[o] + cr);
-          if (!have || e > best) best = e, best_rgb = rgb, have = true;
-        } else {  // first-come: ordinal = octant base + the child's stored position
-          const uint32_t ord = nd.cbase[o] + __ldg(L.vpos + ci.vbase + cr);
-          if (!have || ord < best) best = ord, best_rgb = rgb, have = true;
-        }
-        ++cr;
-      }
-    }
-  }
   uint32_t rgb;
   if (L.mode == LOD_MODE_AVERAGE) {
     if (L.exact_sums) {
@@ -650,14 +622,12 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
     rgb = mean_round(sr, n) | (mean_round(sg, n) << 8) | (mean_round(sb, n) << 16);
   } else if (L.mode == LOD_MODE_RANDOM) {
     const uint32_t e = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
-    // the winner is a leaf point: its ordinal names (child, index) directly
-    rgb = (!have || e > best) ? leaf_winner_rgb(L, nd, e & 0xFFFFFu) : best_rgb;
+    rgb = winner_rgb(L, nd, e & 0xFFFFFu);  // the winning ordinal names the sample
   } else {
     uint32_t* a = reinterpret_cast<uint32_t*>(L.acc) + acc0 + r;
-    const uint32_t e = __ldcg(a);
-    if (e != 0 && (!have || ~e < best)) best = ~e, best_rgb = leaf_winner_rgb(L, nd, ~e);
-    rgb = best_rgb;
-    *a = best;  // winning ordinal, ranked by K5
+    const uint32_t ord = ~__ldcg(a);
+    rgb = winner_rgb(L, nd, ord);
+    *a = ord;  // winning ordinal, ranked by K5
   }
   L.vox[nd.vbase + r].y = rgb;
 }
