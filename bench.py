@@ -257,16 +257,19 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     stage_sum = [0.0] * 5
+    kernel_sum = 0.0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             step()
             stage_sum = [a + b for a, b in zip(stage_sum, dev.stage_ms())]
+            kernel_sum += dev.kernel_ms()
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     stages = [x / args.steps for x in stage_sum]
+    scatter_ms = kernel_sum / args.steps
     dev.set_timing(False)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
@@ -364,26 +367,29 @@ def main():
                "d2h_bytes_per_step": rec_bytes + vox_bytes + node_bytes, "ms_per_step": ems,
                "pipeline": pipeline}
 
-    # ---- roofline of the dominant stage (algorithmic bytes) ----
-    # bounds 16N + count 16N, extension 16E, distribute 32N (read + write each record),
-    # voxelize 16N (leaf points) + 12V (each voxel written and read once as a 6-B record);
-    # the skeleton (merge / nodes / targets) is N-independent and has no per-point bytes.
+    # ---- roofline ----
+    # Dominant single kernel: the distribute's K_scatter (stable counting-sort scatter), the
+    # longest kernel of a build (ncu launch lists in profiles/).  Its algorithmic bytes per
+    # pass: every record read once and written once (32 B/pt).  Timed live with CUDA events
+    # the library records around it on the build's stream, averaged over the timed builds.
+    # Per stage: bounds 16N + count 16N, extension 16E, distribute 32N,
+    # voxelize 16N + 12V (each voxel written and read once as a 6-B record); the skeleton
+    # (merge / nodes / targets) is N-independent.
     peak, peak_kind = hbm_peak()
     V = info.n_voxels
+    passes = max(info.radix_passes, 1)
     stage_names = ["bounds+count", "extension", "merge+nodes+targets", "distribute", "voxelize"]
-    stage_kernels = ["k_bounds_f32, k_count", "k_ext_count", "k_merge, compactions, k_target_*",
-                     "k_dist_hist, k_dist_scan_*, k_dist_scatter",
-                     "per level: k_setup, k_occupy, k_block_sums, k_alloc, k_prefix, k_scatter, k_finalize"]
     stage_bytes = [32 * n, 16 * n if info.n_ext_grids else 0, 0, 32 * n, 16 * n + 12 * V]
-    dom = max(range(5), key=lambda i: stages[i] if stage_bytes[i] else -1)
-    achieved = stage_bytes[dom] / (stages[dom] / 1000.0) / 1e9
+    kern_bytes = 32 * n * passes
+    achieved = kern_bytes / (scatter_ms / 1000.0) / 1e9 if scatter_ms > 0 else 0.0
     whole_bytes = 80 * n + 12 * V
-    traffic = measured_traffic(args.config, args.mode, n, stage_names[dom]) if world == 1 else None
+    traffic = measured_traffic(args.config, args.mode, n, "k_dist_scatter") if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"{stage_names[dom]} stage ({stage_kernels[dom]})",
-                "algorithmic_bytes": stage_bytes[dom], "ms_per_build": stages[dom], "peak_source": peak_kind,
+                "traffic": traffic, "kernel": f"k_dist_scatter (distribute.cu), {passes} pass(es)",
+                "algorithmic_bytes": kern_bytes, "ms_per_build": scatter_ms, "peak_source": peak_kind,
                 "stages": {nm: {"ms": st, "algorithmic_bytes": b,
-                                "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st > 0 else None}
+                                "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st > 0 else None,
+                                "traffic": measured_traffic(args.config, args.mode, n, nm) if world == 1 else None}
                            for nm, st, b in zip(stage_names, stages, stage_bytes)},
                 "whole_build": {"algorithmic_bytes": whole_bytes,
                                 "achieved_gbs": whole_bytes / (ms / 1000.0) / 1e9,

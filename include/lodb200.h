@@ -189,6 +189,10 @@ uint64_t lod_tree_device_bytes(const lod_tree* tree);
 int lod_set_timing(lod_tree* tree, int enabled);
 int lod_tree_stage_ms(const lod_tree* tree, float* out5);
 
+/* Device time of the dominant single kernel of the last build (timing enabled):
+ * out[0] = the distribute's K_scatter, summed over its passes, milliseconds. */
+int lod_tree_kernel_ms(const lod_tree* tree, float* out1);
+
 /* Number of kernel launches issued by the last lod_split + lod_voxelize. */
 uint64_t lod_tree_launches(const lod_tree* tree);
 

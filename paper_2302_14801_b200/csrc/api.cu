@@ -84,6 +84,7 @@ struct lod_tree {
   uint64_t launches = 0;
   bool timing = false;
   cudaEvent_t ev[6] = {};
+  cudaEvent_t kev[4] = {};  // the distribute's K_scatter, per pass (the dominant single kernel)
   float stage_ms[5] = {};
 
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
@@ -495,6 +496,7 @@ int phase_distribute(lod_tree* t, cudaStream_t s, bool sync = true) {
     CK(ensure(t->digit_base, (size_t)(2 << kRadixMaxBits) * 8 * 2));
     if (p.passes == 2) CK(ensure(t->tmp_rec, n * rec));
     CK(ensure(t->tmp_leaf, n * 4 * p.passes));  // leaf ids in input order (+ sorted by the 1st digit)
+    for (int i = 0; i < 4; ++i) p.scatter_ev[i] = t->timing ? t->kev[i] : nullptr;
     p.counts = t->status.as<uint32_t>();
     p.scan_part = p.counts + ((size_t)p.segs << maxb);
     p.digit_base = t->digit_base.as<uint64_t>();
@@ -874,6 +876,7 @@ lod_tree* lod_tree_create(int device) {
     return nullptr;
   }
   for (auto& e : t->ev) cudaEventCreate(&e);
+  for (auto& e : t->kev) cudaEventCreate(&e);
   return t;
 }
 
@@ -891,6 +894,8 @@ void lod_tree_destroy(lod_tree* t) {
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : t->kev)
     if (e) cudaEventDestroy(e);
   if (t->host_state) cudaFreeHost(t->host_state);
   delete t;
@@ -1093,6 +1098,18 @@ int lod_tree_stage_ms(const lod_tree* tc, float* out) {
   for (int i = 0; i < 5; ++i) {
     out[i] = 0;
     if (cudaEventElapsedTime(&out[i], t->ev[i], t->ev[i + 1]) != cudaSuccess) out[i] = -1;
+  }
+  cudaGetLastError();
+  return LOD_OK;
+}
+
+int lod_tree_kernel_ms(const lod_tree* tc, float* out) {
+  lod_tree* t = const_cast<lod_tree*>(tc);
+  if (!t || !t->timing) return fail(LOD_EVALUE, "timing not enabled");
+  out[0] = 0;
+  for (int p = 0; p < t->plan.passes; ++p) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, t->kev[2 * p], t->kev[2 * p + 1]) == cudaSuccess) out[0] += ms;
   }
   cudaGetLastError();
   return LOD_OK;

@@ -344,8 +344,11 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   const uint32_t* leaf_in = FIRST ? leaf_tmp : in_leaf;
   launch_pdl(hist, p.segs, kRadixThreads, hsm, s, v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
   const int nscan = launch_dist_scan(p.counts, p.segs, B, digit_base, p.scan_part, s);
+  const cudaEvent_t* ev = p.scatter_ev + (FIRST ? 0 : 2);
+  if (ev[0]) cudaEventRecord(ev[0], s);
   launch_pdl(scat, p.segs, kRadixThreads, ssm, s, v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,
                                           p.seg_tiles, p.tiles, p.counts);
+  if (ev[1]) cudaEventRecord(ev[1], s);
   return 2 + nscan;
 }
 

@@ -145,6 +145,12 @@ class DeviceTree:
         _abi.check(self.lib.lod_tree_stage_ms(self.h, out))
         return list(out)
 
+    def kernel_ms(self) -> float:
+        """Device ms of the distribute's K_scatter (all passes) in the last timed build."""
+        out = (C.c_float * 1)()
+        _abi.check(self.lib.lod_tree_kernel_ms(self.h, out))
+        return float(out[0])
+
     def launches(self) -> int:
         return int(self.lib.lod_tree_launches(self.h))
 

@@ -34,7 +34,10 @@ for d in items[start:]:
         stage = 3
     if stage <= 3 and "k_setup" in k:
         stage = 4
-    out[names[stage]] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+    b = d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+    out[names[stage]] += b
+    if "k_dist_scatter" in k:   # the dominant single kernel (bench.py roofline)
+        out["k_dist_scatter"] = out.get("k_dist_scatter", 0.0) + b
 dst = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
 t = json.load(open(dst)) if os.path.exists(dst) else {}
 t[f"{config}:{mode}"] = {"points": points, "stages": {k: int(v) for k, v in out.items()},
