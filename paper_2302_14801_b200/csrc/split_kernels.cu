@@ -695,9 +695,8 @@ int launch_leaf_offsets_local(const SplitView& v, ScanScratch& scr, cudaStream_t
 // UNMERGEABLE cell owns nothing, an empty cell inherits its parent's owner.  The result is
 // written in place over node_idx (level l reads level l-1's finished targets); the finest
 // level goes to t8, where extension anchors keep their -(ext+2) pointer.
-__device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t c) {
+__device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t c, uint32_t val) {
   const uint64_t s = level_off(l) + c;
-  const uint32_t val = v.pyr[s];
   int32_t t;
   if (val == UNMERGEABLE) {
     t = -1;
@@ -724,17 +723,25 @@ __device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t 
 __global__ void __launch_bounds__(1024) k_target_small(SplitView v, int top) {
   pdl_wait();
   for (int l = 0; l <= top; ++l) {
-    for (uint64_t c = threadIdx.x; c < (1ull << (3 * l)); c += blockDim.x) target_cell(v, l, c);
+    for (uint64_t c = threadIdx.x; c < (1ull << (3 * l)); c += blockDim.x) target_cell(v, l, c, v.pyr[level_off(l) + c]);
     __syncthreads();
   }
 }
 
+// four consecutive cells per thread per trip: their pyramid loads are independent, so
+// they are in flight together (one cell per thread left this pass latency-bound)
 __global__ void __launch_bounds__(kThreads) k_target_level(SplitView v, int l) {
   pdl_wait();
   const uint64_t cells = 1ull << (3 * l);
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
-       c += (uint64_t)gridDim.x * blockDim.x)
-    target_cell(v, l, c);
+  for (uint64_t c0 = 4 * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x); c0 < cells;
+       c0 += 4ull * gridDim.x * blockDim.x) {
+    uint32_t val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) val[u] = c0 + u < cells ? v.pyr[level_off(l) + c0 + u] : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + u < cells) target_cell(v, l, c0 + u, val[u]);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_target_ext(SplitView v, uint32_t first, uint32_t count, int ext) {
@@ -768,7 +775,7 @@ int launch_targets(const SplitView& v, cudaStream_t s) {
   launch_pdl(k_target_small, 1, 1024, 0, s, v, small);
   int launches = 1;
   for (int l = small + 1; l <= v.D; ++l, ++launches)
-    launch_pdl(k_target_level, merge_blocks(1ull << (3 * l)), kThreads, 0, s, v, l);
+    launch_pdl(k_target_level, merge_blocks(1ull << (3 * l - 2)), kThreads, 0, s, v, l);
   return launches;
 }
 
