@@ -92,7 +92,7 @@ struct lod_tree {
   DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
   DevBuf leaf_pts, status, digit_base, tmp_rec, tmp_leaf, pkey, pc16;
   DevBuf vox, export_buf, stash;
-  DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vleaf_chunks, vvchunks;
+  DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vvchunks;
   DevBuf vpos, vout, obits, opre;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
   DevState* host_state = nullptr;  // pinned mirror
 
@@ -631,7 +631,6 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     const uint64_t chunk_cap = voxelize_chunk_capacity(t->n + cap, widest);
     const uint64_t vchunk_cap = voxelize_vchunk_capacity(cap, widest);
     CK(ensure(t->vchunks, chunk_cap * 16));
-    CK(ensure(t->vleaf_chunks, chunk_cap * 16));
     CK(ensure(t->vvchunks, vchunk_cap * 8));
     if (!(split_errors_pending && attempt == 0))  // else the split's device checks report with ours
       CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
@@ -686,7 +685,6 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.pre = t->vpre.as<uint32_t>();
     L.blk_sum = t->vblk.as<uint32_t>();
     L.chunks = t->vchunks.as<uint4>();
-    L.leaf_chunks = t->vleaf_chunks.as<uint4>();
     L.vchunks = t->vvchunks.as<uint2>();
     L.vox = t->vox.as<uint2>();
     L.vox_cap = cap;
@@ -705,7 +703,6 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
       if (!lst_n[d] && !imp_n[d]) continue;
       L.parity = d & 1;
       L.info = t->vinfo.as<VoxNode>() + (size_t)L.parity * widest;
-      L.cinfo = t->vinfo.as<VoxNode>() + (size_t)(L.parity ^ 1) * widest;
       L.counters = t->vcount.as<uint32_t>() + 64 * d;
       L.level_start = t->vlevel_start.as<uint64_t>() + d;
       if (lst_n[d]) {
@@ -889,7 +886,7 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->leaf_pbox, &t->leaf_pinv, &t->depth_count, &t->depth_off, &t->depth_cursor, &t->depth_lists, &t->leaf_pts, &t->status,
                    &t->digit_base, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
-                   &t->node_slot, &t->vacc, &t->vchunks, &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
+                   &t->node_slot, &t->vacc, &t->vchunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
                    &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
@@ -1079,7 +1076,7 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->leaf_pts, &t->status, &t->digit_base, &t->tmp_rec, &t->tmp_leaf,
                          &t->vox, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
-                         &t->vleaf_chunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
+                         &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
                    &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;

@@ -169,11 +169,9 @@ struct VoxLevel {
   uint32_t* bits;          // [2][slots][2^16] occupancy words
   uint32_t* pre;           // [2][slots][2^16] exclusive popcount prefix per word
   VoxNode* info;           // this level's infos (parity slice)
-  const VoxNode* cinfo;    // child level's infos (other parity slice)
   uint32_t* blk_sum;       // [list_n * 16]
-  uint32_t* counters;      // [3]: sample chunks, leaf chunks, voxel chunks
+  uint32_t* counters;      // [0] sample chunks, [2] voxel chunks
   uint4* chunks;
-  uint4* leaf_chunks;
   uint2* vchunks;
   uint64_t* level_start;   // arena cursor at the start of this level
   uint2* vox;              // arena: {key, rgb}

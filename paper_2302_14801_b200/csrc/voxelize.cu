@@ -151,11 +151,9 @@ __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
   const uint32_t chunk = L.chunk;
   const uint32_t nch = (cnt + chunk - 1) / chunk;
   uint32_t at = atomicAdd(L.counters + 0, nch);
-  uint32_t lat = cslot == -1 ? atomicAdd(L.counters + 1, nch) : 0;
   for (uint32_t j = 0; j < cnt; j += chunk) {
     uint4 ch = make_uint4(s, (uint32_t)o, j, min(cnt, j + chunk));
     L.chunks[at++] = ch;
-    if (cslot == -1) L.leaf_chunks[lat++] = ch;
   }
 }
 
