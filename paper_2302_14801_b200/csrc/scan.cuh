@@ -47,11 +47,18 @@ __device__ __forceinline__ T block_excl_scan(T v, T* total, T* smem /* >= NT/32 
   return out;
 }
 
+// Scan functors provide value(i), store(i, excl, item) and limit(n): the live length, which
+// may be a device-side count below the launch length (blocks past it do no work).
 template <class F>
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(uint64_t n, F f, uint64_t* block_sums) {
   pdl_wait();
   __shared__ uint64_t sm[kScanThreads / 32 + 1];
   uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  n = f.limit(n);
+  if (base >= n) {
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = 0;
+    return;
+  }
   uint64_t s = 0;
 #pragma unroll 4
   for (int k = 0; k < kScanItems; ++k) {
@@ -76,6 +83,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_store(uint64_t n, F f, co
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t running = block_sums[blockIdx.x];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  n = f.limit(n);
+  if (base >= n) return;
   for (int k = 0; k < kScanItems; ++k) {
     const uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
     const uint64_t v = i < n ? f.value(i) : 0;

@@ -626,6 +626,7 @@ struct LeafNumF {
   const uint32_t* val;
   int32_t* n_leaf;
   uint32_t* leaf_node;
+  __device__ uint64_t limit(uint64_t n) const { return n; }
   __device__ uint64_t value(uint64_t k) const { return val[k] != UNMERGEABLE ? 1 : 0; }
   __device__ void store(uint64_t k, uint64_t ex, uint64_t v) const {
     n_leaf[k] = v ? (int32_t)ex : -1;
@@ -647,6 +648,7 @@ struct LeafOffF {
   uint32_t* leaf_count;
   uint64_t* n_first;
   uint32_t* n_count;
+  __device__ uint64_t limit(uint64_t n) const { return n; }
   __device__ uint64_t value(uint64_t j) const { return val ? val[leaf_node[j]] : cnt[j]; }
   __device__ void store(uint64_t j, uint64_t ex, uint64_t v) const {
     uint32_t k = leaf_node[j];

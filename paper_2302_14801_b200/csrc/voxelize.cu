@@ -26,8 +26,8 @@
 //   Random : max (rand12 | ordinal20); the winning ordinal names the sample directly.
 //   First-come (sampling.py:61-66): min ordinal per cell, where a child voxel's ordinal is
 //            octant base + its STORED position in the child (vpos).  The node's voxels are
-//            then listed by winning ordinal: K5 marks the winners in an ordinal bitmap (S
-//            bits per node), one level-wide popcount scan gives every winner its stored
+//            then listed by winning ordinal: K4 marks the winners in an ordinal bitmap (S
+//            bits per node), one popcount scan over the level's live words gives every winner its stored
 //            position p (vpos, used by the parent) and the voxel is written to
 //            vout[vbase + p].  The arena itself stays in key order.
 //   Weighted (sampling.py:100-133): every sample (leaf points AND child voxels) adds
@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
   if (threadIdx.x == 0) {
     if (carry > L.vox_cap || carry - L.level_start[0] > L.acc_cap || ocarry > L.ocap)
       raise_err(L.st, ERR_ARENA, 0, carry);
+    L.counters[4] = (uint32_t)min(ocarry, (uint64_t)L.ocap);  // first-come: ordinal words in use
     L.st->vox_cursor = carry;
   }
 }
@@ -625,7 +626,8 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
     uint32_t* a = reinterpret_cast<uint32_t*>(L.acc) + acc0 + r;
     const uint32_t ord = ~__ldcg(a);
     rgb = winner_rgb(L, nd, ord);
-    *a = ord;  // winning ordinal, ranked by K5
+    *a = ord;  // winning ordinal, ranked by K5 through the node's ordinal bitmap
+    atomicOr(L.obits + nd.obase + (ord >> 5), 1u << (ord & 31));
   }
   L.vox[nd.vbase + r].y = rgb;
 }
@@ -648,25 +650,11 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
 // ---------------------------------------------------------------------------
 // K5 (first-come): stored order = ascending winning ordinal (sampling.py:64-66)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kT) k_fc_mark(VoxLevel L) {
-  pdl_wait();
-  if (L.st->err & ERR_ARENA) return;
-  const uint32_t nch = L.counters[2];
-  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    const uint2 ch = L.vchunks[c];
-    const VoxNode& nd = L.info[ch.x];
-    const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
-    const uint64_t acc0 = nd.vbase - L.level_start[0];
-    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
-      const uint32_t ord = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
-      atomicOr(L.obits + nd.obase + (ord >> 5), 1u << (ord & 31));
-    }
-  }
-}
-
 struct OrdScanF {  // exclusive popcount prefix over the level's ordinal bitmaps
   const uint32_t* bits;
   uint32_t* pre;
+  const uint32_t* live;  // words in use this level (K2's allocation)
+  __device__ uint64_t limit(uint64_t n) const { return min(n, (uint64_t)__ldcg(live)); }
   __device__ uint64_t value(uint64_t i) const { return __popc(__ldcg(bits + i)); }
   __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { pre[i] = (uint32_t)excl; }
 };
@@ -830,14 +818,13 @@ int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStre
     launch_pdl(k_scatter_w, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
   else
     launch_pdl(k_scatter, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
+  if (L.mode == LOD_MODE_FIRST_COME) cudaMemsetAsync(L.obits, 0, L.ocap * 4, s);  // K4 marks winners
   launch_pdl(k_finalize, grid, kT, 0, s, L);
   if (L.mode == LOD_MODE_FIRST_COME) {
-    cudaMemsetAsync(L.obits, 0, L.ocap * 4, s);
-    launch_pdl(k_fc_mark, grid, kT, 0, s, L);
-    const int r = device_scan(L.ocap, OrdScanF{L.obits, L.opre}, scr, nullptr, nullptr, s);
+    const int r = device_scan(L.ocap, OrdScanF{L.obits, L.opre, L.counters + 4}, scr, nullptr, nullptr, s);
     if (r < 0) return r;
     launch_pdl(k_fc_pos, grid, kT, 0, s, L);
-    launches += 2 + r;
+    launches += 1 + r;
   }
   return launches;
 }
