@@ -94,7 +94,14 @@ struct lod_tree {
   DevBuf vox, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vvchunks;
   DevBuf vpos, vout, obits, opre;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
-  DevState* host_state = nullptr;  // pinned mirror
+  // pinned, device-mapped mirror of the device state (+ the per-depth counts): the build's
+  // small device<->host exchanges are done by kernels over mapped memory, never by the copy
+  // engines, so they do not queue behind bulk uploads / downloads of other streams (a
+  // pipelined caller's 400-MB tree download held every build back by its full length)
+  DevState* host_state = nullptr;
+  DevState* host_state_dev = nullptr;
+  uint32_t* host_depth = nullptr;  // [kMaxDepth + 2]: inner nodes per depth, deepest used
+  uint32_t* host_depth_dev = nullptr;
 
   uint32_t n_nodes = 0, n_leaves = 0, n_ext = 0, max_depth_used = 0;
   uint32_t inner_per_depth[kMaxDepth + 1] = {};
@@ -118,8 +125,32 @@ struct lod_tree {
 
 namespace {
 
+// word copies by one CTA: device -> mapped host memory (and small device-side sets)
+__global__ void k_copy_words(uint32_t* dst, const uint32_t* src, uint32_t n) {
+  pdl_wait();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcg(src + i);
+}
+__global__ void k_state_set(DevState* dst, DevState v) {
+  pdl_wait();
+  if (threadIdx.x == 0) *dst = v;
+}
+struct DepthWords {
+  uint32_t v[kMaxDepth + 1];
+};
+__global__ void k_depth_set(uint32_t* dst, DepthWords w) {
+  pdl_wait();
+  if (threadIdx.x <= kMaxDepth) dst[threadIdx.x] = w.v[threadIdx.x];
+}
+__global__ void k_set_u64(uint64_t* dst, uint64_t v) {
+  pdl_wait();
+  *dst = v;
+}
+
 int read_state(lod_tree* t, cudaStream_t s) {
-  LOD_CUDA_CHECK(cudaMemcpyAsync(t->host_state, t->state.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  static_assert(sizeof(DevState) % 4 == 0, "DevState is copied as words");
+  launch_pdl(k_copy_words, 1, 64, 0, s, reinterpret_cast<uint32_t*>(t->host_state_dev),
+             reinterpret_cast<const uint32_t*>(t->state.p), (uint32_t)(sizeof(DevState) / 4));
+  LOD_CUDA_CHECK(cudaGetLastError());
   LOD_CUDA_CHECK(cudaStreamSynchronize(s));
   return LOD_OK;
 }
@@ -290,7 +321,7 @@ int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* 
   for (int a = 0; a < 3; ++a) init.lo_key[a] = ~0ull, init.hi_key[a] = 0;
   *t->host_state = init;
   CK(ensure(t->state, sizeof(DevState)));
-  CK(cudaMemcpyAsync(t->state.p, t->host_state, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  launch_pdl(k_state_set, 1, 32, 0, s, t->state.as<DevState>(), init);
   CK(ensure(t->pyr, main_cells * 4));
   CK(cudaMemsetAsync(t->pyr.p, 0, main_cells * 4, s));
   CK(ensure(t->t8, fine_cells * 4));
@@ -441,10 +472,10 @@ int phase_skeleton(lod_tree* t, cudaStream_t s) {
   RUN(launch_build_nodes(v, t->slots.as<uint64_t>(), s));
   RUN(launch_number_leaves(v, scr, s));
   RUN(launch_depth_lists(v, t->depth_count.as<uint32_t>(), s));
-  CK(cudaMemcpyAsync(t->inner_per_depth, t->depth_count.p, sizeof(t->inner_per_depth), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(&t->max_depth_used, t->depth_count.as<uint32_t>() + kMaxDepth + 1, 4, cudaMemcpyDeviceToHost,
-                     s));
+  launch_pdl(k_copy_words, 1, 64, 0, s, t->host_depth_dev, t->depth_count.as<uint32_t>(), (uint32_t)(kMaxDepth + 2));
   if ((r = read_state(t, s))) return r;
+  for (int d = 0; d <= kMaxDepth; ++d) t->inner_per_depth[d] = t->host_depth[d];
+  t->max_depth_used = t->host_depth[kMaxDepth + 1];
   if ((r = check_errors(t, s))) return r;
   t->n_leaves = (uint32_t)t->host_state->count_a;
   v = make_view(t, t->pts);
@@ -457,7 +488,11 @@ int phase_skeleton(lod_tree* t, cudaStream_t s) {
   CK(ensure(t->depth_lists, (size_t)std::max<uint32_t>(off, 1) * 4));
   CK(ensure(t->depth_off, 64 * 4));
   CK(ensure(t->depth_cursor, 64 * 4));
-  CK(cudaMemcpyAsync(t->depth_off.p, t->inner_off, sizeof(t->inner_off), cudaMemcpyHostToDevice, s));
+  {
+    DepthWords w;
+    for (int d = 0; d <= kMaxDepth; ++d) w.v[d] = t->inner_off[d];
+    launch_pdl(k_depth_set, 1, 64, 0, s, t->depth_off.as<uint32_t>(), w);
+  }
   CK(cudaMemsetAsync(t->depth_cursor.p, 0, 64 * 4, s));
   RUN(launch_depth_scatter(v, t->depth_off.as<uint32_t>(), t->depth_cursor.as<uint32_t>(),
                            t->depth_lists.as<uint32_t>(), s));
@@ -653,9 +688,9 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         cursor += c;
       }
     }
-    if (cursor) {  // host source on the stack: wait for the copy
-      CK(cudaMemcpyAsync((char*)t->state.p + offsetof(DevState, vox_cursor), &cursor, 8, cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));
+    if (cursor) {
+      launch_pdl(k_set_u64, 1, 1, 0, s, reinterpret_cast<uint64_t*>((char*)t->state.p + offsetof(DevState, vox_cursor)),
+                 (uint64_t)cursor);
     } else {
       CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, vox_cursor), 0, 8, s));
     }
@@ -867,11 +902,21 @@ extern "C" {
 lod_tree* lod_tree_create(int device) {
   lod_tree* t = new lod_tree();
   t->device = device;
-  if (cudaSetDevice(device) != cudaSuccess || cudaMallocHost(&t->host_state, sizeof(DevState)) != cudaSuccess) {
+  void* hm = nullptr;
+  void* hm_dev = nullptr;
+  const size_t depth_at = (sizeof(DevState) + 15) & ~(size_t)15;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaHostAlloc(&hm, depth_at + 4 * (kMaxDepth + 2), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&hm_dev, hm, 0) != cudaSuccess) {
+    if (hm) cudaFreeHost(hm);
     fail(LOD_ECUDA, "cannot initialise CUDA device %d", device);
     delete t;
     return nullptr;
   }
+  t->host_state = static_cast<DevState*>(hm);
+  t->host_state_dev = static_cast<DevState*>(hm_dev);
+  t->host_depth = reinterpret_cast<uint32_t*>(static_cast<char*>(hm) + depth_at);
+  t->host_depth_dev = reinterpret_cast<uint32_t*>(static_cast<char*>(hm_dev) + depth_at);
   for (auto& e : t->ev) cudaEventCreate(&e);
   for (auto& e : t->kev) cudaEventCreate(&e);
   return t;
