@@ -32,9 +32,24 @@ __global__ void u32x4(unsigned* a, uint32_t n, uint32_t m) {
     atomicAdd(a + 4 * s, 1u); atomicAdd(a + 4 * s + 1, 2u); atomicAdd(a + 4 * s + 2, 3u); atomicAdd(a + 4 * s + 3, 1u);
   }
 }
+__global__ void st16(uint4* a, uint32_t n, uint32_t m) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t s = hsh(i) % m;
+    a[s] = make_uint4(i, 1, 2, 3);
+  }
+}
+// 16-B reductions where consecutive samples mostly hit nearby slots (spatially sorted input)
+__global__ void f32x4_local(float* a, uint32_t n, uint32_t m) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t s = (uint32_t)(((uint64_t)i * m) / n) + (hsh(i) & 63);
+    if (s >= m) s = m - 1;
+    float* p = a + 4 * s;
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1.f), "f"(2.f), "f"(3.f), "f"(1.f) : "memory");
+  }
+}
 int main() {
   const uint32_t n = 20000000;
-  for (uint32_t m : {9000000u, 1000000u, 100000u}) {
+  for (uint32_t m : {5000000u, 1000000u, 100000u}) {
     void* a; cudaMalloc(&a, (size_t)m * 16); cudaMemset(a, 0, (size_t)m * 16);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     auto run = [&](const char* nm, auto f) {
@@ -46,6 +61,8 @@ int main() {
     run("u64x1", [&] { u64x1<<<148 * 8, 256>>>((unsigned long long*)a, n, m); });
     run("f32x4", [&] { f32x4<<<148 * 8, 256>>>((float*)a, n, m); });
     run("u32x4", [&] { u32x4<<<148 * 8, 256>>>((unsigned*)a, n, m); });
+    run("st16", [&] { st16<<<148 * 8, 256>>>((uint4*)a, n, m); });
+    run("f32x4loc", [&] { f32x4_local<<<148 * 8, 256>>>((float*)a, n, m); });
     cudaFree(a);
   }
 }
