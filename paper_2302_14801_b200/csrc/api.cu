@@ -93,7 +93,7 @@ struct lod_tree {
   DevBuf leaf_pts, status, digit_base, tmp_rec, tmp_leaf, pkey, pc16;
   DevBuf vox, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vvchunks;
-  DevBuf vpos, vout, obits, opre;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
+  DevBuf vpos, vout, obits;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
   // pinned, device-mapped mirror of the device state (+ the per-depth counts): the build's
   // small device<->host exchanges are done by kernels over mapped memory, never by the copy
   // engines, so they do not queue behind bulk uploads / downloads of other streams (a
@@ -659,8 +659,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     if (fc) {
       CK(ensure(t->vpos, cap * 4, base_cursor * 4, s));
       CK(ensure(t->vout, cap * 8, base_cursor * 8, s));
-      CK(ensure(t->obits, ocap * 4));
-      CK(ensure(t->opre, ocap * 4));
+      CK(ensure(t->obits, ocap * 8));
       CK(ensure(t->scan, (ocap / kScanTile + 2) * 8));
     }
     const uint64_t chunk_cap = voxelize_chunk_capacity(t->n + cap, widest);
@@ -731,7 +730,6 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.vpos = t->vpos.as<uint32_t>();
     L.vout = t->vout.as<uint2>();
     L.obits = t->obits.as<uint32_t>();
-    L.opre = t->opre.as<uint32_t>();
     L.ocap = ocap;
     ScanScratch vscr{t->scan.as<uint64_t>(), t->scan.cap / 8};
     for (int d = kMaxDepth; d >= 0; --d) {  // deepest first (sampling.py:171)
@@ -932,7 +930,7 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->digit_base, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
                    &t->node_slot, &t->vacc, &t->vchunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
+                   &t->vpos, &t->vout, &t->obits, &t->pkey, &t->pc16};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -1122,7 +1120,7 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->vox, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
                          &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->opre, &t->pkey, &t->pc16};
+                   &t->vpos, &t->vout, &t->obits, &t->pkey, &t->pc16};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;

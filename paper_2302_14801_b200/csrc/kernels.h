@@ -181,9 +181,9 @@ struct VoxLevel {
   uint64_t acc_cap;        // voxels
   uint32_t* vpos;          // first-come: per voxel (arena index), stored position in its node
   uint2* vout;             // first-come: voxels in stored order (winning ordinal)
-  uint32_t* obits;         // first-come: per-level ordinal bitmaps (node runs at obase)
-  uint32_t* opre;          // first-come: exclusive popcount prefix of obits
-  uint64_t ocap;           // words of obits / opre
+  uint32_t* obits;         // first-come: per-level ordinal bitmaps (node runs at obase), packed
+                           // with their exclusive popcount prefix: [2 w] bits, [2 w + 1] prefix
+  uint64_t ocap;           // bitmap words of obits
   uint32_t chunk;          // samples per K1/K3 chunk
   uint32_t vchunk;         // voxels per K4 chunk
   int mode;

@@ -627,7 +627,7 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
     const uint32_t ord = ~__ldcg(a);
     rgb = winner_rgb(L, nd, ord);
     *a = ord;  // winning ordinal, ranked by K5 through the node's ordinal bitmap
-    atomicOr(L.obits + nd.obase + (ord >> 5), 1u << (ord & 31));
+    atomicOr(L.obits + 2 * (nd.obase + (ord >> 5)), 1u << (ord & 31));
   }
   L.vox[nd.vbase + r].y = rgb;
 }
@@ -650,13 +650,12 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
 // ---------------------------------------------------------------------------
 // K5 (first-come): stored order = ascending winning ordinal (sampling.py:64-66)
 // ---------------------------------------------------------------------------
-struct OrdScanF {  // exclusive popcount prefix over the level's ordinal bitmaps
-  const uint32_t* bits;
-  uint32_t* pre;
+struct OrdScanF {  // exclusive popcount prefix over the level's ordinal bitmaps (packed pairs)
+  uint32_t* bp;
   const uint32_t* live;  // words in use this level (K2's allocation)
   __device__ uint64_t limit(uint64_t n) const { return min(n, (uint64_t)__ldcg(live)); }
-  __device__ uint64_t value(uint64_t i) const { return __popc(__ldcg(bits + i)); }
-  __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { pre[i] = (uint32_t)excl; }
+  __device__ uint64_t value(uint64_t i) const { return __popc(__ldcg(bp + 2 * i)); }
+  __device__ void store(uint64_t i, uint64_t excl, uint64_t) const { bp[2 * i + 1] = (uint32_t)excl; }
 };
 
 __global__ void __launch_bounds__(kT) k_fc_pos(VoxLevel L) {
@@ -668,11 +667,11 @@ __global__ void __launch_bounds__(kT) k_fc_pos(VoxLevel L) {
     const VoxNode& nd = L.info[ch.x];
     const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
     const uint64_t acc0 = nd.vbase - L.level_start[0];
-    const uint32_t p0 = __ldcg(L.opre + nd.obase);
+    const uint32_t p0 = __ldcg(L.obits + 2 * nd.obase + 1);
     for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
       const uint32_t ord = __ldcg(reinterpret_cast<const uint32_t*>(L.acc) + acc0 + r);
-      const uint64_t w = nd.obase + (ord >> 5);
-      const uint32_t p = __ldcg(L.opre + w) - p0 + __popc(__ldcg(L.obits + w) & ((1u << (ord & 31)) - 1));
+      const uint2 e = __ldcg(reinterpret_cast<const uint2*>(L.obits) + nd.obase + (ord >> 5));  // {bits, prefix}
+      const uint32_t p = e.y - p0 + __popc(e.x & ((1u << (ord & 31)) - 1));
       L.vpos[nd.vbase + r] = p;
       L.vout[nd.vbase + p] = L.vox[nd.vbase + r];
     }
@@ -818,10 +817,10 @@ int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStre
     launch_pdl(k_scatter_w, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
   else
     launch_pdl(k_scatter, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
-  if (L.mode == LOD_MODE_FIRST_COME) cudaMemsetAsync(L.obits, 0, L.ocap * 4, s);  // K4 marks winners
+  if (L.mode == LOD_MODE_FIRST_COME) cudaMemsetAsync(L.obits, 0, L.ocap * 8, s);  // K4 marks winners
   launch_pdl(k_finalize, grid, kT, 0, s, L);
   if (L.mode == LOD_MODE_FIRST_COME) {
-    const int r = device_scan(L.ocap, OrdScanF{L.obits, L.opre, L.counters + 4}, scr, nullptr, nullptr, s);
+    const int r = device_scan(L.ocap, OrdScanF{L.obits, L.counters + 4}, scr, nullptr, nullptr, s);
     if (r < 0) return r;
     launch_pdl(k_fc_pos, grid, kT, 0, s, L);
     launches += 1 + r;
