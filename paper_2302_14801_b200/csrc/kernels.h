@@ -170,7 +170,8 @@ struct VoxLevel {
   uint32_t* pre;           // [2][slots][2^16] exclusive popcount prefix per word
   VoxNode* info;           // this level's infos (parity slice)
   uint32_t* blk_sum;       // [list_n * 16]
-  uint32_t* counters;      // [0] sample chunks, [2] voxel chunks
+  uint32_t* counters;      // [0] sample chunks, [2] voxel chunks, [4] first-come ordinal words,
+                           // [6] K2 blocks done
   uint4* chunks;
   uint2* vchunks;
   uint64_t* level_start;   // arena cursor at the start of this level

@@ -249,37 +249,10 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// K2: popcount sums per 4096-word block, node offsets, word prefixes
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kT) k_block_sums(VoxLevel L) {
-  pdl_wait();
-  const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
-  __shared__ uint32_t red[kT / 32];
-  uint32_t c = 0;
-  if (!L.info[s].skip && !(L.st->err & ERR_ARENA)) {
-    const uint4* b = reinterpret_cast<const uint4*>(bits_of(L, L.parity, s) + blk * kBlkWords);
-    for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT) {
-      uint4 q = __ldcg(b + i);
-      c += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-    for (int w = 0; w < kT / 32; ++w) t += red[w];
-    L.blk_sum[blockIdx.x] = t;
-  }
-}
-
-// one block: per-node voxel counts -> arena offsets (bump pointer), K4 voxel chunks
-__global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
-  pdl_wait();
+template <int NT>
+__device__ void alloc_level(const VoxLevel& L) {
   if (L.st->err & ERR_ARENA) return;
-  __shared__ uint64_t sm[1024 / 32 + 1];
+  __shared__ uint64_t sm[NT / 32 + 1];
   __shared__ uint64_t carry, ocarry;
   if (threadIdx.x == 0) {
     ocarry = 0;
@@ -287,24 +260,24 @@ __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
     L.level_start[0] = carry;
   }
   __syncthreads();
-  for (uint32_t s0 = 0; s0 < L.list_n; s0 += 1024) {
+  for (uint32_t s0 = 0; s0 < L.list_n; s0 += NT) {
     const uint32_t s = s0 + threadIdx.x;
     uint32_t m = 0;
     if (s < L.list_n) {
       uint32_t run = 0;
       for (uint32_t b = 0; b < kBlksPerNode; ++b) {
-        uint32_t v = L.blk_sum[s * kBlksPerNode + b];
+        uint32_t v = __ldcg(L.blk_sum + s * kBlksPerNode + b);
         L.blk_sum[s * kBlksPerNode + b] = run;  // becomes the block's exclusive prefix
         run += v;
       }
       m = run;
     }
     uint64_t tot;
-    uint64_t ex = block_excl_scan<uint64_t, 1024>(m, &tot, sm);
+    uint64_t ex = block_excl_scan<uint64_t, NT>(m, &tot, sm);
     uint64_t ow = 0;  // first-come: words of the node's ordinal bitmap
     if (s < L.list_n && L.mode == LOD_MODE_FIRST_COME && !L.info[s].skip) ow = (L.info[s].S + 31) / 32;
     uint64_t otot;
-    uint64_t oex = block_excl_scan<uint64_t, 1024>(ow, &otot, sm);
+    uint64_t oex = block_excl_scan<uint64_t, NT>(ow, &otot, sm);
     if (s < L.list_n) {
       VoxNode& nd = L.info[s];
       nd.obase = ocarry + oex;
@@ -329,6 +302,42 @@ __global__ void __launch_bounds__(1024) k_alloc(VoxLevel L) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2: popcount sums per 4096-word block, node offsets, word prefixes
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kT) k_block_sums(VoxLevel L) {
+  pdl_wait();
+  const uint32_t s = blockIdx.x / kBlksPerNode, blk = blockIdx.x % kBlksPerNode;
+  __shared__ uint32_t red[kT / 32];
+  uint32_t c = 0;
+  if (!L.info[s].skip && !(L.st->err & ERR_ARENA)) {
+    const uint4* b = reinterpret_cast<const uint4*>(bits_of(L, L.parity, s) + blk * kBlkWords);
+    for (uint32_t i = threadIdx.x; i < kBlkWords / 4; i += kT) {
+      uint4 q = __ldcg(b + i);
+      c += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kT / 32; ++w) t += red[w];
+    L.blk_sum[blockIdx.x] = t;
+    __threadfence();
+    last = atomicAdd(L.counters + 6, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    alloc_level<kT>(L);
+  }
+}
+
+// one block: per-node voxel counts -> arena offsets (bump pointer), K4 voxel chunks.  Run by
+// the last K2 block to finish (no launch of its own).
 // Stage one 4096-word block of a node's bitmap in shared memory and compute every word's
 // exclusive popcount prefix (= voxel rank of its first set bit) into spre; returns the
 // block's voxel count.
@@ -794,18 +803,17 @@ int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s
   return 6;
 }
 
-// Runs one depth level; returns launches.  counters[0..2] must be zero on entry and the
+// Runs one depth level; returns launches.  counters[0..6] must be zero on entry and the
 // level's bitmaps cleared.
 int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s) {
   const int grid = sms * 8;
-  int launches = 7;
+  int launches = 6;
   launch_pdl(k_setup, ceil_div_u32(8ull * L.list_n, kT), kT, 0, s, L);
   if (L.fmt == LOD_POINTS_F32)
     launch_pdl(k_occupy<LOD_POINTS_F32>, sms * 2, kRT, 0, s, L);
   else
     launch_pdl(k_occupy<LOD_POINTS_F64>, sms * 2, kRT, 0, s, L);
-  launch_pdl(k_block_sums, L.list_n * kBlksPerNode, kT, 0, s, L);
-  launch_pdl(k_alloc, 1, 1024, 0, s, L);
+  launch_pdl(k_block_sums, L.list_n * kBlksPerNode, kT, 0, s, L);  // + the arena allocation (last block)
   launch_pdl(k_prefix, L.list_n * kBlksPerNode, kT, 0, s, L);
   static bool configured = false;
   if (!configured) {
