@@ -385,7 +385,7 @@ def main():
     whole_bytes = 80 * n + 12 * V
     traffic = measured_traffic(args.config, args.mode, n, "k_dist_scatter") if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"k_dist_scatter (distribute.cu), {passes} pass(es)",
+                "traffic": traffic, "kernel": f"K_scatter (distribute.cu: k_dist_scatter_staged for f32 records), {passes} pass(es)",
                 "algorithmic_bytes": kern_bytes, "ms_per_build": scatter_ms, "peak_source": peak_kind,
                 "stages": {nm: {"ms": st, "algorithmic_bytes": b,
                                 "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st > 0 else None,
