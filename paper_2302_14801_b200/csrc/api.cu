@@ -85,6 +85,8 @@ struct lod_tree {
   bool timing = false;
   cudaEvent_t ev[6] = {};
   cudaEvent_t kev[4] = {};  // the distribute's K_scatter, per pass (the dominant single kernel)
+  cudaStream_t vback = nullptr;        // voxelize: K4/K5 of level L overlap level L+1's front half
+  cudaEvent_t vev[3] = {};             // fork, accumulated (K3 done), finalized (K4/K5 done)
   float stage_ms[5] = {};
 
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
@@ -647,13 +649,13 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
   const uint32_t acc_stride = voxelize_acc_bytes(mode);
   const bool fc = mode == LOD_MODE_FIRST_COME;
   uint64_t acc_cap = std::max<uint64_t>(t->n <= (1ull << 27) ? t->n / 2 : t->n / 4, 1ull << 21);
-  if (t->vacc.cap / acc_stride > acc_cap) acc_cap = t->vacc.cap / acc_stride;
+  if (t->vacc.cap / (2 * acc_stride) > acc_cap) acc_cap = t->vacc.cap / (2 * acc_stride);
   bool exact_sums = false;
   for (int attempt = 0; attempt < 8; ++attempt) {
     CK(ensure(t->vox, cap * 8, base_cursor * 8, s));
     cap = t->vox.cap / 8;
-    CK(ensure(t->vacc, acc_cap * acc_stride));
-    acc_cap = t->vacc.cap / acc_stride;
+    CK(ensure(t->vacc, 2 * acc_cap * acc_stride));  // two depth parities (launch_voxelize_back)
+    acc_cap = t->vacc.cap / (2 * acc_stride) & ~3ull;  // each parity half 16-B aligned
     // first-come: a level samples at most every leaf point once plus every child voxel
     const uint64_t ocap = fc ? (t->n + cap) / 32 + 2ull * widest + 64 : 0;
     if (fc) {
@@ -665,7 +667,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     const uint64_t chunk_cap = voxelize_chunk_capacity(t->n + cap, widest);
     const uint64_t vchunk_cap = voxelize_vchunk_capacity(cap, widest);
     CK(ensure(t->vchunks, chunk_cap * 16));
-    CK(ensure(t->vvchunks, vchunk_cap * 8));
+    CK(ensure(t->vvchunks, 2 * vchunk_cap * 8));
     if (!(split_errors_pending && attempt == 0))  // else the split's device checks report with ours
       CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
                          sizeof(DevState) - offsetof(DevState, err), s));
@@ -719,10 +721,8 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.pre = t->vpre.as<uint32_t>();
     L.blk_sum = t->vblk.as<uint32_t>();
     L.chunks = t->vchunks.as<uint4>();
-    L.vchunks = t->vvchunks.as<uint2>();
     L.vox = t->vox.as<uint2>();
     L.vox_cap = cap;
-    L.acc = t->vacc.as<uint64_t>();
     L.acc_cap = acc_cap;
     L.mode = mode;
     L.exact_sums = exact_sums ? 1 : 0;
@@ -732,12 +732,19 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.obits = t->obits.as<uint32_t>();
     L.ocap = ocap;
     ScanScratch vscr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+    const uint64_t vchunk_half = t->vvchunks.cap / 16;
+    // K4/K5 of each level run on t->vback, overlapping the next level up to its K3
+    CK(cudaEventRecord(t->vev[0], s));
+    CK(cudaStreamWaitEvent(t->vback, t->vev[0], 0));
+    bool back_pending = false;
     for (int d = kMaxDepth; d >= 0; --d) {  // deepest first (sampling.py:171)
       if (!lst_n[d] && !imp_n[d]) continue;
       L.parity = d & 1;
       L.info = t->vinfo.as<VoxNode>() + (size_t)L.parity * widest;
       L.counters = t->vcount.as<uint32_t>() + 64 * d;
       L.level_start = t->vlevel_start.as<uint64_t>() + d;
+      L.acc = reinterpret_cast<uint64_t*>(t->vacc.as<char>() + (size_t)L.parity * acc_cap * acc_stride);
+      L.vchunks = t->vvchunks.as<uint2>() + (size_t)L.parity * vchunk_half;
       if (lst_n[d]) {
         L.list = d_lists + lst_off[d];
         L.list_n = lst_n[d];
@@ -745,9 +752,17 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         L.vchunk = voxelize_vchunk(L.list_n);
         CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
                            (size_t)L.list_n * kWordsPerNode * 4, s));
-        RUN(launch_voxelize_level(L, sms, vscr, s));
+        RUN(launch_voxelize_front(L, sms, s));
+        if (back_pending) CK(cudaStreamWaitEvent(s, t->vev[2], 0));  // the children's colours
+        RUN(launch_voxelize_accumulate(L, sms, s));
+        CK(cudaEventRecord(t->vev[1], s));
+        CK(cudaStreamWaitEvent(t->vback, t->vev[1], 0));
+        RUN(launch_voxelize_back(L, sms, vscr, t->vback));
+        CK(cudaEventRecord(t->vev[2], t->vback));
+        back_pending = true;
       }
       if (imp_n[d]) {
+        if (back_pending) CK(cudaStreamWaitEvent(s, t->vev[2], 0));
         L.list = d_imp + imp_off[d];
         L.list_n = imp_n[d];
         CK(cudaMemsetAsync(L.bits + ((size_t)L.parity * widest + plan->imp_slot_base) * kWordsPerNode, 0,
@@ -755,6 +770,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         RUN(launch_voxelize_import(L, plan->imp_slot_base, s));
       }
     }
+    if (back_pending) CK(cudaStreamWaitEvent(s, t->vev[2], 0));
     int r = read_state(t, s);
     if (r) return r;
     CK(cudaGetLastError());
@@ -917,6 +933,8 @@ lod_tree* lod_tree_create(int device) {
   t->host_depth_dev = reinterpret_cast<uint32_t*>(static_cast<char*>(hm_dev) + depth_at);
   for (auto& e : t->ev) cudaEventCreate(&e);
   for (auto& e : t->kev) cudaEventCreate(&e);
+  for (auto& e : t->vev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&t->vback, cudaStreamNonBlocking);
   return t;
 }
 
@@ -937,6 +955,9 @@ void lod_tree_destroy(lod_tree* t) {
     if (e) cudaEventDestroy(e);
   for (auto& e : t->kev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : t->vev)
+    if (e) cudaEventDestroy(e);
+  if (t->vback) cudaStreamDestroy(t->vback);
   if (t->host_state) cudaFreeHost(t->host_state);
   delete t;
 }

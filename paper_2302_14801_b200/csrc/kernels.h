@@ -191,7 +191,9 @@ struct VoxLevel {
   int exact_sums;          // average: u64 sums (fallback) instead of f32 vector reductions
   uint64_t seed;
 };
-int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s);
+int launch_voxelize_front(const VoxLevel& L, int sms, cudaStream_t s);
+int launch_voxelize_accumulate(const VoxLevel& L, int sms, cudaStream_t s);
+int launch_voxelize_back(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s);
 uint32_t voxelize_acc_bytes(int mode);
 int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s);
 uint32_t voxelize_chunk(uint32_t nodes);

@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kT) k_prefix(VoxLevel L) {
     while (bw) {
       const uint32_t bit = __ffs(bw) - 1;
       bw &= bw - 1;
-      L.vox[nd.vbase + rr++].x = key0 + bit;
+      L.vox[nd.vbase + rr++] = make_uint2(key0 + bit, 0u);  // whole records: full sectors
     }
   }
   const uint64_t a0 = nd.vbase - L.level_start[0] + L.blk_sum[blockIdx.x];
@@ -612,10 +612,9 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
       const double m = floor(__dadd_rn(__ddiv_rn((double)__ldcg(a + 1 + k), W), 0.5));
       rgb |= (uint32_t)fmin(fmax(m, 0.0), 255.0) << (8 * k);
     }
-    L.vox[nd.vbase + r].y = rgb;
+    L.vox[nd.vbase + r] = make_uint2(key, rgb);
     return;
   }
-  (void)key;
   uint64_t sr = 0, sg = 0, sb = 0, n = 0;
   uint32_t rgb;
   if (L.mode == LOD_MODE_AVERAGE) {
@@ -638,7 +637,7 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
     *a = ord;  // winning ordinal, ranked by K5 through the node's ordinal bitmap
     atomicOr(L.obits + 2 * (nd.obase + (ord >> 5)), 1u << (ord & 31));
   }
-  L.vox[nd.vbase + r].y = rgb;
+  L.vox[nd.vbase + r] = make_uint2(key, rgb);  // the whole record: no half-written sectors
 }
 
 // K4: finalize every voxel of the level, one thread per voxel (rank chunks): a word-walk
@@ -803,11 +802,13 @@ int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s
   return 6;
 }
 
-// Runs one depth level; returns launches.  counters[0..6] must be zero on entry and the
-// level's bitmaps cleared.
-int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s) {
-  const int grid = sms * 8;
-  int launches = 6;
+// One depth level in two halves.  front (stream s): setup, occupancy, allocation, rank
+// structures, accumulation -- counters[0..6] must be zero on entry and the level's bitmaps
+// cleared, and the child level's colours must be final before K3 (the caller orders it).
+// back (its own stream): K4 finalize (+ first-come K5).  The back half of level L overlaps the
+// front half of level L+1 up to its K3: the accumulators and K4 chunk lists alternate by depth
+// parity, every other buffer they share is written by one and not read by the other.
+int launch_voxelize_front(const VoxLevel& L, int sms, cudaStream_t s) {
   launch_pdl(k_setup, ceil_div_u32(8ull * L.list_n, kT), kT, 0, s, L);
   if (L.fmt == LOD_POINTS_F32)
     launch_pdl(k_occupy<LOD_POINTS_F32>, sms * 2, kRT, 0, s, L);
@@ -815,6 +816,10 @@ int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStre
     launch_pdl(k_occupy<LOD_POINTS_F64>, sms * 2, kRT, 0, s, L);
   launch_pdl(k_block_sums, L.list_n * kBlksPerNode, kT, 0, s, L);  // + the arena allocation (last block)
   launch_pdl(k_prefix, L.list_n * kBlksPerNode, kT, 0, s, L);
+  return 4;
+}
+
+int launch_voxelize_accumulate(const VoxLevel& L, int sms, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);
@@ -825,6 +830,12 @@ int launch_voxelize_level(const VoxLevel& L, int sms, ScanScratch& scr, cudaStre
     launch_pdl(k_scatter_w, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
   else
     launch_pdl(k_scatter, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
+  return 1;
+}
+
+int launch_voxelize_back(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s) {
+  const int grid = sms * 8;
+  int launches = 1;
   if (L.mode == LOD_MODE_FIRST_COME) cudaMemsetAsync(L.obits, 0, L.ocap * 8, s);  // K4 marks winners
   launch_pdl(k_finalize, grid, kT, 0, s, L);
   if (L.mode == LOD_MODE_FIRST_COME) {
