@@ -332,7 +332,9 @@ __host__ __device__ constexpr size_t staged_region(int B) {  // count rows / rec
 }
 __host__ __device__ constexpr size_t staged_smem(int B) { return staged_region(B) + (size_t)kRadixTile * 4 + (size_t)B * 8; }
 
-template <bool TAGOUT, int NB>
+// TAGIN (2nd pass): the digit is the record's pad byte, read as the record's last word (the
+// sectors stay in L2 for the record loads after the ranking); the pad is cleared on output.
+template <bool TAGIN, bool TAGOUT, int NB>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_dist_scatter_staged(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, int bits,
                           int tag_shift, const uint32_t* firsts) {
@@ -356,7 +358,10 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   const uint64_t last = v.n - 1;
   uint32_t leaf[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) leaf[k] = __ldcs(in_leaf + min(base + (uint64_t)k * 32 + lane, last));
+  for (int k = 0; k < K; ++k) {
+    const uint64_t i = min(base + (uint64_t)k * 32 + lane, last);
+    leaf[k] = TAGIN ? __ldg(reinterpret_cast<const uint32_t*>(in_rec) + 4 * i + 3) >> 24 : __ldcs(in_leaf + i);
+  }
   __syncthreads();
   // stable in-warp ranks (item-major, lane order)
   const uint32_t lt_mask = (1u << lane) - 1;
@@ -432,6 +437,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     for (int u = 0; u < G; ++u) {
       if (base + (uint64_t)(g + u) * 32 + lane < v.n) {
         if (TAGOUT) r[u].w = (r[u].w & 0xFFFFFFu) | ((leaf[g + u] >> tag_shift) << 24);  // the next pass's digit
+        if (TAGIN) r[u].w &= 0xFFFFFFu;
         srec[rk[g + u]] = r[u];
       }
     }
@@ -485,10 +491,11 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   const int nscan = launch_dist_scan(p.counts, p.segs, B, digit_base, p.scan_part, s);
   const cudaEvent_t* ev = p.scatter_ev + (FIRST ? 0 : 2);
   if (ev[0]) cudaEventRecord(ev[0], s);
-  constexpr bool kStaged = FMT == LOD_POINTS_F32 && FIRST && !TAGIN && OUT != OUT_LEAF;
-  if (kStaged && p.seg_tiles == 1) {  // digit = leaf id (shift 0): staged, coalesced stores
-    auto st6 = k_dist_scatter_staged<OUT == OUT_TAG, 6>;
-    auto st11 = k_dist_scatter_staged<OUT == OUT_TAG, kRadixMaxBits>;
+  // staged, coalesced stores whenever the digit starts at bit 0 (pass 1: leaf id; pass 2: pad)
+  constexpr bool kStaged = FMT == LOD_POINTS_F32 && (FIRST || TAGIN) && OUT != OUT_LEAF;
+  if (kStaged && p.seg_tiles == 1 && shift == 0) {
+    auto st6 = k_dist_scatter_staged<TAGIN, OUT == OUT_TAG, 6>;
+    auto st11 = k_dist_scatter_staged<TAGIN, OUT == OUT_TAG, kRadixMaxBits>;
     static bool staged_cfg = false;
     if (!staged_cfg) {
       cudaFuncSetAttribute(st6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)staged_smem(1 << 6));
