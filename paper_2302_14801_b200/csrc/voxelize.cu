@@ -381,16 +381,20 @@ __global__ void __launch_bounds__(kT) k_prefix(VoxLevel L) {
     const uint4 b4 = reinterpret_cast<const uint4*>(sbits)[i];
     if (b4.x | b4.y | b4.z | b4.w) reinterpret_cast<uint4*>(pre)[i] = reinterpret_cast<const uint4*>(spre)[i];
   }
-  // voxel keys in rank order (K4 reads them back voxel-parallel)
-  for (uint32_t wi = threadIdx.x; wi < kBlkWords; wi += kT) {
-    uint32_t bw = sbits[wi];
-    uint32_t rr = spre[wi];
-    const uint32_t key0 = (blk * kBlkWords + wi) << 5;
-    while (bw) {
-      const uint32_t bit = __ffs(bw) - 1;
-      bw &= bw - 1;
-      L.vox[nd.vbase + rr++] = make_uint2(key0 + bit, 0u);  // whole records: full sectors
+  // voxel keys in rank order (K4 reads them back voxel-parallel), one thread per voxel so the
+  // records are written coalesced: the voxel's word by binary search over the word prefixes
+  // (the last word whose prefix <= rank holds it), its bit by select-in-word
+  const uint32_t r0 = spre[0];
+  for (uint32_t i = threadIdx.x; i < tot; i += kT) {
+    const uint32_t r = r0 + i;
+    uint32_t lo = 0, hi = kBlkWords - 1;
+#pragma unroll
+    for (int step = 0; step < 12; ++step) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (spre[mid] <= r) lo = mid; else hi = mid - 1;
     }
+    const uint32_t bit = __fns(sbits[lo], 0, (int)(r - spre[lo]) + 1);
+    L.vox[nd.vbase + r] = make_uint2(((blk * kBlkWords + lo) << 5) + bit, 0u);
   }
   const uint64_t a0 = nd.vbase - L.level_start[0] + L.blk_sum[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < tot; i += kT) {
