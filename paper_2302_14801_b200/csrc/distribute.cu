@@ -337,7 +337,7 @@ __host__ __device__ constexpr size_t staged_smem(int B) { return staged_region(B
 template <bool TAGIN, bool TAGOUT, int NB>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_dist_scatter_staged(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, int bits,
-                          int tag_shift, const uint32_t* firsts, const uint64_t* digit_base) {
+                          int tag_shift, const uint32_t* firsts) {
   pdl_wait();
   extern __shared__ __align__(16) uint32_t sm[];
   const int B = 1 << bits;
@@ -349,6 +349,11 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   uint16_t* wh16 = reinterpret_cast<uint16_t*>(wh);
   const uint32_t tile = gridDim.x - 1 - blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const uint32_t n4 = (uint32_t)(((size_t)B * kRowWords + 3) / 4);
+    for (uint32_t i = threadIdx.x; i < n4; i += kRadixThreads) reinterpret_cast<uint4*>(wh)[i] = make_uint4(0, 0, 0, 0);
+    for (int d = threadIdx.x; d < B; d += kRadixThreads) run[d] = __ldcs(firsts + (uint64_t)tile * B + d);
+  }
   const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
   const uint64_t last = v.n - 1;
   uint32_t leaf[K];
@@ -356,38 +361,6 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   for (int k = 0; k < K; ++k) {
     const uint64_t i = min(base + (uint64_t)k * 32 + lane, last);
     leaf[k] = TAGIN ? __ldg(reinterpret_cast<const uint32_t*>(in_rec) + 4 * i + 3) >> 24 : __ldcs(in_leaf + i);
-  }
-  {
-    const uint32_t n4 = (uint32_t)(((size_t)B * kRowWords + 3) / 4);
-    for (uint32_t i = threadIdx.x; i < n4; i += kRadixThreads) reinterpret_cast<uint4*>(wh)[i] = make_uint4(0, 0, 0, 0);
-    // the tile's first slot per digit, and its count = the next tile's first slot - this one
-    // (the digit's end for the last tile): tile-local first slots by one block scan, while
-    // the digit loads are in flight (consecutive digits per thread)
-    __shared__ uint32_t wsum[kW + 1];
-    const int per = (B + kRadixThreads - 1) / kRadixThreads;
-    const int d0 = threadIdx.x * per;
-    uint32_t cnt[(1 << kRadixMaxBits) / kRadixThreads], c = 0;
-#pragma unroll
-    for (int j = 0; j < (1 << kRadixMaxBits) / kRadixThreads; ++j) {
-      cnt[j] = 0;
-      const int d = d0 + j;
-      if (j < per && d < B) {
-        const uint32_t f = __ldcs(firsts + (uint64_t)tile * B + d);
-        const uint32_t e = tile + 1 < gridDim.x ? __ldcs(firsts + (uint64_t)(tile + 1) * B + d)
-                                                : (uint32_t)(d + 1 < B ? digit_base[d + 1] : v.n);
-        run[d] = f;
-        cnt[j] = e - f;
-        c += cnt[j];
-      }
-    }
-    uint32_t tot;
-    uint32_t x = block_excl_scan<uint32_t, kRadixThreads>(c, &tot, wsum);
-#pragma unroll
-    for (int j = 0; j < (1 << kRadixMaxBits) / kRadixThreads; ++j)
-      if (j < per && d0 + j < B) {
-        tf[d0 + j] = x;
-        x += cnt[j];
-      }
   }
   __syncthreads();
   // stable in-warp ranks (item-major, lane order)
@@ -415,7 +388,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive prefix over the warps in warp order
+  // per digit: exclusive prefix over the warps in warp order; the row total -> tf
   for (int d = threadIdx.x; d < B; d += kRadixThreads) {
     uint32_t* row = wh + (size_t)d * kRowWords;
     uint32_t r = 0;
@@ -425,6 +398,23 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
       row[q] = r | ((r + lo) << 16);
       r += lo + (c >> 16);
     }
+    tf[d] = r;
+  }
+  __syncthreads();
+  {  // tile-local first slot per digit: exclusive scan of the totals (consecutive digits per thread)
+    __shared__ uint32_t wsum[kW + 1];
+    const int per = (B + kRadixThreads - 1) / kRadixThreads;
+    const int d0 = threadIdx.x * per;
+    uint32_t c = 0;
+    for (int j = 0; j < per; ++j) c += d0 + j < B ? tf[d0 + j] : 0;
+    uint32_t tot;
+    uint32_t x = block_excl_scan<uint32_t, kRadixThreads>(c, &tot, wsum);
+    for (int j = 0; j < per; ++j)
+      if (d0 + j < B) {
+        const uint32_t t = tf[d0 + j];
+        tf[d0 + j] = x;
+        x += t;
+      }
   }
   __syncthreads();
 #pragma unroll
@@ -513,7 +503,7 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
       staged_cfg = true;
     }
     launch_pdl(bits <= 6 ? st6 : st11, p.segs, kRadixThreads, staged_smem(B), s, v, in_rec, leaf_in, out_rec, bits,
-               tag_shift, p.counts, digit_base);
+               tag_shift, p.counts);
   } else {
     launch_pdl(scat, p.segs, kRadixThreads, ssm, s, v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,
                p.seg_tiles, p.tiles, p.counts);
