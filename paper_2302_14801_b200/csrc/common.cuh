@@ -12,6 +12,9 @@
 // c16 = min(floor(q * 65536), 65535), so each point is projected once per pass.
 #pragma once
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/lodb200.h"
@@ -306,9 +309,25 @@ __device__ __forceinline__ uint32_t ld_hint(const uint32_t* a, uint64_t pol) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// More than 48 KB of dynamic shared memory is an opt-in per kernel AND per device: remembered
+// per (device, kernel) so a process driving several GPUs sets it on each.
+inline void allow_dynamic_smem(const void* kernel, size_t bytes) {
+  if (bytes <= 48u * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  size_t& cur = done[{dev, kernel}];
+  if (cur >= bytes) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  cur = bytes;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {
+  allow_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -479,13 +479,6 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   auto hist = k_dist_hist<FMT, FIRST, TAGIN>;
   auto scat = k_dist_scatter<FMT, TAGIN, OUT>;
   const size_t hsm = (size_t)B * 4, ssm = (size_t)B * 8 + (size_t)kW * B * 2 + 4 * kW;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((4u << kRadixMaxBits)));
-    cudaFuncSetAttribute(scat, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((8u << kRadixMaxBits) + (size_t)kW * (2u << kRadixMaxBits) + 4 * kW));
-    configured = true;
-  }
   const uint32_t* leaf_in = FIRST ? leaf_tmp : in_leaf;
   launch_pdl(hist, p.segs, kRadixThreads, hsm, s, v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
   const int nscan = launch_dist_scan(p.counts, p.segs, B, digit_base, p.scan_part, s);
@@ -496,12 +489,6 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   if (kStaged && p.seg_tiles == 1 && shift == 0) {
     auto st6 = k_dist_scatter_staged<TAGIN, OUT == OUT_TAG, 6>;
     auto st11 = k_dist_scatter_staged<TAGIN, OUT == OUT_TAG, kRadixMaxBits>;
-    static bool staged_cfg = false;
-    if (!staged_cfg) {
-      cudaFuncSetAttribute(st6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)staged_smem(1 << 6));
-      cudaFuncSetAttribute(st11, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)staged_smem(1 << kRadixMaxBits));
-      staged_cfg = true;
-    }
     launch_pdl(bits <= 6 ? st6 : st11, p.segs, kRadixThreads, staged_smem(B), s, v, in_rec, leaf_in, out_rec, bits,
                tag_shift, p.counts);
   } else {

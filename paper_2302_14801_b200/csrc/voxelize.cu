@@ -824,12 +824,6 @@ int launch_voxelize_front(const VoxLevel& L, int sms, cudaStream_t s) {
 }
 
 int launch_voxelize_accumulate(const VoxLevel& L, int sms, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);
-    cudaFuncSetAttribute(k_scatter_w, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kRegionWords * 4);
-    configured = true;
-  }
   if (L.mode == LOD_MODE_WEIGHTED)
     launch_pdl(k_scatter_w, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
   else
