@@ -11,8 +11,10 @@
 //             scatter), digit histogram in shared memory -> counts[chunk][B]
 //   K_scan    per digit: exclusive prefix over chunks + the digit's global base (known
 //             from the leaf counts of the pyramid) -> first slot of every (chunk, digit)
-//   K_scatter per chunk, its sub-tiles in order: stable in-sub-tile ranks (warp-major,
-//             item-major, lane = input order), records re-read (L1/L2) and stored.
+//   K_scatter per tile: stable in-tile ranks (warp-major, item-major, lane = input order);
+//             f32 records are then permuted in shared memory into destination order and
+//             stored by consecutive threads (k_dist_scatter_staged: each leaf's run leaves
+//             as full sectors), f64 / leaf-id-array passes store directly (k_dist_scatter).
 // Scatter CTAs take the chunks in REVERSE order: the last chunks K_hist read may still be
 // in L2.  Concurrent CTAs hold adjacent chunks, so every leaf has ONE contiguous write
 // front and L2 merges the 16-B records into full sectors before they reach HBM (per-
