@@ -561,22 +561,19 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter_w(VoxLevel L) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint32_t cx = base[0] + (q >> 2), cy = base[1] + ((q >> 1) & 1), cz = base[2] + (q & 1);
-        const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(wdist_axis(g[0], cx), wdist_axis(g[1], cy)),
-                                              wdist_axis(g[2], cz)));
-        const double w = __dsub_rn(1.0, d);
-        if (!(w > 0.0)) continue;
+        // the cheap tests first, each exact: occupancy (sampling.py:125-128), then the squared
+        // distance (sqrt(s) >= 1 for s >= 1, so w = 1 - RN(sqrt(s)) <= 0 there), then w itself
         const uint32_t key = (cx << 14) | (cy << 7) | cz;
         const uint32_t bit = 1u << (key & 31);
         uint32_t lw, word, rank;
-        if (region_word(key, o, lw)) {
-          word = rbits[lw];
-          if (!(word & bit)) continue;  // only occupied cells emit (sampling.py:125-128)
-          rank = rpre[lw] + __popc(word & (bit - 1));
-        } else {
-          word = __ldcg(bits + (key >> 5));
-          if (!(word & bit)) continue;
-          rank = __ldcg(pre + (key >> 5)) + __popc(word & (bit - 1));
-        }
+        const bool local = region_word(key, o, lw);
+        word = local ? rbits[lw] : __ldcg(bits + (key >> 5));
+        if (!(word & bit)) continue;
+        const double s2 = __dadd_rn(__dadd_rn(wdist_axis(g[0], cx), wdist_axis(g[1], cy)), wdist_axis(g[2], cz));
+        if (s2 >= 1.0) continue;
+        const double w = __dsub_rn(1.0, __dsqrt_rn(s2));
+        if (!(w > 0.0)) continue;
+        rank = (local ? rpre[lw] : __ldcg(pre + (key >> 5))) + __popc(word & (bit - 1));
         unsigned long long* acc = reinterpret_cast<unsigned long long*>(L.acc) + 4 * (acc0 + rank);
         atomicAdd(acc, (unsigned long long)__double2ll_rn(__dmul_rn(w, kWScale)));
 #pragma unroll
