@@ -97,7 +97,10 @@ typedef struct lod_node {
 
 typedef struct lod_tree lod_tree;
 
-/* Handle lifecycle.  `device` is the CUDA ordinal the tree's buffers live on. */
+/* Handle lifecycle.  `device` is the CUDA ordinal the tree's buffers live on.  Calls on one
+ * tree must not overlap; different trees may build concurrently on different streams (a tree
+ * owns a private stream for its voxelize overlap and a small pinned, device-mapped status
+ * block, so its host reads never wait behind other streams' bulk copies). */
 lod_tree* lod_tree_create(int device);
 void lod_tree_destroy(lod_tree* tree);
 
