@@ -697,7 +697,10 @@ int launch_leaf_offsets_local(const SplitView& v, ScanScratch& scr, cudaStream_t
 // UNMERGEABLE cell owns nothing, an empty cell inherits its parent's owner.  The result is
 // written in place over node_idx (level l reads level l-1's finished targets); the finest
 // level goes to t8, where extension anchors keep their -(ext+2) pointer.
-__device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t c, uint32_t val) {
+// ptarget: the parent cell's target when the caller already has it (k_target_level), else
+// INT32_MIN and it is loaded here
+__device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t c, uint32_t val,
+                                            int32_t ptarget = INT32_MIN) {
   const uint64_t s = level_off(l) + c;
   int32_t t;
   if (val == UNMERGEABLE) {
@@ -706,6 +709,8 @@ __device__ __forceinline__ void target_cell(const SplitView& v, int l, uint64_t 
     t = v.n_leaf[v.node_idx[s]];
   } else if (l == 0) {
     t = -1;
+  } else if (ptarget != INT32_MIN) {
+    t = ptarget;
   } else {
     const uint32_t msk = (1u << l) - 1;
     uint32_t x = (uint32_t)(c >> (2 * l)) >> 1, y = ((uint32_t)(c >> l) & msk) >> 1, z = ((uint32_t)c & msk) >> 1;
@@ -730,19 +735,24 @@ __global__ void __launch_bounds__(1024) k_target_small(SplitView v, int top) {
   }
 }
 
-// four consecutive cells per thread per trip: their pyramid loads are independent, so
-// they are in flight together (one cell per thread left this pass latency-bound)
+// four consecutive cells per thread per trip (l >= 2: same x, y; z0 % 4 == 0): their pyramid
+// values and the targets of their two parent cells are loaded together, so an empty /
+// merged cell's target costs no dependent load (one cell per thread left this pass
+// latency-bound)
 __global__ void __launch_bounds__(kThreads) k_target_level(SplitView v, int l) {
   pdl_wait();
   const uint64_t cells = 1ull << (3 * l);
+  const uint32_t msk = (1u << l) - 1, dp = 1u << (l - 1);
   for (uint64_t c0 = 4 * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x); c0 < cells;
        c0 += 4ull * gridDim.x * blockDim.x) {
     uint32_t val[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) val[u] = c0 + u < cells ? v.pyr[level_off(l) + c0 + u] : 0;
+    for (int u = 0; u < 4; ++u) val[u] = v.pyr[level_off(l) + c0 + u];
+    const uint32_t x = (uint32_t)(c0 >> (2 * l)) >> 1, y = ((uint32_t)(c0 >> l) & msk) >> 1, z = ((uint32_t)c0 & msk) >> 1;
+    const uint64_t ps = level_off(l - 1) + ((uint64_t)x * dp + y) * dp + z;
+    const int32_t par[2] = {v.node_idx[ps], v.node_idx[ps + 1]};
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (c0 + u < cells) target_cell(v, l, c0 + u, val[u]);
+    for (int u = 0; u < 4; ++u) target_cell(v, l, c0 + u, val[u], par[u >> 1]);
   }
 }
 
