@@ -263,13 +263,20 @@ __device__ void alloc_level(const VoxLevel& L) {
   for (uint32_t s0 = 0; s0 < L.list_n; s0 += NT) {
     const uint32_t s = s0 + threadIdx.x;
     uint32_t m = 0;
-    if (s < L.list_n) {
+    if (s < L.list_n) {  // the node's 16 block sums as 4 vector loads, all in flight
+      uint4* bs = reinterpret_cast<uint4*>(L.blk_sum + s * kBlksPerNode);
+      uint4 q[kBlksPerNode / 4];
+#pragma unroll
+      for (uint32_t b = 0; b < kBlksPerNode / 4; ++b) q[b] = __ldcg(bs + b);
       uint32_t run = 0;
-      for (uint32_t b = 0; b < kBlksPerNode; ++b) {
-        uint32_t v = __ldcg(L.blk_sum + s * kBlksPerNode + b);
-        L.blk_sum[s * kBlksPerNode + b] = run;  // becomes the block's exclusive prefix
-        run += v;
+#pragma unroll
+      for (uint32_t b = 0; b < kBlksPerNode / 4; ++b) {  // -> the blocks' exclusive prefixes
+        const uint4 v = q[b];
+        q[b] = make_uint4(run, run + v.x, run + v.x + v.y, run + v.x + v.y + v.z);
+        run += v.x + v.y + v.z + v.w;
       }
+#pragma unroll
+      for (uint32_t b = 0; b < kBlksPerNode / 4; ++b) bs[b] = q[b];
       m = run;
     }
     uint64_t tot;
