@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(uint64_t n, F f, u
     return;
   }
   uint64_t s = 0;
-#pragma unroll
+#pragma unroll 4
   for (int k = 0; k < kScanItems; ++k) {
     uint64_t i = base + (uint64_t)k * kScanThreads + threadIdx.x;
     if (i < n) s += f.value(i);
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kScanThreads) k_compact_count(uint64_t n, F f,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)warp * 32 * kScanItems;
   uint32_t c = 0;
-#pragma unroll
+#pragma unroll 4
   for (int k = 0; k < kScanItems; ++k) {
     uint64_t i = base + (uint64_t)k * 32 + lane;
     c += __popc(__ballot_sync(0xFFFFFFFFu, i < n && f.pred(i)));
