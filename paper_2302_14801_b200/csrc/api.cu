@@ -85,8 +85,10 @@ struct lod_tree {
   bool timing = false;
   cudaEvent_t ev[6] = {};
   cudaEvent_t kev[4] = {};  // the distribute's K_scatter, per pass (the dominant single kernel)
-  cudaStream_t vback = nullptr;        // voxelize: K4/K5 of level L overlap level L+1's front half
-  cudaEvent_t vev[3] = {};             // fork, accumulated (K3 done), finalized (K4/K5 done)
+  // voxelize runs each level on three streams: front (K0-K2b) on vfront, K3 on the caller's
+  // stream, back (K4/K5) on vback -- so level L+1's front overlaps level L's K3 and K4
+  cudaStream_t vfront = nullptr, vback = nullptr;
+  cudaEvent_t vev[6] = {};  // fork/join, front done, K3 done, back done (x2: depth parity), spare
   float stage_ms[5] = {};
 
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
@@ -666,7 +668,7 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     }
     const uint64_t chunk_cap = voxelize_chunk_capacity(t->n + cap, widest);
     const uint64_t vchunk_cap = voxelize_vchunk_capacity(cap, widest);
-    CK(ensure(t->vchunks, chunk_cap * 16));
+    CK(ensure(t->vchunks, 2 * chunk_cap * 16));  // two depth parities
     CK(ensure(t->vvchunks, 2 * vchunk_cap * 8));
     if (!(split_errors_pending && attempt == 0))  // else the split's device checks report with ours
       CK(cudaMemsetAsync((char*)t->state.p + offsetof(DevState, err), 0,
@@ -720,7 +722,6 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.bits = t->vbits.as<uint32_t>();
     L.pre = t->vpre.as<uint32_t>();
     L.blk_sum = t->vblk.as<uint32_t>();
-    L.chunks = t->vchunks.as<uint4>();
     L.vox = t->vox.as<uint2>();
     L.vox_cap = cap;
     L.acc_cap = acc_cap;
@@ -732,11 +733,20 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     L.obits = t->obits.as<uint32_t>();
     L.ocap = ocap;
     ScanScratch vscr{t->scan.as<uint64_t>(), t->scan.cap / 8};
-    const uint64_t vchunk_half = t->vvchunks.cap / 16;
-    // K4/K5 of each level run on t->vback, overlapping the next level up to its K3
-    CK(cudaEventRecord(t->vev[0], s));
-    CK(cudaStreamWaitEvent(t->vback, t->vev[0], 0));
-    bool back_pending = false;
+    const uint64_t vchunk_half = t->vvchunks.cap / 16, chunk_half = t->vchunks.cap / 32;
+    // Per level L: front(L) on vfront, K3(L) on s, back(L) on vback.  front(L) reuses the
+    // depth-parity buffers of the last level of its parity, so it waits for that level's back
+    // half; K3(L) waits for front(L) and for the children's colours (the last back half of the
+    // other parity).  front(L+1) thus runs under K3(L) and back(L).
+    cudaEvent_t& e_fork = t->vev[0];
+    cudaEvent_t& e_front = t->vev[1];
+    cudaEvent_t& e_k3 = t->vev[2];
+    cudaEvent_t* e_back = t->vev + 3;  // [parity]
+    cudaEvent_t& e_misc = t->vev[5];
+    CK(cudaEventRecord(e_fork, s));
+    CK(cudaStreamWaitEvent(t->vfront, e_fork, 0));
+    CK(cudaStreamWaitEvent(t->vback, e_fork, 0));
+    bool has_back[2] = {false, false};
     for (int d = kMaxDepth; d >= 0; --d) {  // deepest first (sampling.py:171)
       if (!lst_n[d] && !imp_n[d]) continue;
       L.parity = d & 1;
@@ -745,32 +755,45 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
       L.level_start = t->vlevel_start.as<uint64_t>() + d;
       L.acc = reinterpret_cast<uint64_t*>(t->vacc.as<char>() + (size_t)L.parity * acc_cap * acc_stride);
       L.vchunks = t->vvchunks.as<uint2>() + (size_t)L.parity * vchunk_half;
+      L.chunks = t->vchunks.as<uint4>() + (size_t)L.parity * chunk_half;
       if (lst_n[d]) {
         L.list = d_lists + lst_off[d];
         L.list_n = lst_n[d];
         L.chunk = voxelize_chunk(L.list_n);
         L.vchunk = voxelize_vchunk(L.list_n);
+        if (has_back[L.parity]) CK(cudaStreamWaitEvent(t->vfront, e_back[L.parity], 0));
         CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
-                           (size_t)L.list_n * kWordsPerNode * 4, s));
-        RUN(launch_voxelize_front(L, sms, s));
-        if (back_pending) CK(cudaStreamWaitEvent(s, t->vev[2], 0));  // the children's colours
+                           (size_t)L.list_n * kWordsPerNode * 4, t->vfront));
+        RUN(launch_voxelize_front(L, sms, t->vfront));
+        CK(cudaEventRecord(e_front, t->vfront));
+        CK(cudaStreamWaitEvent(s, e_front, 0));
+        if (has_back[1 - L.parity]) CK(cudaStreamWaitEvent(s, e_back[1 - L.parity], 0));  // children's colours
         RUN(launch_voxelize_accumulate(L, sms, s));
-        CK(cudaEventRecord(t->vev[1], s));
-        CK(cudaStreamWaitEvent(t->vback, t->vev[1], 0));
+        CK(cudaEventRecord(e_k3, s));
+        CK(cudaStreamWaitEvent(t->vback, e_k3, 0));
         RUN(launch_voxelize_back(L, sms, vscr, t->vback));
-        CK(cudaEventRecord(t->vev[2], t->vback));
-        back_pending = true;
+        CK(cudaEventRecord(e_back[L.parity], t->vback));
+        has_back[L.parity] = true;
       }
-      if (imp_n[d]) {
-        if (back_pending) CK(cudaStreamWaitEvent(s, t->vev[2], 0));
+      if (imp_n[d]) {  // imports (multi-GPU rank 0): everything before them done, everything after waits
+        for (int q = 0; q < 2; ++q)
+          if (has_back[q]) CK(cudaStreamWaitEvent(s, e_back[q], 0));
+        CK(cudaEventRecord(e_misc, t->vfront));
+        CK(cudaStreamWaitEvent(s, e_misc, 0));
         L.list = d_imp + imp_off[d];
         L.list_n = imp_n[d];
         CK(cudaMemsetAsync(L.bits + ((size_t)L.parity * widest + plan->imp_slot_base) * kWordsPerNode, 0,
                            (size_t)L.list_n * kWordsPerNode * 4, s));
         RUN(launch_voxelize_import(L, plan->imp_slot_base, s));
+        CK(cudaEventRecord(e_misc, s));
+        CK(cudaStreamWaitEvent(t->vfront, e_misc, 0));
+        CK(cudaStreamWaitEvent(t->vback, e_misc, 0));
       }
     }
-    if (back_pending) CK(cudaStreamWaitEvent(s, t->vev[2], 0));
+    for (int q = 0; q < 2; ++q)  // join
+      if (has_back[q]) CK(cudaStreamWaitEvent(s, e_back[q], 0));
+    CK(cudaEventRecord(e_misc, t->vfront));
+    CK(cudaStreamWaitEvent(s, e_misc, 0));
     int r = read_state(t, s);
     if (r) return r;
     CK(cudaGetLastError());
@@ -935,6 +958,7 @@ lod_tree* lod_tree_create(int device) {
   for (auto& e : t->kev) cudaEventCreate(&e);
   for (auto& e : t->vev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&t->vback, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&t->vfront, cudaStreamNonBlocking);
   return t;
 }
 
@@ -958,6 +982,7 @@ void lod_tree_destroy(lod_tree* t) {
   for (auto& e : t->vev)
     if (e) cudaEventDestroy(e);
   if (t->vback) cudaStreamDestroy(t->vback);
+  if (t->vfront) cudaStreamDestroy(t->vfront);
   if (t->host_state) cudaFreeHost(t->host_state);
   delete t;
 }
