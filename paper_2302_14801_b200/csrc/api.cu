@@ -483,10 +483,15 @@ int phase_skeleton(lod_tree* t, cudaStream_t s) {
   if ((r = check_errors(t, s))) return r;
   t->n_leaves = (uint32_t)t->host_state->count_a;
   v = make_view(t, t->pts);
+  // the targets (node_idx / t8 / te: a chain of per-level passes) on the front stream, under
+  // the leaf offsets, parent boxes and depth lists, which touch none of those arrays
+  CK(cudaEventRecord(t->vev[0], s));
+  CK(cudaStreamWaitEvent(t->vfront, t->vev[0], 0));
+  RUN(launch_targets(v, t->vfront));
+  for (auto& rd : t->rounds) RUN(launch_targets_ext(v, rd.first, rd.count, rd.ext, t->vfront));
+  CK(cudaEventRecord(t->vev[1], t->vfront));
   RUN(launch_leaf_offsets(v, scr, s));
   RUN(launch_leaf_parent_boxes(v, s));
-  RUN(launch_targets(v, s));
-  for (auto& rd : t->rounds) RUN(launch_targets_ext(v, rd.first, rd.count, rd.ext, s));
   uint32_t off = 0;
   for (int d = 0; d <= kMaxDepth; ++d) t->inner_off[d] = off, off += t->inner_per_depth[d];
   CK(ensure(t->depth_lists, (size_t)std::max<uint32_t>(off, 1) * 4));
@@ -500,6 +505,7 @@ int phase_skeleton(lod_tree* t, cudaStream_t s) {
   CK(cudaMemsetAsync(t->depth_cursor.p, 0, 64 * 4, s));
   RUN(launch_depth_scatter(v, t->depth_off.as<uint32_t>(), t->depth_cursor.as<uint32_t>(),
                            t->depth_lists.as<uint32_t>(), s));
+  CK(cudaStreamWaitEvent(s, t->vev[1], 0));  // join the targets
   for (int a = 0; a < 3; ++a) t->world[a] = t->host_state->lo[a];
   t->world[3] = t->host_state->size;
   t->inv_world = t->host_state->inv_size;
