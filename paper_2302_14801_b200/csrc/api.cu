@@ -542,6 +542,9 @@ int phase_distribute(lod_tree* t, cudaStream_t s, bool sync = true) {
     if (p.passes == 2) CK(ensure(t->tmp_rec, n * rec));
     CK(ensure(t->tmp_leaf, n * 4 * p.passes));  // leaf ids in input order (+ sorted by the 1st digit)
     for (int i = 0; i < 4; ++i) p.scatter_ev[i] = t->timing ? t->kev[i] : nullptr;
+    p.aux = t->vfront;
+    p.aux_ev[0] = t->vev[4];
+    p.aux_ev[1] = t->vev[5];
     p.counts = t->status.as<uint32_t>();
     p.scan_part = p.counts + ((size_t)p.segs << maxb);
     p.digit_base = t->digit_base.as<uint64_t>();

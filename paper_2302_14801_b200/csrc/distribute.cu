@@ -483,6 +483,7 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   const size_t hsm = (size_t)B * 4, ssm = (size_t)B * 8 + (size_t)kW * B * 2 + 4 * kW;
   const uint32_t* leaf_in = FIRST ? leaf_tmp : in_leaf;
   launch_pdl(hist, p.segs, kRadixThreads, hsm, s, v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
+  if (FIRST && p.aux) cudaStreamWaitEvent(s, p.aux_ev[1], 0);  // the digit bases
   const int nscan = launch_dist_scan(p.counts, p.segs, B, digit_base, p.scan_part, s);
   const cudaEvent_t* ev = p.scatter_ev + (FIRST ? 0 : 2);
   if (ev[0]) cudaEventRecord(ev[0], s);
@@ -508,19 +509,29 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
   const int B1 = p.passes > 1 ? 1 << p.bits[1] : 0;
   uint64_t* base0 = p.digit_base;
   uint64_t* base1 = p.digit_base + B0;
-  cudaMemsetAsync(p.digit_base, 0, (size_t)(B0 + B1) * 8, s);
+  // the global digit bases (from the leaf counts) on the side stream, under the first K_hist;
+  // run_pass waits for them before its scan
+  cudaStream_t a = p.aux ? p.aux : s;
+  if (p.aux) {
+    cudaEventRecord(p.aux_ev[0], s);
+    cudaStreamWaitEvent(a, p.aux_ev[0], 0);
+  }
+  cudaMemsetAsync(p.digit_base, 0, (size_t)(B0 + B1) * 8, a);
   uint32_t lb = ceil_div_u32(v.n_leaves, 256);
-  launch_pdl(k_digit_hist, lb, 256, 0, s, v.leaf_count, v.n_leaves, 0, p.bits[0],
-                                  reinterpret_cast<unsigned long long*>(base0));
-  launch_pdl(k_digit_scan, 1, 1024, 0, s, base0, B0);
+  launch_pdl(k_digit_hist, lb, 256, 0, a, v.leaf_count, v.n_leaves, 0, p.bits[0],
+             reinterpret_cast<unsigned long long*>(base0));
+  launch_pdl(k_digit_scan, 1, 1024, 0, a, base0, B0);
   launches += 2;
+  if (p.passes > 1) {
+    launch_pdl(k_digit_hist, lb, 256, 0, a, v.leaf_count, v.n_leaves, p.bits[0], p.bits[1],
+               reinterpret_cast<unsigned long long*>(base1));
+    launch_pdl(k_digit_scan, 1, 1024, 0, a, base1, B1);
+    launches += 2;
+  }
+  if (p.aux) cudaEventRecord(p.aux_ev[1], a);
   if (p.passes == 1)
     return launches + run_pass<FMT, true, false, OUT_FINAL>(v, v.pts, nullptr, p.tmp_leaf, leaf_out, nullptr, 0,
                                                            p.bits[0], 0, base0, p, s);
-  launch_pdl(k_digit_hist, lb, 256, 0, s, v.leaf_count, v.n_leaves, p.bits[0], p.bits[1],
-                                  reinterpret_cast<unsigned long long*>(base1));
-  launch_pdl(k_digit_scan, 1, 1024, 0, s, base1, B1);
-  launches += 2;
   if (p.bits[1] <= Rec<FMT>::kTagBits) {
     // the 2nd digit rides in the record pad: no scattered 4-B leaf-id stream (its partial
     // sectors cost read-modify-writes), the 2nd pass reads digits from the records

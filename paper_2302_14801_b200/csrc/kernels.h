@@ -125,6 +125,8 @@ struct RadixPlan {
   uint32_t* scan_part;    // 2 x 512 x 2^bits words: per-segment column sums of the counts
   uint64_t* digit_base;   // per pass: 2^bits global exclusive prefix
   cudaEvent_t scatter_ev[4];  // timing: start/end of each pass's K_scatter (null = off)
+  cudaStream_t aux;           // side stream for the digit bases (null: the build's stream)
+  cudaEvent_t aux_ev[2];      // fork, digit bases done
   void* tmp_rec;          // pass-0 output records (2 passes)
   uint32_t* tmp_leaf;     // leaf ids: input order (K_hist, pass 0) [+ sorted by digit 0]
 };
