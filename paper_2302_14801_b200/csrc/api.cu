@@ -477,19 +477,22 @@ int phase_skeleton(lod_tree* t, cudaStream_t s) {
   RUN(launch_number_leaves(v, scr, s));
   RUN(launch_depth_lists(v, t->depth_count.as<uint32_t>(), s));
   launch_pdl(k_copy_words, 1, 64, 0, s, t->host_depth_dev, t->depth_count.as<uint32_t>(), (uint32_t)(kMaxDepth + 2));
-  if ((r = read_state(t, s))) return r;
-  for (int d = 0; d <= kMaxDepth; ++d) t->inner_per_depth[d] = t->host_depth[d];
-  t->max_depth_used = t->host_depth[kMaxDepth + 1];
-  if ((r = check_errors(t, s))) return r;
-  t->n_leaves = (uint32_t)t->host_state->count_a;
-  v = make_view(t, t->pts);
-  // the targets (node_idx / t8 / te: a chain of per-level passes) on the front stream, under
-  // the leaf offsets, parent boxes and depth lists, which touch none of those arrays
+  // the targets (node_idx / t8 / te: a chain of per-level passes) only need the node table
+  // and the leaf numbering: on the front stream, under this host round trip and the leaf
+  // offsets / parent boxes / depth lists below, which touch none of those arrays
   CK(cudaEventRecord(t->vev[0], s));
   CK(cudaStreamWaitEvent(t->vfront, t->vev[0], 0));
   RUN(launch_targets(v, t->vfront));
   for (auto& rd : t->rounds) RUN(launch_targets_ext(v, rd.first, rd.count, rd.ext, t->vfront));
   CK(cudaEventRecord(t->vev[1], t->vfront));
+  if ((r = read_state(t, s)) || (r = check_errors(t, s))) {
+    cudaStreamWaitEvent(s, t->vev[1], 0);  // nothing of this build may outlive the call
+    return r;
+  }
+  for (int d = 0; d <= kMaxDepth; ++d) t->inner_per_depth[d] = t->host_depth[d];
+  t->max_depth_used = t->host_depth[kMaxDepth + 1];
+  t->n_leaves = (uint32_t)t->host_state->count_a;
+  v = make_view(t, t->pts);
   RUN(launch_leaf_offsets(v, scr, s));
   RUN(launch_leaf_parent_boxes(v, s));
   uint32_t off = 0;
