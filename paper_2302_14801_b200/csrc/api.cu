@@ -301,6 +301,12 @@ int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* 
   if (cfg->extension_depth < 1 || cfg->extension_depth > 5)
     return fail(LOD_EUNSUPPORTED, "extension_depth must be in [1, 5] on the GPU path");
   if (fmt != LOD_POINTS_F32 && fmt != LOD_POINTS_F64) return fail(LOD_EVALUE, "unknown point format %d", fmt);
+  CK(cudaSetDevice(t->device));
+  // a build that ended early (error path) may have left work on the tree's side streams
+  CK(cudaEventRecord(t->vev[4], t->vfront));
+  CK(cudaStreamWaitEvent(s, t->vev[4], 0));
+  CK(cudaEventRecord(t->vev[5], t->vback));
+  CK(cudaStreamWaitEvent(s, t->vev[5], 0));
   if (n >= 0xFFFFFFFFull) return fail(LOD_EUNSUPPORTED, "at most 2^32 - 2 points per GPU build");
   if (ub && !(ub[3] > 0)) return fail(LOD_EVALUE, "AABB size must be positive");
   CK(cudaSetDevice(t->device));
@@ -604,6 +610,10 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
   if (!t || !t->split_done) return fail(LOD_EVALUE, "lod_voxelize before a successful lod_split");
   if (mode < LOD_MODE_RANDOM || mode > LOD_MODE_WEIGHTED) return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
   CK(cudaSetDevice(t->device));
+  CK(cudaEventRecord(t->vev[4], t->vfront));  // side-stream work of an earlier call that ended early
+  CK(cudaStreamWaitEvent(s, t->vev[4], 0));
+  CK(cudaEventRecord(t->vev[5], t->vback));
+  CK(cudaStreamWaitEvent(s, t->vev[5], 0));
   t->voxel_mode = -1;
   if (!(plan && plan->append)) t->n_voxels = 0;
   uint32_t widest = 0;
