@@ -1,18 +1,26 @@
 """Benchmark: LOD construction points/sec (split + voxelize) on B200, BASELINE.json's metric.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config terrain20M] [--mode color_filter]
-    python bench.py --impl reference ...      # the reference's CPU path (oracle port) on host cores
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cluster2B] [--mode color_filter]
+    python bench.py --impl reference ...      # the reference's own CPU path on the host cores
 
 One step = one full LOD build of the configured synthetic cloud: world bounds ->
 counting grid -> extension rounds -> merge pyramid -> node table -> stable distribute
 -> bottom-up voxelization of every inner node.  `value` is whole-job points/s with the
 input resident in HBM (device time, CUDA events, max over ranks); `e2e` is the same metric
-through the public API from pinned HOST buffers, with the H2D copy of the input and the
+through the public C ABI from pinned HOST buffers, with the H2D copy of the input and the
 D2H copy of the whole built tree (leaf points, voxels, node table) inside the timed region.
 
-Default workload (N=1): BASELINE configs[1] = 20M-point terrain heightfield, color
-filtering (reference "average"), T = 50,000, 128^3 inner grids.  The 320 MB input is
-larger than the 126 MB L2, so no L2 flush is inserted between steps.
+Default workload: BASELINE configs[3] = cluster2B, the largest configuration that fits one
+B200 (2,000,000,000 points: 90% sphere surface, 16 dense clusters forcing extension to depth
+16, an exact-duplicate oversized leaf), color filtering (reference "average"), T = 50,000,
+128^3 inner grids.  For N > 1 GPUs the same fixed cloud is split N ways (rank r holds rows
+[r*N_pts/N, (r+1)*N_pts/N)): strong scaling, as the north star's 2/4/8-GPU curve.  The 32-GB
+input is far larger than the 126 MB L2, so no L2 flush is inserted between steps.
+
+The CPU reference (cpu_baseline, --impl reference) is the UNMODIFIED reference (`lodforge`,
+installed into baseline/_ref) when present, else the numpy oracle port, run on a subtree subset
+of the same cloud: `Partitioner(subset, BuildConfig(), bounds=world)` +
+`build_lod`, whose subtree is identical to the full build's (tests/test_gpu_large.py).
 """
 from __future__ import annotations
 
@@ -32,6 +40,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 
 def parse():
@@ -39,12 +48,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="terrain20M")
+    ap.add_argument("--config", default="cluster2B")
     ap.add_argument("--mode", default="color_filter",
                     choices=["color_filter", "average", "random", "first-come", "weighted"])
     ap.add_argument("--points", type=int, default=0, help="override the config's point count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=1_500_000,
+                    help="target size of the subtree subset the CPU reference builds")
+    ap.add_argument("--cpu-runs", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--stages", action="store_true", help="also print per-stage device times to stderr")
@@ -63,9 +74,9 @@ def dist_env():
 def hbm_peak():
     try:
         with open(PEAKS_PATH) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return FALLBACK_HBM, "fallback"
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
 class Clocks:
@@ -121,25 +132,8 @@ class Clocks:
 
 def make_input_device(torch, kind, n, seed, start=0):
     """Generate the synthetic cloud directly in HBM (bit-identical to generators.py)."""
-    from paper_2302_14801_b200 import _abi
-    from paper_2302_14801_b200.generators import scene_objects
-    lib = _abi.load()
-    buf = torch.empty(n * 16, dtype=torch.uint8, device="cuda")
-    table = None
-    if kind == "scene":
-        kinds, params, cdf = scene_objects(seed)
-        tab = np.zeros((65, 9))
-        tab[:, 0], tab[:, 1:8], tab[:, 8] = kinds, params, cdf
-        table = torch.from_numpy(tab.reshape(-1)).cuda()
-    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    tptr = C.cast(C.c_void_p(table.data_ptr()), C.POINTER(C.c_double)) if table is not None else None
-    chunk = 1 << 28
-    for s in range(0, n, chunk):
-        m = min(chunk, n - s)
-        _abi.check(lib.lod_generate(kind.encode(), seed, start + s, m, C.c_void_p(buf.data_ptr() + s * 16), tptr,
-                                    stream))
-    torch.cuda.synchronize()
-    return buf
+    from paper_2302_14801_b200.device import generate_device
+    return generate_device(kind, n, seed, start)
 
 
 def measured_traffic(config, mode, n, stage):
@@ -154,50 +148,244 @@ def measured_traffic(config, mode, n, stage):
         return None
 
 
-def cpu_reference_rate(kind, seed, sample, mode, steps=1):
-    """The reference algorithm on the host (oracle port, numpy, 1 core): points/s on a sample."""
+def extension_points(nodes, initial_depth=8, extension_depth=4, max_depth=16):
+    """E of SURVEY 8(d): points re-read by the extension rounds = the points under every
+    extension anchor (inner node at depth initial_depth + k * extension_depth < max_depth,
+    partition.py:109-151), from the node table's leaf counts."""
+    depth = nodes["depth"].astype(np.int64)
+    cell = nodes["cell"].astype(np.int64)
+    leaf = (nodes["flags"] & 1) == 1
+    ldepth, lcell, lcount = depth[leaf], cell[leaf], nodes["count"][leaf].astype(np.int64)
+    E = 0
+    for d in range(initial_depth, max_depth, extension_depth):
+        anchors = (~leaf) & (depth == d)
+        if not anchors.any():
+            break
+        ac = cell[anchors]
+        akey = (ac[:, 0] << 32) | (ac[:, 1] << 16) | ac[:, 2]
+        deep = ldepth > d
+        lc = lcell[deep] >> (ldepth[deep] - d)[:, None]
+        lkey = (lc[:, 0] << 32) | (lc[:, 1] << 16) | lc[:, 2]
+        E += int(lcount[deep][np.isin(lkey, akey)].sum())
+    return E
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+
+def reference_impl():
+    """('reference', lodforge modules) when the unmodified reference is installed in
+    baseline/_ref, else ('port', the oracle)."""
+    if os.path.isdir(os.path.join(REF_PATH, "lodforge")):
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        try:
+            import importlib
+            M, P, S = (importlib.import_module(f"lodforge.{m}") for m in ("model", "partition", "sampling"))
+            from lodforge.ingest import PointCloud
+            return "reference", (M, P, S, PointCloud)
+        except Exception:
+            pass
     from oracle import lod_oracle as O
-    from paper_2302_14801_b200.generators import synthetic_rows
-    pos, col = synthetic_rows(kind, seed, 0, sample)
-    pos64 = pos.astype(np.float64)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        sp = O.split(pos64)
-        O.voxelize(sp, pos64, col, mode, 0)
-        times.append(time.perf_counter() - t0)
-    return sample / statistics.median(times), times
+    return "port", O
+
+
+def reference_sample(config, target):
+    from oracle.synth import subtree_subset
+    from paper_2302_14801_b200.generators import CONFIGS
+    kind, n, seed, _ = CONFIGS[config]
+    return subtree_subset(kind, n, seed, target=target)
+
+
+def reference_build(sample, mode, impl):
+    """One timed CPU build of the subset: Partitioner(subset, cfg, bounds=world) + build_lod,
+    the cli.py:105-109 scope.  Returns (seconds, outcome)."""
+    kind, mod = impl
+    strat = "average" if mode in ("color_filter", "average") else mode
+    (lo, size) = sample["world"]
+    t0 = time.perf_counter()
+    outcome = "ok"
+    if kind == "reference":
+        M, P, S, PointCloud = mod
+        cloud = PointCloud(sample["positions"], sample["colors"])
+        cfg = M.BuildConfig(T=50_000, strategy=strat, seed=0)
+        tree = P.Partitioner(cloud, cfg, bounds=M.AABB(tuple(lo), size)).run()
+        try:
+            S.build_lod(tree)
+        except Exception as e:   # the 2^20 random limit (sampling.py:73-75)
+            outcome = f"{type(e).__name__}: {e}"
+    else:
+        sp = mod.split(sample["positions"], T=50_000, bounds=(tuple(lo), size))
+        try:
+            mod.voxelize(sp, sample["positions"], sample["colors"], strat, 0)
+        except Exception as e:
+            outcome = f"{type(e).__name__}: {e}"
+    return time.perf_counter() - t0, outcome
+
+
+def _sample_desc(config, sample, impl_kind):
+    who = ("lodforge (unmodified reference, baseline/_ref)" if impl_kind == "reference"
+           else "numpy oracle port of lodforge")
+    return (f"subtree subset of {config}: the {sample['count']} points of the depth-{sample['depth']} node "
+            f"{tuple(sample['cell'])} in input order, Partitioner(subset, BuildConfig(T=50000), bounds=world) + "
+            f"build_lod via {who}, numpy single-threaded like the reference (cli.py:246-247 ignores threads)")
 
 
 def run_reference(args):
-    """--impl reference: rank 0 times the reference's CPU path (oracle port); others exit."""
+    """--impl reference: rank 0 times the reference's CPU path on a subtree subset; others exit."""
     rank, world, _ = dist_env()
-    from paper_2302_14801_b200.generators import CONFIGS
-    kind, n, seed, _ = CONFIGS[args.config]
     if rank != 0:
         return
-    sample = min(args.cpu_sample, n)
-    mode = "average" if args.mode in ("color_filter", "average") else args.mode
+    impl = reference_impl()
+    sample = reference_sample(args.config, args.cpu_sample)
     for _ in range(args.warmup):
-        cpu_reference_rate(kind, seed, min(sample, 100_000), mode)
-    rates, times = [], []
+        reference_build(sample, args.mode, impl)
+    times, outcome = [], "ok"
     for _ in range(args.steps):
-        r, t = cpu_reference_rate(kind, seed, sample, mode)
-        rates.append(r)
-        times += t
-    value = sample / (sum(times) / len(times))
+        t, outcome = reference_build(sample, args.mode, impl)
+        times.append(t)
+    sec = sum(times) / len(times)
+    value = sample["count"] / sec
+    from paper_2302_14801_b200.generators import CONFIGS
     line = {
         "impl": "reference", "metric": f"LOD construction points/sec ({args.mode})",
         "value": value, "unit": "points/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "points": n, "mode": args.mode, "T": 50_000, "grid": 128},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "port",
-                         "sample": f"first {sample} points of {args.config} per step (numpy oracle port of "
-                                   f"lodforge partition + build_lod, single-threaded like the reference)"},
+        "ms_per_step": 1000 * sec, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "points": CONFIGS[args.config][1], "mode": args.mode, "T": 50_000,
+                   "grid": 128},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "host_cpu_count": os.cpu_count(),
+                         "kind": impl[0], "sample": _sample_desc(args.config, sample, impl[0]),
+                         "outcome": outcome},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# e2e: host buffers in, whole tree out, through the public C ABI
+# ---------------------------------------------------------------------------
+
+def _tree_bytes(dev, n):
+    from paper_2302_14801_b200 import _abi
+    info = dev.info()
+    return n * 16 + info.n_voxels * 8 + info.n_nodes * _abi.node_dtype().itemsize
+
+
+def e2e_two_trees(torch, dev, d_in, n, cfg, mode_code, steps, stream):
+    """Clouds that fit twice: two trees on two streams, 2-deep pipeline (upload k+1 ||
+    build k || download k-1; PCIe is full duplex)."""
+    from paper_2302_14801_b200 import _abi
+    from paper_2302_14801_b200.device import DeviceTree
+    info = dev.info()
+    rec_bytes, vox_bytes = n * 16, info.n_voxels * 8
+    node_bytes = info.n_nodes * _abi.node_dtype().itemsize
+    lib = dev.lib
+    h_in = torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True)
+    h_in.copy_(d_in)
+    trees = [dev, DeviceTree(dev.device)]
+    d_stage = [torch.empty(rec_bytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    h_leaf = [torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    h_vox = [torch.empty(max(vox_bytes, 8), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    h_nodes = [torch.empty(max(node_bytes, 8), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    up = torch.cuda.Stream()
+    cs = [torch.cuda.Stream(), torch.cuda.Stream()]
+    uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+    built = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def run(k_steps):
+        for b in range(2):
+            built[b].record(cs[b])
+        with torch.cuda.stream(up):
+            d_stage[0].copy_(h_in, non_blocking=True)
+            uploaded[0].record(up)
+        for k in range(k_steps):
+            b = k & 1
+            if k + 1 < k_steps:  # next input, once the build that last read the buffer is done
+                up.wait_event(built[1 - b])
+                with torch.cuda.stream(up):
+                    d_stage[1 - b].copy_(h_in, non_blocking=True)
+                    uploaded[1 - b].record(up)
+            cs[b].wait_event(uploaded[b])
+            sp = C.c_void_p(cs[b].cuda_stream)
+            trees[b].build(d_stage[b], n, _abi.LOD_POINTS_F32, cfg, mode_code, 0, stream=sp)
+            built[b].record(cs[b])
+            _abi.check(lib.lod_tree_copy_async(trees[b].h, C.c_void_p(h_leaf[b].data_ptr()),
+                                               C.c_void_p(h_vox[b].data_ptr()),
+                                               C.c_void_p(h_nodes[b].data_ptr()), sp))
+        for st in (up, cs[0], cs[1]):
+            stream.wait_stream(st)
+
+    run(2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    up.wait_stream(stream)
+    run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return (e0.elapsed_time(e1) / steps, "2 trees, 2-deep on 3 streams: upload k+1 || build k || download k-1",
+            rec_bytes, _tree_bytes(dev, n))
+
+
+def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
+    """Clouds that fit once (cluster2B: ~100 GB working set): one tree, split and voxelize as
+    separate ABI calls so the copies overlap the work that no longer needs their buffers --
+    the next upload starts when the split has consumed the input, the leaf download runs under
+    the voxelize, the voxel/node download under the next upload."""
+    from paper_2302_14801_b200 import _abi
+    info = dev.info()
+    rec_bytes = n * 16
+    lib = dev.lib
+    h_in = torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True)
+    h_in.copy_(d_in)
+    h_leaf = torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True)
+    h_vox = torch.empty(max(info.n_voxels * 8, 8), dtype=torch.uint8, pin_memory=True)
+    h_nodes = torch.empty(max(info.n_nodes * _abi.node_dtype().itemsize, 88), dtype=torch.uint8, pin_memory=True)
+    d_stage = d_in            # the device input buffer is the staging buffer
+    up, dl = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_up, ev_split, ev_vox, ev_dl = (torch.cuda.Event() for _ in range(4))
+    sp = C.c_void_p(stream.cuda_stream)
+    dlp = C.c_void_p(dl.cuda_stream)
+
+    def run(k_steps):
+        up.wait_stream(stream)
+        with torch.cuda.stream(up):
+            d_stage.copy_(h_in, non_blocking=True)
+            ev_up.record(up)
+        ev_dl.record(dl)
+        for k in range(k_steps):
+            stream.wait_event(ev_up)
+            stream.wait_event(ev_dl)        # the previous tree's downloads are done
+            dev.split(d_stage, n, _abi.LOD_POINTS_F32, cfg, stream=sp)
+            ev_split.record(stream)
+            if k + 1 < k_steps:             # the split consumed the input: upload the next one
+                up.wait_event(ev_split)
+                with torch.cuda.stream(up):
+                    d_stage.copy_(h_in, non_blocking=True)
+                    ev_up.record(up)
+            dl.wait_event(ev_split)         # leaf points are final after the distribute
+            _abi.check(lib.lod_tree_copy_async(dev.h, C.c_void_p(h_leaf.data_ptr()), None, None, dlp))
+            dev.voxelize(mode_code, seed, stream=sp)
+            ev_vox.record(stream)
+            dl.wait_event(ev_vox)
+            _abi.check(lib.lod_tree_copy_async(dev.h, None, C.c_void_p(h_vox.data_ptr()),
+                                               C.c_void_p(h_nodes.data_ptr()), dlp))
+            ev_dl.record(dl)
+        stream.wait_stream(dl)
+        stream.wait_stream(up)
+
+    run(1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return (e0.elapsed_time(e1) / steps,
+            "1 tree, 3 streams: split k -> (voxelize k || leaf download k || upload k+1) -> voxel+node download k",
+            rec_bytes, _tree_bytes(dev, n))
 
 
 def main():
@@ -219,14 +407,15 @@ def main():
     from paper_2302_14801_b200.generators import CONFIGS
 
     kind, n_cfg, seed, _ = CONFIGS[args.config]
-    n = args.points or n_cfg
+    n_total = args.points or n_cfg
+    # strong scaling: the fixed cloud split N ways, rank r holds rows [r*N/R, (r+1)*N/R)
+    start = n_total * rank // world
+    n = n_total * (rank + 1) // world - start
     from paper_2302_14801_b200.sampling import _mode_code
     mode_code = _mode_code(args.mode)
     cfg = make_config(50_000)
 
-    # weak scaling: rank r holds rows [r*n, (r+1)*n) of one N*n-point cloud; for N > 1 the
-    # ranks build ONE tree together (dist.py: all-reduced grids, subtree all-to-all, rank-0 merge)
-    d_in = make_input_device(torch, kind, n, seed, start=rank * n)
+    d_in = make_input_device(torch, kind, n, seed, start=start)
     dev = DeviceTree(local)
     stream = torch.cuda.current_stream()
     sptr = C.c_void_p(stream.cuda_stream)
@@ -276,75 +465,32 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
         torch.distributed.barrier()
-    value = n * world / (ms / 1000.0)
+    value = n_total / (ms / 1000.0)
+    E = extension_points(dev.nodes())
+    V = info.n_voxels
+    if args.stages:
+        print(f"stages ms {stages} scatter {scatter_ms} E {E} device bytes {dev.device_bytes()}", file=sys.stderr)
 
-    # ---- e2e: host buffers in, whole tree out, through the public C ABI ----
-    # Every step uploads its input from pinned host memory and downloads the whole built
-    # tree (leaf points, voxels, node table).  On one GPU the steps are pipelined two deep
-    # on separate streams -- upload of step k+1 || build of step k || download of step k-1
-    # (PCIe is full duplex; the library's lod_tree_copy_async enqueues the downloads) -- the
-    # way a stream of clouds would be processed.  N > 1 ranks run the steps serially.
+    # ---- e2e ----
     e2e = None
     if not args.no_e2e:
-        rec_bytes = n * 16
-        vox_bytes = info.n_voxels * 8
-        node_bytes = info.n_nodes * _abi.node_dtype().itemsize
-        h_in = torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True)
-        h_in.copy_(d_in.cpu())
-        lib = dev.lib
         if world == 1:
-            trees = [dev, DeviceTree(local)]
-            d_stage = [torch.empty(rec_bytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
-            h_leaf = [torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-            h_vox = [torch.empty(max(vox_bytes, 8), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-            h_nodes = [torch.empty(max(node_bytes, 8), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-            up = torch.cuda.Stream()
-            cs = [torch.cuda.Stream(), torch.cuda.Stream()]
-            uploaded = [torch.cuda.Event(), torch.cuda.Event()]
-            built = [torch.cuda.Event(), torch.cuda.Event()]
-
-            def run(k_steps):
-                for b in range(2):
-                    built[b].record(cs[b])
-                with torch.cuda.stream(up):
-                    d_stage[0].copy_(h_in, non_blocking=True)
-                    uploaded[0].record(up)
-                for k in range(k_steps):
-                    b = k & 1
-                    if k + 1 < k_steps:  # next input, once the build that last read the buffer is done
-                        up.wait_event(built[1 - b])
-                        with torch.cuda.stream(up):
-                            d_stage[1 - b].copy_(h_in, non_blocking=True)
-                            uploaded[1 - b].record(up)
-                    cs[b].wait_event(uploaded[b])
-                    sp = C.c_void_p(cs[b].cuda_stream)
-                    trees[b].build(d_stage[b], n, _abi.LOD_POINTS_F32, cfg, mode_code, 0, stream=sp)
-                    built[b].record(cs[b])
-                    _abi.check(lib.lod_tree_copy_async(trees[b].h, C.c_void_p(h_leaf[b].data_ptr()),
-                                                       C.c_void_p(h_vox[b].data_ptr()),
-                                                       C.c_void_p(h_nodes[b].data_ptr()), sp))
-                for st in (up, cs[0], cs[1]):
-                    stream.wait_stream(st)
-
-            run(2)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            up.wait_stream(stream)
-            run(args.steps)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ems = e0.elapsed_time(e1) / args.steps
-            pipeline = "2-deep on 3 streams: upload k+1 || build k || download k-1"
+            free, _ = torch.cuda.mem_get_info()
+            if free > dev.device_bytes() + 2 * n * 16 + (4 << 30):
+                ems, pipeline, hb, db = e2e_two_trees(torch, dev, d_in, n, cfg, mode_code, args.steps, stream)
+            else:
+                ems, pipeline, hb, db = e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, 0, args.steps, stream)
         else:
-            h_leaf = torch.empty(rec_bytes * 2, dtype=torch.uint8, pin_memory=True)
-            h_vox = torch.empty(max(vox_bytes, 8) * 2, dtype=torch.uint8, pin_memory=True)
+            h_in = torch.empty(n * 16, dtype=torch.uint8, pin_memory=True)
+            h_in.copy_(d_in)
+            h_leaf = torch.empty(n_total * 16 + 64, dtype=torch.uint8, pin_memory=True)
+            h_vox = torch.empty(max(V * 8 * 2, 8), dtype=torch.uint8, pin_memory=True)
             h_nodes = np.zeros(info.n_nodes, _abi.node_dtype())
-            d_stage = torch.empty(rec_bytes, dtype=torch.uint8, device="cuda")
+            lib = dev.lib
 
             def e2e_step():
-                d_stage.copy_(h_in, non_blocking=True)
-                step(d_stage)
+                d_in.copy_(h_in, non_blocking=True)
+                step(d_in)
                 _abi.check(lib.lod_tree_copy_leaf_points(dev.h, C.c_void_p(h_leaf.data_ptr()), sptr))
                 _abi.check(lib.lod_tree_copy_voxels(dev.h, C.c_void_p(h_vox.data_ptr()), sptr))
                 _abi.check(lib.lod_tree_copy_nodes(dev.h, h_nodes.ctypes.data_as(C.c_void_p), sptr))
@@ -362,62 +508,67 @@ def main():
             t = torch.tensor([ems], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ems = float(t.item())
-            pipeline = "serial per step"
-        e2e = {"value": n * world / (ems / 1000.0), "unit": "points/s", "h2d_bytes_per_step": rec_bytes,
-               "d2h_bytes_per_step": rec_bytes + vox_bytes + node_bytes, "ms_per_step": ems,
-               "pipeline": pipeline}
+            li = dev.info()
+            pipeline, hb = "serial per step", n * 16
+            db = li.n_points * 16 + li.n_voxels * 8 + li.n_nodes * _abi.node_dtype().itemsize
+        e2e = {"value": n_total / (ems / 1000.0), "unit": "points/s", "h2d_bytes_per_step": hb,
+               "d2h_bytes_per_step": db, "ms_per_step": ems, "pipeline": pipeline}
 
-    # ---- roofline ----
+    # ---- roofline (SURVEY 8(d) algorithmic bytes: B = 80 N + 16 E + 12 V) ----
     # Dominant single kernel: the distribute's K_scatter (stable counting-sort scatter), the
-    # longest kernel of a build (ncu launch lists in profiles/).  Its algorithmic bytes per
-    # pass: every record read once and written once (32 B/pt).  Timed live with CUDA events
-    # the library records around it on the build's stream, averaged over the timed builds.
-    # Per stage: bounds 16N + count 16N, extension 16E, distribute 32N,
-    # voxelize 16N + 12V (each voxel written and read once as a 6-B record); the skeleton
-    # (merge / nodes / targets) is N-independent.
+    # longest kernel of a build (ncu launch lists in profiles/).  Algorithmic bytes: each
+    # record read once and written once, 32 B/pt, however many radix passes the
+    # implementation takes (a second pass is implementation overhead, not algorithm).  Timed
+    # live with CUDA events the library records around it on the build's stream.
     peak, peak_kind = hbm_peak()
-    V = info.n_voxels
     passes = max(info.radix_passes, 1)
     stage_names = ["bounds+count", "extension", "merge+nodes+targets", "distribute", "voxelize"]
-    stage_bytes = [32 * n, 16 * n if info.n_ext_grids else 0, 0, 32 * n, 16 * n + 12 * V]
-    kern_bytes = 32 * n * passes
+    stage_bytes = [32 * n, 16 * E, 0, 32 * n, 16 * n + 12 * V]
+    kern_bytes = 32 * n
     achieved = kern_bytes / (scatter_ms / 1000.0) / 1e9 if scatter_ms > 0 else 0.0
-    whole_bytes = 80 * n + 12 * V
-    traffic = measured_traffic(args.config, args.mode, n, "k_dist_scatter") if world == 1 else None
+    whole_bytes = 80 * n + 16 * E + 12 * V
+    mode_key = "color_filter" if args.mode in ("color_filter", "average") else args.mode
+    traffic = measured_traffic(args.config, mode_key, n, "k_dist_scatter") if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"K_scatter (distribute.cu: k_dist_scatter_staged for f32 records), {passes} pass(es)",
+                "traffic": traffic,
+                "kernel": f"K_scatter (distribute.cu k_dist_scatter_staged, f32 records), {passes} radix pass(es) "
+                          f"timed together against one read + one write per record",
                 "algorithmic_bytes": kern_bytes, "ms_per_build": scatter_ms, "peak_source": peak_kind,
                 "stages": {nm: {"ms": st, "algorithmic_bytes": b,
                                 "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st > 0 else None,
-                                "traffic": measured_traffic(args.config, args.mode, n, nm) if world == 1 else None}
+                                "frac": (b / (st / 1000.0) / 1e9 / peak) if b and st > 0 else None,
+                                "traffic": measured_traffic(args.config, mode_key, n, nm) if world == 1 else None}
                            for nm, st, b in zip(stage_names, stages, stage_bytes)},
-                "whole_build": {"algorithmic_bytes": whole_bytes,
+                "whole_build": {"algorithmic_bytes": whole_bytes, "E": E, "V": V,
                                 "achieved_gbs": whole_bytes / (ms / 1000.0) / 1e9,
                                 "frac": whole_bytes / (ms / 1000.0) / 1e9 / peak}}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        mode = "average" if args.mode in ("color_filter", "average") else args.mode
-        rate, times = cpu_reference_rate(kind, seed, args.cpu_sample, mode, steps=2)
-        cpu = {"value": rate, "unit": "points/s", "cores": 1, "kind": "port",
-               "sample": f"first {args.cpu_sample} points of {args.config}, {mode}, numpy oracle port of "
-                         f"lodforge partition + build_lod (single-threaded like the reference), median of 2"}
+    if rank == 0 and not args.no_cpu_baseline:
+        impl = reference_impl()
+        sample = reference_sample(args.config, args.cpu_sample)
+        runs = [reference_build(sample, args.mode, impl) for _ in range(args.cpu_runs)]
+        sec = statistics.median(t for t, _ in runs)
+        cpu = {"value": sample["count"] / sec, "unit": "points/s", "cores": 1, "host_cpu_count": os.cpu_count(),
+               "kind": impl[0], "sample": _sample_desc(args.config, sample, impl[0]) + f", median of {len(runs)}",
+               "outcome": runs[-1][1], "same_config": True}
 
     if rank == 0:
         line = {
             "metric": f"LOD construction points/sec ({args.mode})",
             "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64-geometry/u32-counts", "data": "synthetic",
-            "config": {"workload": args.config, "points_per_gpu": n, "mode": args.mode, "T": 50_000,
-                       "grid": 128, "l2": "input 16 B/pt x points > 126 MB L2, no flush",
+            "config": {"workload": args.config, "points": n_total, "points_per_gpu": n, "mode": args.mode,
+                       "T": 50_000, "grid": 128, "l2": "input 16 B/pt x points > 126 MB L2, no flush",
                        "parallelism": f"subtree-sharded x{world} ({args.backend} all-reduce + all-to-all + rank-0 merge)"
                        if world > 1 else "single"},
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "stages_ms": dict(zip(stage_names, stages)),
             "tree": {"nodes": info.n_nodes, "leaves": info.n_leaves, "depth": info.depth, "voxels": V,
-                     "ext_grids": info.n_ext_grids, "radix_passes": info.radix_passes},
+                     "ext_grids": info.n_ext_grids, "ext_points": E, "radix_passes": info.radix_passes,
+                     "device_bytes": dev.device_bytes()},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -143,6 +143,13 @@ int lod_tree_copy_async(const lod_tree* tree, void* h_leaf_points, void* h_voxel
 int lod_tree_copy_leaf_points(const lod_tree* tree, void* host, void* stream);
 int lod_tree_copy_voxels(const lod_tree* tree, void* host, void* stream);
 
+/* Copy a range of one output to host memory and wait: what = 0 leaf points (records
+ * [first, first+count) of the leaf buffer), what = 1 voxels (stored order).  With a node's
+ * lod_node.first / count this fetches one node's points or voxels without the whole tree
+ * (reference OctreeNode.point_positions / voxel_coords of a single node, model.py:130-168). */
+int lod_tree_copy_range(const lod_tree* tree, int what, uint64_t first, uint64_t count, void* host,
+                        void* stream);
+
 /* VLPC payload (reference codec.py:28-47): for the n nodes h_order[i] (node ids, in the
  * file's path order, codec.py:51) write each node's records at byte h_offsets[i] of the
  * device buffer d_payload -- leaves 16-B {f32 offset from node min, rgb, pad}, inner nodes

@@ -71,6 +71,7 @@ SIGNATURES = [
     ("lod_tree_copy_leaf_points", C.c_int, [_P, _P, _P]),
     ("lod_tree_copy_voxels", C.c_int, [_P, _P, _P]),
     ("lod_tree_copy_async", C.c_int, [_P, _P, _P, _P, _P]),
+    ("lod_tree_copy_range", C.c_int, [_P, C.c_int, C.c_uint64, C.c_uint64, _P, _P]),
     ("lod_tree_encode_payload", C.c_int, [_P, _P, _P, C.c_uint32, _P, _P]),
     ("lod_ingest_las", C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_int32, _P, _P, _P, _P]),
     ("lod_ingest_ply", C.c_int, [_P, C.c_uint64, C.c_uint32, _P, _P, C.c_int, C.c_int, _P, _P]),

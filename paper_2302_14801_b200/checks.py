@@ -50,7 +50,7 @@ def _device_checks(tree, expected_points, require_lod):
     flags = np.zeros(len(nodes), np.uint8)
     _abi.check(dev.lib.lod_tree_checks(dev.h, int(tree.config.T), int(tree.config.max_depth),
                                        flags.ctypes.data_as(C.c_void_p),
-                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+                                       C.c_void_p(torch.cuda.current_stream(dev.device).cuda_stream)))
     order = np.argsort(path_sort_keys(nodes["cell"], nodes["depth"]), kind="stable")   # DFS preorder
     bad = {}
     for bit in (CAPACITY, OVERSIZED, MAXIMALITY, CONTAINMENT, VOXEL_BOUNDS, UNIQUENESS, EMPTY_INNER, NO_CHILDREN):

@@ -159,6 +159,20 @@ int read_state(lod_tree* t, cudaStream_t s) {
   return LOD_OK;
 }
 
+// Every entry point runs on the tree's device and gives the caller's current device back
+// (the ABI must not change torch's current device for the calling thread).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t status;
+  explicit DeviceGuard(int d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    status = cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 std::string path_of(uint64_t cell) {
   uint32_t cx = (uint32_t)cell & 0xFFFF, cy = (uint32_t)(cell >> 16) & 0xFFFF, cz = (uint32_t)(cell >> 32) & 0xFFFF;
   int depth = (int)(cell >> 48) & 0xFF;
@@ -221,8 +235,8 @@ int check_errors(lod_tree* t, cudaStream_t s) {
     return fail(LOD_ECONSISTENCY, "%llu samples exceed the 20-bit index limit of random sampling",
                 (unsigned long long)best_s);
   }
-  if (e & ERR_EMPTY_CHILD) return fail(LOD_ECONSISTENCY, "child of node %s has no samples",
-                                       node_path(h.err_detail).c_str());
+  if (e & ERR_EMPTY_CHILD)  // f"child {child.path} has no samples" (sampling.py:35)
+    return fail(LOD_ECONSISTENCY, "child %s has no samples", node_path(h.err_detail).c_str());
   if (e & ERR_ZERO_WEIGHT) return fail(LOD_ECONSISTENCY, "occupied cell accumulated zero weight");
   return fail(LOD_ECONSISTENCY, "device error 0x%x", e);
 }
@@ -301,7 +315,8 @@ int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* 
   if (cfg->extension_depth < 1 || cfg->extension_depth > 5)
     return fail(LOD_EUNSUPPORTED, "extension_depth must be in [1, 5] on the GPU path");
   if (fmt != LOD_POINTS_F32 && fmt != LOD_POINTS_F64) return fail(LOD_EVALUE, "unknown point format %d", fmt);
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   // a build that ended early (error path) may have left work on the tree's side streams
   CK(cudaEventRecord(t->vev[4], t->vfront));
   CK(cudaStreamWaitEvent(s, t->vev[4], 0));
@@ -309,7 +324,6 @@ int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* 
   CK(cudaStreamWaitEvent(s, t->vev[5], 0));
   if (n >= 0xFFFFFFFFull) return fail(LOD_EUNSUPPORTED, "at most 2^32 - 2 points per GPU build");
   if (ub && !(ub[3] > 0)) return fail(LOD_EVALUE, "AABB size must be positive");
-  CK(cudaSetDevice(t->device));
   t->split_done = false;
   t->voxel_mode = -1;
   t->n_voxels = 0;
@@ -609,7 +623,8 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
                 bool split_errors_pending = false) {
   if (!t || !t->split_done) return fail(LOD_EVALUE, "lod_voxelize before a successful lod_split");
   if (mode < LOD_MODE_RANDOM || mode > LOD_MODE_WEIGHTED) return fail(LOD_EVALUE, "unknown sampling strategy: %d", mode);
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   CK(cudaEventRecord(t->vev[4], t->vfront));  // side-stream work of an earlier call that ended early
   CK(cudaStreamWaitEvent(s, t->vev[4], 0));
   CK(cudaEventRecord(t->vev[5], t->vback));
@@ -647,6 +662,10 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
   for (int d = 0; d <= kMaxDepth; ++d) total += lst_n[d] + imp_n[d];
   mark(t, 4, s);
   if (total == 0 && !(plan && plan->n_imp)) {  // single-leaf root: nothing to voxelize (test_sampling.py:163-166)
+    if (split_errors_pending) {  // lod_build: the split's deferred device checks
+      int r = read_state(t, s);
+      if (r || (r = check_errors(t, s))) return r;
+    }
     t->voxel_mode = mode;
     mark(t, 5, s);
     return LOD_OK;
@@ -668,14 +687,17 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
   // first guess at the arena (grown and re-run on ERR_ARENA): surfaces give V/N ~ 0.3-1.0,
   // volumes up to ~1.8; very large clouds start lean to leave HBM for the rest
   const uint64_t guess = t->n <= (1ull << 27) ? t->n + t->n / 2 : t->n - t->n / 4;
-  uint64_t cap = std::max<uint64_t>(guess, 1ull << 21) + base_cursor + imp_total;
-  if (t->vox.cap / 8 > cap) cap = t->vox.cap / 8;
-  const uint32_t acc_stride = voxelize_acc_bytes(mode);
+  // LODB200_TINY_ARENA=1 (tests only): start from a tiny arena so the grow-and-retry path runs
+  static const bool tiny_arena = getenv("LODB200_TINY_ARENA") && getenv("LODB200_TINY_ARENA")[0] == '1';
+  uint64_t cap = (tiny_arena ? 4096 : std::max<uint64_t>(guess, 1ull << 21)) + base_cursor + imp_total;
+  if (t->vox.cap / 8 > cap && !tiny_arena) cap = t->vox.cap / 8;
+  uint32_t acc_stride = voxelize_acc_bytes(mode, false);
   const bool fc = mode == LOD_MODE_FIRST_COME;
-  uint64_t acc_cap = std::max<uint64_t>(t->n <= (1ull << 27) ? t->n / 2 : t->n / 4, 1ull << 21);
-  if (t->vacc.cap / (2 * acc_stride) > acc_cap) acc_cap = t->vacc.cap / (2 * acc_stride);
+  uint64_t acc_cap = tiny_arena ? 1024 : std::max<uint64_t>(t->n <= (1ull << 27) ? t->n / 2 : t->n / 4, 1ull << 21);
+  if (t->vacc.cap / (2 * acc_stride) > acc_cap && !tiny_arena) acc_cap = t->vacc.cap / (2 * acc_stride);
   bool exact_sums = false;
   for (int attempt = 0; attempt < 8; ++attempt) {
+    acc_stride = voxelize_acc_bytes(mode, exact_sums);  // the u64 fallback needs 32 B per voxel
     CK(ensure(t->vox, cap * 8, base_cursor * 8, s));
     cap = t->vox.cap / 8;
     CK(ensure(t->vacc, 2 * acc_cap * acc_stride));  // two depth parities (launch_voxelize_back)
@@ -819,6 +841,9 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
     int r = read_state(t, s);
     if (r) return r;
     CK(cudaGetLastError());
+    // lod_build defers the split's device checks to here: report them before any retry
+    // (a retry clears the error word, and the arena size in err_value would be the split's)
+    if (split_errors_pending && (t->host_state->err & kSplitErrors)) return check_errors(t, s);
     if ((t->host_state->err & ERR_ARENA) && !(t->host_state->err & ERR_RANDOM_LIMIT)) {
       uint64_t need = t->host_state->err_value;
       cap = std::max<uint64_t>(cap * 2, need + (need >> 2));
@@ -964,7 +989,8 @@ lod_tree* lod_tree_create(int device) {
   void* hm = nullptr;
   void* hm_dev = nullptr;
   const size_t depth_at = (sizeof(DevState) + 15) & ~(size_t)15;
-  if (cudaSetDevice(device) != cudaSuccess ||
+  DeviceGuard dg_(device);
+  if (dg_.status != cudaSuccess ||
       cudaHostAlloc(&hm, depth_at + 4 * (kMaxDepth + 2), cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(&hm_dev, hm, 0) != cudaSuccess) {
     if (hm) cudaFreeHost(hm);
@@ -986,7 +1012,7 @@ lod_tree* lod_tree_create(int device) {
 
 void lod_tree_destroy(lod_tree* t) {
   if (!t) return;
-  cudaSetDevice(t->device);
+  DeviceGuard dg_(t->device);
   DevBuf* all[] = {&t->state, &t->pyr, &t->node_idx, &t->t8, &t->te, &t->meta, &t->list, &t->scan, &t->slots,
                    &t->n_cell, &t->n_val, &t->n_parent, &t->n_child, &t->n_slot, &t->n_extid, &t->n_lvl,
                    &t->n_leaf, &t->n_box, &t->n_first, &t->n_count, &t->leaf_node, &t->leaf_first, &t->leaf_count,
@@ -1052,7 +1078,8 @@ int lod_tree_copy_nodes(const lod_tree* tc, lod_node* host, void* stream) {
   lod_tree* t = const_cast<lod_tree*>(tc);
   if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
   cudaStream_t s = (cudaStream_t)stream;
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   CK(ensure(t->export_buf, (size_t)t->n_nodes * sizeof(lod_node)));
   SplitView v = make_view(t, nullptr);
   launch_export_nodes(v, t->export_buf.as<lod_node>(), s);
@@ -1066,7 +1093,8 @@ int lod_tree_copy_async(const lod_tree* tc, void* h_leaf, void* h_vox, lod_node*
   if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
   if (h_vox && t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
   cudaStream_t s = (cudaStream_t)stream;
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   if (h_nodes) {
     CK(ensure(t->export_buf, (size_t)t->n_nodes * sizeof(lod_node)));
     SplitView v = make_view(t, nullptr);
@@ -1100,7 +1128,8 @@ int lod_tree_voxels(const lod_tree* t, const void** p) {
 int lod_tree_copy_leaf_points(const lod_tree* t, void* host, void* stream) {
   if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
   size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   CK(cudaMemcpyAsync(host, t->leaf_pts.p, t->n * rec, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   return LOD_OK;
@@ -1108,9 +1137,27 @@ int lod_tree_copy_leaf_points(const lod_tree* t, void* host, void* stream) {
 
 int lod_tree_copy_voxels(const lod_tree* t, void* host, void* stream) {
   if (!t || t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   if (t->n_voxels)
     CK(cudaMemcpyAsync(host, stored_voxels(t), t->n_voxels * 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return LOD_OK;
+}
+
+int lod_tree_copy_range(const lod_tree* t, int what, uint64_t first, uint64_t count, void* host, void* stream) {
+  if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
+  if (what != 0 && what != 1) return fail(LOD_EVALUE, "unknown output %d", what);
+  if (what == 1 && t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
+  const uint64_t total = what == 0 ? t->n : t->n_voxels;
+  if (first > total || count > total - first)
+    return fail(LOD_EVALUE, "range [%llu, +%llu) outside the %llu %s", (unsigned long long)first,
+                (unsigned long long)count, (unsigned long long)total, what == 0 ? "points" : "voxels");
+  const size_t rec = what == 1 ? 8 : t->fmt == LOD_POINTS_F32 ? 16 : 32;
+  const char* src = static_cast<const char*>(what == 0 ? t->leaf_pts.p : stored_voxels(t));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
+  if (count) CK(cudaMemcpyAsync(host, src + first * rec, count * rec, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
   return LOD_OK;
 }
@@ -1123,7 +1170,8 @@ int lod_tree_encode_payload(const lod_tree* tc, const int32_t* h_order, const ui
     return fail(LOD_EVALUE, "encode needs voxels: run lod_voxelize first");
   if (n > t->n_nodes) return fail(LOD_EVALUE, "node order longer than the node table");
   cudaStream_t s = (cudaStream_t)stream;
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   CK(ensure(t->export_buf, (size_t)n * 12 + 16));
   int32_t* d_order = t->export_buf.as<int32_t>();
   uint64_t* d_offs = reinterpret_cast<uint64_t*>(t->export_buf.as<uint8_t>() + (((size_t)n * 4 + 15) & ~(size_t)15));
@@ -1167,7 +1215,8 @@ int lod_tree_checks(const lod_tree* tc, uint32_t T, int32_t max_depth, uint8_t* 
   lod_tree* t = const_cast<lod_tree*>(tc);
   if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
   cudaStream_t s = (cudaStream_t)stream;
-  CK(cudaSetDevice(t->device));
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
   CK(ensure(t->export_buf, (size_t)t->n_nodes + 16));
   SplitView v = make_view(t, nullptr);
   // uniqueness is checked on the key-ordered arena (first-come's stored order is a permutation)

@@ -42,6 +42,9 @@ enum : uint32_t {
   ERR_ZERO_WEIGHT = 1u << 11,  // sampling.py:129-130
   ERR_F32_SUMS = 1u << 12,     // internal: an f32 colour sum reached 2^24, re-run with u64 sums
 };
+// bits only the split raises (lod_build reports them after the voxelizer, api.cu)
+constexpr uint32_t kSplitErrors = ERR_NONFINITE | ERR_OUTSIDE | ERR_EXT_ROOT | ERR_OVERSIZED | ERR_NO_PARENT |
+                                  ERR_UNRESOLVED | ERR_COUNT | ERR_NO_ROOT;
 
 // Device-resident scalars of one build; read back with a single small D2H copy.
 struct DevState {

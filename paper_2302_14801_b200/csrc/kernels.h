@@ -196,7 +196,7 @@ struct VoxLevel {
 int launch_voxelize_front(const VoxLevel& L, int sms, cudaStream_t s);
 int launch_voxelize_accumulate(const VoxLevel& L, int sms, cudaStream_t s);
 int launch_voxelize_back(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s);
-uint32_t voxelize_acc_bytes(int mode);
+uint32_t voxelize_acc_bytes(int mode, bool exact_sums);
 int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s);
 uint32_t voxelize_chunk(uint32_t nodes);
 uint32_t voxelize_vchunk(uint32_t nodes);

@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
     if (o >= d) incl += t;
   }
   const uint32_t S = __shfl_sync(0xFFFFFFFFu, incl, 7, 8);
-  const bool empty = __any_sync(0xFFFFFFFFu, c >= 0 && cnt == 0) &&
-                     (__ballot_sync(0xFFFFFFFFu, c >= 0 && cnt == 0) >> (threadIdx.x & 24) & 0xFF);
+  const uint32_t emask = (__ballot_sync(0xFFFFFFFFu, c >= 0 && cnt == 0) >> (threadIdx.x & 24)) & 0xFF;
+  const bool empty = emask != 0;
+  // the reference raises on the first empty child in octant order (sampling.py:33-35)
+  const int32_t empty_child = __shfl_sync(0xFFFFFFFFu, c, (threadIdx.x & 24) + (empty ? __ffs(emask) - 1 : 0));
   if (!live) return;
   VoxNode& info = L.info[s];
   info.cbase[o] = incl - cnt;
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
     info.m = 0;
     info.skip = skip;
     L.node_slot[node] = s;
-    if (empty) raise_err(L.st, ERR_EMPTY_CHILD, node);
+    if (empty) raise_err(L.st, ERR_EMPTY_CHILD, (uint32_t)empty_child);
     else if (skip) raise_err(L.st, ERR_RANDOM_LIMIT, node, S);
   }
   if (skip || cnt == 0) return;
@@ -405,9 +407,9 @@ __global__ void __launch_bounds__(kT) k_prefix(VoxLevel L) {
   }
   const uint64_t a0 = nd.vbase - L.level_start[0] + L.blk_sum[blockIdx.x];
   for (uint32_t i = threadIdx.x; i < tot; i += kT) {
-    if (L.mode == LOD_MODE_AVERAGE) {
+    if (L.mode == LOD_MODE_AVERAGE && !L.exact_sums) {
       reinterpret_cast<uint4*>(L.acc)[a0 + i] = make_uint4(0, 0, 0, 0);
-    } else if (L.mode == LOD_MODE_WEIGHTED) {
+    } else if (L.mode == LOD_MODE_WEIGHTED || L.mode == LOD_MODE_AVERAGE) {
       reinterpret_cast<uint4*>(L.acc)[2 * (a0 + i)] = make_uint4(0, 0, 0, 0);
       reinterpret_cast<uint4*>(L.acc)[2 * (a0 + i) + 1] = make_uint4(0, 0, 0, 0);
     } else {
@@ -480,9 +482,13 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
                        "f"((float)((rgb >> 8) & 0xFF)), "f"((float)((rgb >> 16) & 0xFF)), "f"(1.0f)
                        : "memory");
         } else if (L.mode == LOD_MODE_AVERAGE) {
-          unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 2 * a;
-          atomicAdd(p, (unsigned long long)(rgb & 0xFF) | ((unsigned long long)((rgb >> 8) & 0xFF) << 32));
-          atomicAdd(p + 1, (unsigned long long)((rgb >> 16) & 0xFF) | (1ull << 32));
+          // exact fallback: four u64 sums {r, g, b, count} per voxel (32 B), exact for any
+          // sample count (the reference sums in int64, sampling.py:92-96)
+          unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 4 * a;
+          atomicAdd(p, (unsigned long long)(rgb & 0xFF));
+          atomicAdd(p + 1, (unsigned long long)((rgb >> 8) & 0xFF));
+          atomicAdd(p + 2, (unsigned long long)((rgb >> 16) & 0xFF));
+          atomicAdd(p + 3, 1ull);
         } else if (L.mode == LOD_MODE_RANDOM) {  // a child voxel's ordinal is its index in the child
           atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, rand_enc(nd.hash, ob + j));
         } else {  // first-come: the smallest ordinal is the largest complement; a child voxel's
@@ -627,8 +633,9 @@ __device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode&
   uint32_t rgb;
   if (L.mode == LOD_MODE_AVERAGE) {
     if (L.exact_sums) {
-      const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2*>(L.acc) + acc0 + r);
-      sr += a.x & 0xFFFFFFFFull, sg += a.x >> 32, sb += a.y & 0xFFFFFFFFull, n += a.y >> 32;
+      const ulonglong2* a = reinterpret_cast<const ulonglong2*>(L.acc) + 2 * (acc0 + r);
+      const ulonglong2 a0 = __ldcg(a), a1 = __ldcg(a + 1);
+      sr += a0.x, sg += a0.y, sb += a1.x, n += a1.y;
     } else {
       const float4 a = __ldcg(reinterpret_cast<const float4*>(L.acc) + acc0 + r);
       if (fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)) >= 16777216.0f) raise_err(L.st, ERR_F32_SUMS, nd.node);
@@ -849,8 +856,8 @@ int launch_voxelize_back(const VoxLevel& L, int sms, ScanScratch& scr, cudaStrea
   return launches;
 }
 
-uint32_t voxelize_acc_bytes(int mode) {
-  return mode == LOD_MODE_AVERAGE ? 16 : mode == LOD_MODE_WEIGHTED ? 32 : 4;
+uint32_t voxelize_acc_bytes(int mode, bool exact_sums) {
+  return mode == LOD_MODE_AVERAGE ? (exact_sums ? 32 : 16) : mode == LOD_MODE_WEIGHTED ? 32 : 4;
 }
 
 // chunk sizes: small levels get small chunks so every SM has work

@@ -49,13 +49,38 @@ def unpack_records(raw: np.ndarray, fmt: int):
     return pos, col
 
 
+def generate_device(kind: str, n: int, seed: int, start: int = 0, out=None):
+    """Rows [start, start+n) of a BASELINE synthetic cloud generated in HBM as 16-B F32 records
+    (uint8 torch tensor of n*16 bytes; `lod_generate`, bit-identical to generators.py)."""
+    torch = _torch()
+    from .generators import scene_objects
+    lib = _abi.load()
+    buf = torch.empty(n * 16, dtype=torch.uint8, device="cuda") if out is None else out
+    table = None
+    if kind == "scene":
+        kinds, params, cdf = scene_objects(seed)
+        tab = np.zeros((65, 9))
+        tab[:, 0], tab[:, 1:8], tab[:, 8] = kinds, params, cdf
+        table = torch.from_numpy(tab.reshape(-1)).to(buf.device)
+    stream = C.c_void_p(torch.cuda.current_stream(buf.device).cuda_stream)
+    tptr = C.cast(C.c_void_p(table.data_ptr()), C.POINTER(C.c_double)) if table is not None else None
+    chunk = 1 << 28
+    for s in range(0, n, chunk):
+        m = min(chunk, n - s)
+        _abi.check(lib.lod_generate(kind.encode(), seed, start + s, m, C.c_void_p(buf.data_ptr() + s * 16), tptr,
+                                    stream))
+    torch.cuda.current_stream(buf.device).synchronize()
+    return buf
+
+
 def make_config(T=50_000, initial_depth=8, extension_depth=4, max_depth=16) -> LodConfig:
     return LodConfig(int(T), int(initial_depth), int(extension_depth), int(max_depth))
 
 
-def current_stream_ptr():
+def current_stream_ptr(device: int | None = None):
+    """torch's current stream ON `device` (default: the current device) as a void*."""
     torch = _torch()
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 class DeviceTree:
@@ -69,6 +94,7 @@ class DeviceTree:
         if not self.h:
             raise RuntimeError(self.lib.lod_last_error().decode())
         self._input = None
+        self.generation = 0   # bumped by every split: trees built earlier on this handle are stale
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -91,19 +117,21 @@ class DeviceTree:
         b = None
         if bounds is not None:
             b = (C.c_double * 4)(*[float(x) for x in bounds])
+        self.generation += 1
         self._input = d_records  # keep alive for the duration of the call
         _abi.check(self.lib.lod_split(self.h, C.c_void_p(d_records.data_ptr()), n, fmt, b, C.byref(config),
-                                      stream if stream is not None else current_stream_ptr()))
+                                      stream if stream is not None else current_stream_ptr(self.device)))
         self._input = None
 
     def voxelize(self, mode: int, seed: int, stream=None):
         _abi.check(self.lib.lod_voxelize(self.h, mode, int(seed) & ((1 << 64) - 1),
-                                         stream if stream is not None else current_stream_ptr()))
+                                         stream if stream is not None else current_stream_ptr(self.device)))
 
     def build(self, d_records, n: int, fmt: int, config: LodConfig, mode: int, seed: int, stream=None):
+        self.generation += 1
         _abi.check(self.lib.lod_build(self.h, C.c_void_p(d_records.data_ptr()), n, fmt, C.byref(config), mode,
                                       int(seed) & ((1 << 64) - 1),
-                                      stream if stream is not None else current_stream_ptr()))
+                                      stream if stream is not None else current_stream_ptr(self.device)))
 
     def info(self) -> LodTreeInfo:
         out = LodTreeInfo()
@@ -113,21 +141,36 @@ class DeviceTree:
     def nodes(self) -> np.ndarray:
         info = self.info()
         arr = np.zeros(info.n_nodes, _abi.node_dtype())
-        _abi.check(self.lib.lod_tree_copy_nodes(self.h, arr.ctypes.data_as(C.c_void_p), current_stream_ptr()))
+        _abi.check(self.lib.lod_tree_copy_nodes(self.h, arr.ctypes.data_as(C.c_void_p), current_stream_ptr(self.device)))
         return arr
 
     def leaf_records(self) -> np.ndarray:
         info = self.info()
         size = 16 if info.point_format == LOD_POINTS_F32 else 32
         raw = np.empty(info.n_points * size, np.uint8)
-        _abi.check(self.lib.lod_tree_copy_leaf_points(self.h, raw.ctypes.data_as(C.c_void_p), current_stream_ptr()))
+        _abi.check(self.lib.lod_tree_copy_leaf_points(self.h, raw.ctypes.data_as(C.c_void_p), current_stream_ptr(self.device)))
         return raw
 
     def voxels(self) -> np.ndarray:
         info = self.info()
         raw = np.empty((info.n_voxels, 2), np.uint32)
         if info.n_voxels:
-            _abi.check(self.lib.lod_tree_copy_voxels(self.h, raw.ctypes.data_as(C.c_void_p), current_stream_ptr()))
+            _abi.check(self.lib.lod_tree_copy_voxels(self.h, raw.ctypes.data_as(C.c_void_p), current_stream_ptr(self.device)))
+        return raw
+
+    def leaf_range(self, first: int, count: int) -> np.ndarray:
+        """Raw records [first, first+count) of the leaf buffer (one node's points)."""
+        size = 16 if self.info().point_format == LOD_POINTS_F32 else 32
+        raw = np.empty(count * size, np.uint8)
+        _abi.check(self.lib.lod_tree_copy_range(self.h, 0, first, count, raw.ctypes.data_as(C.c_void_p),
+                                                current_stream_ptr(self.device)))
+        return raw
+
+    def voxel_range(self, first: int, count: int) -> np.ndarray:
+        """(count, 2) u32 {key, rgb} voxels [first, first+count) in stored order."""
+        raw = np.empty((count, 2), np.uint32)
+        _abi.check(self.lib.lod_tree_copy_range(self.h, 1, first, count, raw.ctypes.data_as(C.c_void_p),
+                                                current_stream_ptr(self.device)))
         return raw
 
     def device_ptrs(self):

@@ -38,6 +38,7 @@ class GpuOctree(Octree):
 
     def __init__(self, dev: DeviceTree, config: BuildConfig):
         self._dev = dev
+        self._generation = dev.generation
         self.config = config
         info = dev.info()
         self.world_bounds = AABB(tuple(float(v) for v in info.world_min), float(info.world_size))
@@ -46,13 +47,22 @@ class GpuOctree(Octree):
         self._objs = None        # node id -> OctreeNode
         self.strategy_built = None
 
+    def _check_live(self):
+        """A DeviceTree's buffers are reused by its next split: a tree built earlier on the same
+        handle must not silently show the new build's data."""
+        if self._dev.generation != self._generation:
+            raise RuntimeError("this tree's device buffers were reused by a later build on the same DeviceTree; "
+                               "materialise it (tree.root) before reusing the handle, or use a new DeviceTree")
+
     @property
     def device_tree(self) -> DeviceTree:
+        self._check_live()
         return self._dev
 
     @property
     def root(self) -> OctreeNode:
         if self._root is None:
+            self._check_live()
             self._materialize()
         return self._root
 
@@ -98,8 +108,14 @@ class GpuOctree(Octree):
     # cheap summaries straight from the node table (no materialisation)
     @property
     def node_count(self) -> int:
+        if self._objs is not None:
+            return len(self._objs)
+        self._check_live()
         return int(self._dev.info().n_nodes)
 
     @property
     def point_count(self) -> int:
+        if self._objs is not None:
+            return sum(len(o.point_positions) for o in self._objs if o.children is None)
+        self._check_live()
         return int(self._dev.info().n_points)

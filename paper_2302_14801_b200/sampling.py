@@ -11,6 +11,8 @@ fallback; unknown names raise ValueError like the reference (sampling.py:169-170
 """
 from __future__ import annotations
 
+import dataclasses
+
 import numpy as np
 
 from ._abi import LOD_MODE_AVERAGE, LOD_MODE_FIRST_COME, LOD_MODE_RANDOM, LOD_MODE_WEIGHTED
@@ -67,7 +69,13 @@ def build_lod_points(points, colors, T: int = 50_000, grid: int = GRID_SIZE, mod
         pos = pos.reshape(-1, 3)
     if len(pos) == 0:
         raise ValueError("cannot partition an empty point cloud")
-    cfg = config or BuildConfig(T=T, strategy=MODE_ALIASES[mode], seed=seed)
+    if config is None:
+        cfg = BuildConfig(T=T, strategy=MODE_ALIASES[mode], seed=seed)
+    else:
+        if T != 50_000 and T != config.T:
+            raise ValueError(f"T={T} conflicts with config.T={config.T}")
+        # the tree's config records what was actually built (codec.encode writes it)
+        cfg = dataclasses.replace(config, strategy=MODE_ALIASES[mode], seed=seed)
     dev = device_tree or DeviceTree()
     d_rec, fmt, n = dev.upload(pos, colors)
     dev.build(d_rec, n, fmt, make_config(cfg.T, cfg.initial_depth, cfg.extension_depth, cfg.max_depth), code, seed)

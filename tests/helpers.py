@@ -66,3 +66,54 @@ def compare_weighted(got, exp):
         if d.max(initial=0) > 1:
             errors.append((k, "colour off by", int(d.max())))
     return errors, off, total
+
+
+def cell_path_str(cell, depth):
+    cx, cy, cz = (int(c) for c in cell)
+    return "".join(str(((cx >> b) & 1) | (((cy >> b) & 1) << 1) | (((cz >> b) & 1) << 2))
+                   for b in range(depth - 1, -1, -1)) or "-"
+
+
+def subtree_index(nodes, depth, cell):
+    """Node-table ids of the subtree rooted at (depth, cell), vectorised over the table."""
+    d = nodes["depth"].astype(np.int64)
+    c = nodes["cell"].astype(np.int64)
+    sh = np.maximum(d - depth, 0)[:, None]
+    inside = (d >= depth) & np.all((c >> sh) == np.asarray(cell, np.int64)[None, :], axis=1)
+    return np.flatnonzero(inside)
+
+
+def device_subtree_split(dev, nodes, ids):
+    """Split digests (make_golden format) of node ids, reading only those nodes' points."""
+    from paper_2302_14801_b200.device import unpack_records
+    fmt = dev.info().point_format
+    out = {}
+    for k in ids:
+        nd = nodes[k]
+        b = [float(v).hex() for v in nd["min"]] + [float(nd["size"]).hex()]
+        p = cell_path_str(nd["cell"], int(nd["depth"]))
+        if nd["flags"] & 1:
+            pos, col = unpack_records(dev.leaf_range(int(nd["first"]), int(nd["count"])), fmt)
+            out[p] = ["L", int(nd["count"]), bool(nd["flags"] & 2), b, sha(pos, col)]
+        else:
+            out[p] = ["I", 0, False, b, ""]
+    return out
+
+
+def decode_voxels(raw):
+    key, rgb = raw[:, 0], raw[:, 1]
+    coords = np.stack([key >> 14, (key >> 7) & 127, key & 127], axis=1).astype(np.uint8)
+    colors = np.stack([rgb & 255, (rgb >> 8) & 255, (rgb >> 16) & 255], axis=1).astype(np.uint8)
+    return coords, colors
+
+
+def device_subtree_voxels(dev, nodes, ids):
+    """Voxel digests [m, sha1(coords || colors)] of the inner nodes among `ids`."""
+    out = {}
+    for k in ids:
+        nd = nodes[k]
+        if nd["flags"] & 1:
+            continue
+        c, col = decode_voxels(dev.voxel_range(int(nd["first"]), int(nd["count"])))
+        out[cell_path_str(nd["cell"], int(nd["depth"]))] = [int(nd["count"]), sha(c, col)]
+    return out

@@ -47,6 +47,16 @@ def test_average_sum_overflow_falls_back_to_exact():
     assert over and max(nd.point_count for nd in over) == 70_000
 
 
+def test_average_exact_sums_past_2_32():
+    """17M coincident samples of colour 255 in one voxel: the channel sums (4.3e9) pass 2^32,
+    so the exact fallback must keep full u64 sums per channel (the reference sums in int64,
+    sampling.py:92-96)."""
+    pos, col = _cloud(17_000_000, 30_000)
+    tree = _compare(pos, col, 1000, "average")
+    over = [nd for nd in tree.leaves() if nd.oversized]
+    assert over and max(nd.point_count for nd in over) == 17_000_000
+
+
 @pytest.mark.parametrize("strategy", ["first-come", "random", "weighted"])
 def test_oversized_duplicates_all_strategies(strategy):
     pos, col = _cloud(3_000, 20_000, seed=1)
