@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--cpu-runs", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-api-config", default="terrain20M",
+                    help="config of the Python-API e2e leg ('' to skip)")
     ap.add_argument("--stages", action="store_true", help="also print per-stage device times to stderr")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="collectives for --gpus > 1 (gloo = host-staged, for testing on one GPU)")
@@ -388,6 +390,50 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
             rec_bytes, _tree_bytes(dev, n))
 
 
+def e2e_api(torch, config, mode, steps, warmup):
+    """The Python drop-in from host numpy arrays: the fused
+    `build_lod(points, colors, mode=...)` with float32 positions, and the reference form
+    `partition(PointCloud(float64 positions, colors))` + `build_lod(tree, strategy)`.  Each
+    call uploads its arrays (pinned staging) and packs them on the device; the timed region
+    ends with a device->host read of the built tree's node count (the tree stays in HBM, as a
+    user's lazily materialised Octree does)."""
+    from paper_2302_14801_b200 import BuildConfig, Partitioner, PointCloud, build_lod
+    from paper_2302_14801_b200.device import DeviceTree, generate_device
+    from paper_2302_14801_b200.generators import CONFIGS
+    kind, n, seed, _ = CONFIGS[config]
+    raw = generate_device(kind, n, seed).view(torch.float32).view(n, 4)
+    pos32 = raw[:, :3].cpu().numpy().copy()
+    col = raw.view(torch.uint8).view(n, 16)[:, 12:15].cpu().numpy().copy()
+    pos64 = pos32.astype(np.float64)
+    del raw
+    dev = DeviceTree()
+    strat = "average" if mode in ("color_filter", "average") else mode
+    out = {}
+
+    def fused():
+        return build_lod(pos32, col, mode=mode, seed=0, device_tree=dev).node_count
+
+    def reference_form():
+        tree = Partitioner(PointCloud(pos64, col), BuildConfig(T=50_000), device_tree=dev).run()
+        return build_lod(tree, strat, 0).node_count
+
+    for name, fn, hb in (("fused_f32", fused, 15 * n), ("partition_f64", reference_form, 27 * n)):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            fn()
+        torch.cuda.synchronize()
+        sec = (time.perf_counter() - t0) / steps
+        out[name] = {"value": n / sec, "unit": "points/s", "ms_per_step": 1000 * sec, "h2d_bytes_per_step": hb,
+                     "d2h_bytes_per_step": 8}
+    out["config"] = config
+    out["note"] = ("wall clock around the public Python API calls from host numpy arrays (upload + device pack + "
+                   "build + node-count read); the built tree stays in HBM")
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -514,6 +560,10 @@ def main():
         e2e = {"value": n_total / (ems / 1000.0), "unit": "points/s", "h2d_bytes_per_step": hb,
                "d2h_bytes_per_step": db, "ms_per_step": ems, "pipeline": pipeline}
 
+    api = None
+    if world == 1 and not args.no_e2e and args.e2e_api_config:
+        api = e2e_api(torch, args.e2e_api_config, args.mode, max(3, min(args.steps, 10)), 2)
+
     # ---- roofline (SURVEY 8(d) algorithmic bytes: B = 80 N + 16 E + 12 V) ----
     # Dominant single kernel: the distribute's K_scatter (stable counting-sort scatter), the
     # longest kernel of a build (ncu launch lists in profiles/).  Algorithmic bytes: each
@@ -563,7 +613,7 @@ def main():
                        "T": 50_000, "grid": 128, "l2": "input 16 B/pt x points > 126 MB L2, no flush",
                        "parallelism": f"subtree-sharded x{world} ({args.backend} all-reduce + all-to-all + rank-0 merge)"
                        if world > 1 else "single"},
-            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "e2e": e2e, "e2e_api": api, "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "stages_ms": dict(zip(stage_names, stages)),
             "tree": {"nodes": info.n_nodes, "leaves": info.n_leaves, "depth": info.depth, "voxels": V,

@@ -206,6 +206,16 @@ int lod_tree_kernel_ms(const lod_tree* tree, float* out1);
 /* Number of kernel launches issued by the last lod_split + lod_voxelize. */
 uint64_t lod_tree_launches(const lod_tree* tree);
 
+/* Pack caller arrays into point records on the device (the drop-in's upload path; the
+ * reference's PointCloud is float64 (n,3) + uint8 (n,3), ingest.py:21-35).
+ * d_xyz: n x 3 coordinates, float64 (xyz_is_f64 = 1) or float32; d_rgb: n x 3 uint8.
+ * out_format: LOD_POINTS_F32, LOD_POINTS_F64, or -1 = F32 when every float64 coordinate
+ * survives a float32 round trip (exact), else F64 (float32 input is always F32).
+ * d_records must hold n records of the chosen format (32 B/pt covers both); *chosen_format
+ * receives it.  Waits for the exactness test (one 4-byte read); the packing is enqueued. */
+int lod_pack_points(const void* d_xyz, int xyz_is_f64, const uint8_t* d_rgb, uint64_t n, int out_format,
+                    void* d_records, int* chosen_format, void* stream);
+
 /* Deterministic synthetic generators on the device, rows
  * [start, start+n) of cloud `kind` ("sphere", "terrain", "scene", "cluster", "surface")
  * written as LOD_POINTS_F32 records.  `table`: scene object table from the host

@@ -81,6 +81,7 @@ SIGNATURES = [
     ("lod_tree_stage_ms", C.c_int, [_P, C.POINTER(C.c_float)]),
     ("lod_tree_kernel_ms", C.c_int, [_P, C.POINTER(C.c_float)]),
     ("lod_tree_launches", C.c_uint64, [_P]),
+    ("lod_pack_points", C.c_int, [_P, C.c_int, _P, C.c_uint64, C.c_int, _P, C.POINTER(C.c_int), _P]),
     ("lod_generate", C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint64, _P, C.POINTER(C.c_double), _P]),
     ("lod_dist_begin", C.c_int, [_P, _P, C.c_uint64, C.c_int, C.POINTER(LodConfig), _P, _P]),
     ("lod_dist_count", C.c_int, [_P, C.c_uint64, _P, C.POINTER(LodSpan), _P]),

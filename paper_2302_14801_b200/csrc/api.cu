@@ -94,7 +94,9 @@ struct lod_tree {
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
   DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
   DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
-  DevBuf leaf_pts, status, digit_base, tmp_rec, tmp_leaf, pkey, pc16;
+  DevBuf leaf_pts, status, digit_base, tmp_rec, tmp_leaf, pkey, elist, abits;
+  uint64_t elist_cap = 0;
+  bool use_abits = false;
   DevBuf vox, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vvchunks;
   DevBuf vpos, vout, obits;  // first-come: stored positions, stored-order voxels, ordinal bitmaps
@@ -254,7 +256,9 @@ SplitView make_view(lod_tree* t, const void* pts) {
   v.node_idx = t->node_idx.as<int32_t>();
   v.t8 = t->t8.as<int32_t>();
   v.pkey = t->pkey.as<uint32_t>();
-  v.pc16 = t->pc16.as<uint64_t>();
+  v.elist = t->elist_cap ? t->elist.as<uint4>() : nullptr;
+  v.elist_cap = t->elist_cap;
+  v.abits = t->use_abits ? t->abits.as<uint32_t>() : nullptr;
   v.te = t->te.as<int32_t>();
   v.meta = t->meta.as<ExtMeta>();
   v.n_ext = t->n_ext;
@@ -335,6 +339,8 @@ int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* 
   t->n_ext = 0;
   t->n_nodes = t->n_leaves = 0;
   t->rounds.clear();
+  t->elist_cap = 0;
+  t->use_abits = false;
   t->ext_pyr_used = t->ext_tgt_used = 0;
   t->round_cur = 0;
   const int D = cfg->initial_depth;
@@ -386,6 +392,12 @@ int phase_anchors(lod_tree* t, uint32_t* cur, cudaStream_t s) {
   if ((r = check_errors(t, s))) return r;
   *cur = (uint32_t)t->host_state->count_a;
   if (*cur) RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s, true));  // none: no store pass
+  // anchor bitmap for the first extension round's membership test (2 MB at depth 8)
+  t->use_abits = *cur && 3 * D <= 27;
+  if (t->use_abits) {
+    CK(ensure(t->abits, (fine_cells + 7) / 8));
+    CK(cudaMemsetAsync(t->abits.p, 0, (fine_cells + 7) / 8, s));
+  }
   t->round_base = D;
   t->round_first = 0;
   t->round_parent_first = 0;
@@ -408,8 +420,19 @@ int phase_round(lod_tree* t, cudaStream_t s) {
   CK(ensure(t->meta, (size_t)(first + cur) * sizeof(ExtMeta), (size_t)first * sizeof(ExtMeta), s));
   CK(cudaMemsetAsync(t->pyr.as<uint32_t>() + pyr_base, 0, new_pyr * 4, s));
   CK(cudaMemsetAsync(t->te.as<int32_t>() + tgt_base, 0xFF, new_tgt * 4, s));
-  if (t->rounds.empty()) CK(ensure(t->pc16, std::max<uint64_t>(t->n, 1) * 8));  // depth-16 cells of ext points
   SplitView v = make_view(t, t->pts);
+  if (t->rounds.empty()) {
+    // extension-list capacity: the points under the anchors (all-reduced counts in the
+    // multi-GPU path: an upper bound of the local ones)
+    DevState* st = t->state.as<DevState>();
+    CK(cudaMemsetAsync(&st->ext_n, 0, sizeof(st->ext_n), s));
+    RUN(launch_anchor_sum(v, t->list.as<uint64_t>(), cur, s));
+    int r = read_state(t, s);
+    if (r) return r;
+    t->elist_cap = std::min<uint64_t>(t->n, t->host_state->ext_n);
+    CK(ensure(t->elist, std::max<uint64_t>(t->elist_cap, 1) * 16));
+    CK(cudaMemsetAsync(&st->ext_n, 0, sizeof(st->ext_n), s));
+  }
   RUN(launch_ext_create(v, (int)t->rounds.size(), first, cur, t->list.as<uint64_t>(), t->round_parent_first,
                         pyr_base, tgt_base, base, ext, s));
   t->n_ext = first + cur;
@@ -1020,7 +1043,7 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->digit_base, &t->tmp_rec, &t->tmp_leaf, &t->vox, &t->export_buf,
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
                    &t->node_slot, &t->vacc, &t->vchunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->pkey, &t->pc16};
+                   &t->vpos, &t->vout, &t->obits, &t->pkey, &t->elist, &t->abits};
   for (DevBuf* b : all)
     if (b->p) cudaFree(b->p);
   for (auto& e : t->ev)
@@ -1237,7 +1260,7 @@ uint64_t lod_tree_device_bytes(const lod_tree* t) {
                          &t->vox, &t->export_buf, &t->stash, &t->vbits, &t->vpre, &t->vinfo,
                          &t->vblk, &t->vcount, &t->vlevel_start, &t->node_slot, &t->vacc, &t->vchunks,
                          &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
-                   &t->vpos, &t->vout, &t->obits, &t->pkey, &t->pc16};
+                   &t->vpos, &t->vout, &t->obits, &t->pkey, &t->elist, &t->abits};
   uint64_t b = 0;
   for (const DevBuf* x : all) b += x->cap;
   return b;
@@ -1273,6 +1296,33 @@ int lod_tree_kernel_ms(const lod_tree* tc, float* out) {
 }
 
 uint64_t lod_tree_launches(const lod_tree* t) { return t ? t->launches : 0; }
+
+int lod_pack_points(const void* d_xyz, int xyz_is_f64, const uint8_t* d_rgb, uint64_t n, int out_format,
+                    void* d_records, int* chosen_format, void* stream) {
+  if (n && (!d_xyz || !d_rgb || !d_records)) return fail(LOD_EVALUE, "null buffer");
+  if (out_format != -1 && out_format != LOD_POINTS_F32 && out_format != LOD_POINTS_F64)
+    return fail(LOD_EVALUE, "unknown point format %d", out_format);
+  cudaStream_t s = (cudaStream_t)stream;
+  int fmt = out_format;
+  if (fmt == -1) {
+    fmt = LOD_POINTS_F32;
+    if (xyz_is_f64 && n) {
+      uint32_t* flag = nullptr;
+      uint32_t h = 1;
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&flag), 4, s));
+      CK(cudaMemcpyAsync(flag, &h, 4, cudaMemcpyHostToDevice, s));
+      launch_f32_exact(static_cast<const double*>(d_xyz), n, flag, s);
+      CK(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaFreeAsync(flag, s));
+      CK(cudaStreamSynchronize(s));
+      if (!h) fmt = LOD_POINTS_F64;
+    }
+  }
+  if (chosen_format) *chosen_format = fmt;
+  launch_pack(d_xyz, xyz_is_f64 != 0, d_rgb, n, fmt, d_records, s);
+  CK(cudaGetLastError());
+  return LOD_OK;
+}
 
 int lod_generate(const char* kind, uint64_t seed, uint64_t start, uint64_t n, void* d_out, const double* table,
                  void* stream) {

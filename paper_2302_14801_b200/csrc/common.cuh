@@ -53,6 +53,7 @@ struct DevState {
   double lo[3];                   // world cube (model.py:199-209 or caller bounds)
   double size;
   double inv_size;                // RN(1 / size), fast-path projection
+  unsigned long long ext_n;       // entries of the extension-point list (first extension round)
   uint32_t err;
   uint32_t err_detail;            // node id for voxelize errors
   unsigned long long err_value;   // e.g. the sample count of the 2^20 violation
@@ -71,6 +72,57 @@ __device__ __forceinline__ void raise_err(DevState* st, uint32_t bit, uint32_t d
     st->err_value = value;
   }
 }
+
+// Per-CTA cache of hot counters in shared memory.  Counting passes whose points pile into a
+// few cells (dense clusters interleaved with other points, so warps see distinct hot keys
+// and warp aggregation cannot help) would serialise millions of L2 atomics on a handful of
+// addresses.  Each key may live in one of two slots; a slot is claimed once (CAS from EMPTY)
+// and counts in shared memory until the periodic flush; keys that find both slots taken go
+// to global memory directly.  Resetting every few ten thousand points gives hot keys that
+// lost their slots to cold ones another chance.
+template <int SLOTS>
+struct HotCounts {
+  static constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+  uint32_t key[SLOTS];
+  uint32_t cnt[SLOTS];
+  __device__ __forceinline__ void clear() {
+    for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) key[i] = kEmpty, cnt[i] = 0;
+  }
+  __device__ __forceinline__ void add(uint32_t* global, uint32_t k, uint32_t inc) {
+    static_assert((SLOTS & (SLOTS - 1)) == 0, "power of two");
+    constexpr int B = __builtin_ctz(SLOTS);
+    const uint32_t s1 = (k * 0x9E3779B1u) >> (32 - B);
+    const uint32_t s2 = (s1 + 1 + ((k * 0x85EBCA77u) >> (33 - B))) & (SLOTS - 1);
+    uint32_t s = s1, cur = key[s1];
+    if (cur != k) {
+      if (cur == kEmpty) {
+        cur = atomicCAS(key + s1, kEmpty, k);
+        if (cur == kEmpty) cur = k;
+      }
+      if (cur != k) {
+        s = s2;
+        cur = key[s2];
+        if (cur == kEmpty) {
+          cur = atomicCAS(key + s2, kEmpty, k);
+          if (cur == kEmpty) cur = k;
+        }
+      }
+    }
+    if (cur == k) atomicAdd(cnt + s, inc);
+    else atomicAdd(global + k, inc);
+  }
+  // every thread of the CTA: all adds done -> counts to global, slots emptied
+  __device__ __forceinline__ void flush(uint32_t* global) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < SLOTS; i += blockDim.x) {
+      const uint32_t k = key[i], c = cnt[i];
+      if (k != kEmpty && c) atomicAdd(global + k, c);
+      key[i] = kEmpty;
+      cnt[i] = 0;
+    }
+    __syncthreads();
+  }
+};
 
 // order-preserving u64 key of a double (for atomicMin / atomicMax)
 __device__ __forceinline__ unsigned long long dkey(double d) {

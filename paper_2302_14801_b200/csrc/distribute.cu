@@ -37,21 +37,14 @@ constexpr int kW = kRadixThreads / 32;
 constexpr int K = kRadixItems;
 
 
-// Leaf of point i inside an extension grid (target t <= -2): descend from the depth-16 cell
-// the first extension round stored (pc16); -1 if unresolved.
-__device__ __forceinline__ int32_t leaf_from_c16(const SplitView& v, uint64_t i, int32_t t) {
-  const Cell16 c = unpack_c16(__ldg(v.pc16 + i));
-  uint32_t e, rr;
-  if (ext_descend(v, c, e, rr, t)) t = v.te[v.meta[e].tgt_off + rr];
-  return t;
-}
-
 // Leaf ids of one warp's K x 32 items starting at `base`.  FIRST: through the target table
-// from the point's finest main-grid key (no record read, no fp64 projection except for
-// points inside extension grids); else the ids of the previous pass.
+// from the point's finest main-grid key (no record read, no fp64 projection); points inside
+// extension grids (target <= -2) take the id K_ext_leaf resolved from the extension list
+// (ext_leaf, indexed by point); else the ids of the previous pass.
 template <int FMT, bool FIRST, bool TAGIN>
 __device__ __forceinline__ void load_items(const SplitView& v, const void* in_rec, const uint32_t* in_leaf,
-                                           uint64_t base, int lane, uint32_t (&leaf)[K], bool& unresolved) {
+                                           const uint32_t* ext_leaf, uint64_t base, int lane, uint32_t (&leaf)[K],
+                                           bool& unresolved) {
   const uint64_t last = v.n - 1;
   if (FIRST) {
     uint32_t key[K];
@@ -67,7 +60,7 @@ __device__ __forceinline__ void load_items(const SplitView& v, const void* in_re
     for (int k = 0; k < K; ++k) {
       const uint64_t i = base + (uint64_t)k * 32 + lane;
       int32_t t = (int32_t)leaf[k];
-      if (t <= -2) t = leaf_from_c16(v, i < last ? i : last, t);
+      if (t <= -2) t = (int32_t)__ldcg(ext_leaf + (i < last ? i : last));
       if (t < 0) {
         unresolved |= i < v.n;
         t = 0;
@@ -108,7 +101,7 @@ __global__ void __launch_bounds__(kRadixThreads, 3)
   for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
     uint32_t leaf[K];
-    load_items<FMT, FIRST, TAGIN>(v, in_rec, in_leaf, base, lane, leaf, unresolved);
+    load_items<FMT, FIRST, TAGIN>(v, in_rec, in_leaf, leaf_out, base, lane, leaf, unresolved);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const bool valid = base + (uint64_t)k * 32 + lane < v.n;
@@ -247,7 +240,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
     uint32_t leaf[K];
     uint16_t rk[K];
-    load_items<FMT, false, TAGIN>(v, in_rec, in_leaf, base, lane, leaf, unresolved);
+    load_items<FMT, false, TAGIN>(v, in_rec, in_leaf, nullptr, base, lane, leaf, unresolved);
     // stable in-warp ranks (item-major, lane order)
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -529,6 +522,7 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
     launches += 2;
   }
   if (p.aux) cudaEventRecord(p.aux_ev[1], a);
+  if (v.elist) launches += launch_ext_leaf(v, p.tmp_leaf, s);  // leaf ids of the extension points
   if (p.passes == 1)
     return launches + run_pass<FMT, true, false, OUT_FINAL>(v, v.pts, nullptr, p.tmp_leaf, leaf_out, nullptr, 0,
                                                            p.bits[0], 0, base0, p, s);

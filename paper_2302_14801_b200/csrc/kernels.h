@@ -23,8 +23,10 @@ struct SplitView {
   int32_t* node_idx;      // slot -> node id (valid at non-zero slots)
   int32_t* t8;            // main finest level: leaf id, -(ext+2), or -1
   uint32_t* pkey;         // per point: its main finest-level key (written by K_count)
-  uint64_t* pc16;         // per point inside an extension grid: packed depth-16 cell
-                          // (x | y << 16 | z << 32), written by the first extension round
+  uint4* elist;           // extension points {index, round-1 extension id, x | y << 16, z}
+                          // (depth-16 cell), appended by the first extension round
+  uint64_t elist_cap;
+  uint32_t* abits;        // anchor bitmap over the main finest grid (null: test t8)
   int32_t* te;            // ext finest levels: same encoding
   ExtMeta* meta;
   uint32_t n_ext;
@@ -94,6 +96,10 @@ int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_
                       const uint64_t* list, uint32_t parent_first, uint64_t pyr_base, uint64_t tgt_base,
                       int base_depth, int ext_levels, cudaStream_t s);
 int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first_ext, cudaStream_t s);
+// sum of the anchors' main-grid counts (t->list[0..n)) -> st->ext_n (extension-list capacity)
+int launch_anchor_sum(const SplitView& v, const uint64_t* list, uint32_t n, cudaStream_t s);
+// leaf ids of the extension-list points -> leaf_out[index] (before the distribute's K_hist)
+int launch_ext_leaf(const SplitView& v, uint32_t* leaf_out, cudaStream_t s);
 
 __device__ __forceinline__ Cell16 unpack_c16(uint64_t p) {
   return Cell16{(uint32_t)p & 0xFFFF, (uint32_t)(p >> 16) & 0xFFFF, (uint32_t)(p >> 32) & 0xFFFF};
@@ -225,6 +231,9 @@ int launch_checks(int fmt, const SplitView& v, const void* leaf_pts, const uint2
                   int max_depth, uint8_t* flags, cudaStream_t s);
 
 // --- generators (generate.cu) ---
+int launch_f32_exact(const double* xyz, uint64_t n, uint32_t* flag, cudaStream_t s);
+int launch_pack(const void* xyz, bool f64_in, const uint8_t* rgb, uint64_t n, int out_format, void* out,
+                cudaStream_t s);
 int launch_generate(int kind, uint64_t seed, uint64_t start, uint64_t n, void* out, const double* table,
                     cudaStream_t s);
 

@@ -150,10 +150,15 @@ int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const doub
 // K2: count into the main finest grid, warp-aggregated atomics
 // ---------------------------------------------------------------------------
 constexpr int kCountUnroll = 4;
+constexpr int kHotSlots = 1024;     // per-CTA hot-counter cache (common.cuh HotCounts)
+constexpr int kHotReset = 64;       // loop trips between flushes (64 x 1024 points per CTA)
 
 template <int FMT>
 __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
   pdl_wait();
+  __shared__ HotCounts<kHotSlots> hot;
+  hot.clear();
+  __syncthreads();
   const DevState st = *v.st;
   const Frame32 fr = make_frame32(st.lo[0], st.lo[1], st.lo[2], st.size, v.D);
   const float lim = (float)(1u << v.D);
@@ -161,7 +166,9 @@ __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
   const int lane = threadIdx.x & 31;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   bool bad = false;
+  uint32_t trip = 0;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < v.n; base += stride * kCountUnroll) {
+    if (++trip % kHotReset == 0) hot.flush(grid);
     typename Rec<FMT>::Raw r[kCountUnroll];
 #pragma unroll
     for (int u = 0; u < kCountUnroll; ++u) {
@@ -184,17 +191,19 @@ __global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
           key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
         v.pkey[i] = key;  // reused by extension counting and the distribute (no re-projection)
       }
-      // warp-uniform cell (coherent scans, dense clusters): one aggregated add;
-      // otherwise one fire-and-forget RED per point (MATCH would saturate the ADU pipe)
+      // warp-uniform cell (coherent scans): one aggregated add; otherwise through the
+      // CTA's hot-counter cache (interleaved dense clusters), else one RED per point
+      // (MATCH would saturate the ADU pipe)
       const uint32_t k0 = __shfl_sync(0xFFFFFFFFu, key, 0);
       const unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
       if (__all_sync(0xFFFFFFFFu, !valid || key == k0)) {
         if (lane == 0 && act) atomicAdd(grid + k0, (uint32_t)__popc(act));
       } else if (valid) {
-        atomicAdd(grid + key, 1u);
+        hot.add(grid, key, 1u);
       }
     }
   }
+  hot.flush(grid);
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) raise_err(v.st, ERR_OUTSIDE);
 }
 
@@ -266,6 +275,7 @@ __global__ void k_ext_create(SplitView v, int round, uint32_t first, uint32_t co
     m.az = (uint16_t)(key & msk);
     m.anchor_slot = level_off(D) + key;
     v.t8[key] = -(int32_t)(e + 2);
+    if (v.abits) atomicOr(v.abits + (key >> 5), 1u << (key & 31));
   } else {  // anchor = finest cell r of parent extension pyramid
     const ExtMeta& p = v.meta[parent_first];
     int pe = p.ext;
@@ -290,71 +300,139 @@ int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_
   return 1;
 }
 
-// Count one point into the extension grids of this round (if it reaches one).
-__device__ __forceinline__ void ext_count_point(const SplitView& v, const Cell16& c, int32_t t, uint32_t round_first,
-                                                bool live) {
-  uint64_t slot = ~0ull;
+// Extension rounds (partition.py:109-151).  The first round scans every point's main
+// finest key (pkey) against the anchor bitmap; an extension point's record is projected once
+// to its depth-16 cell and appended to the extension list {index, round-1 extension id,
+// x | y << 16, z} (one global atomic per CTA trip for the list cursor), so later rounds and
+// the distribute's leaf resolution read only the list.  Counts go through the CTA's
+// hot-counter cache: an anchor cell is by definition dense, and interleaved clusters would
+// otherwise serialise millions of atomics on a few extension-grid cells.
+__device__ __forceinline__ void ext_count_point(const SplitView& v, HotCounts<kHotSlots>& hot, const Cell16& c,
+                                                int32_t t, uint32_t round_first) {
   uint32_t e, rr;
-  if (live && ext_descend(v, c, e, rr, t) && e >= round_first) {
+  if (ext_descend(v, c, e, rr, t) && e >= round_first) {
     const ExtMeta& m = v.meta[e];
-    slot = m.pyr_off + level_off(m.ext) + rr;
-  }
-  // dense clusters put whole warps into one cell: aggregate
-  const unsigned act = __ballot_sync(0xFFFFFFFFu, slot != ~0ull);
-  if (slot != ~0ull) {
-    const unsigned peers = __match_any_sync(act, slot);
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(v.pyr + slot, (uint32_t)__popc(peers));
+    const uint64_t slot = m.pyr_off + level_off(m.ext) + rr;
+    if (slot < 0xFFFFFFFFull) hot.add(v.pyr, (uint32_t)slot, 1u);
+    else atomicAdd(v.pyr + slot, 1u);
   }
 }
 
-// Every extension round scans all points, four per thread per trip so the key -> target
-// loads stay in flight.  Points inside an extension grid (target <= -2) need their depth-16
-// cell: the first round projects the record once and keeps it (pc16) for the later rounds
-// and the distribute.  (Listing those points for the later rounds cost more in the
-// single-counter append than the full scan it saved.)
-template <int FMT, bool FIRST>
-__global__ void __launch_bounds__(kThreads) k_ext_count(SplitView v, uint32_t round_first) {
+__device__ __forceinline__ bool is_anchor(const SplitView& v, uint32_t key) {
+  return v.abits ? (__ldg(v.abits + (key >> 5)) >> (key & 31)) & 1 : v.t8[key] <= -2;
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(kThreads) k_ext_first(SplitView v) {
   pdl_wait();
+  __shared__ HotCounts<kHotSlots> hot;
+  __shared__ uint32_t wsum[kThreads / 32 + 1];
+  __shared__ unsigned long long lbase;
+  hot.clear();
+  __syncthreads();
   const DevState st = *v.st;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  constexpr int U = 4;
+  constexpr int U = 8;
   bool bad = false;
-  const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+  uint32_t trip = 0;
+  const uint64_t stream = policy_evict_first();
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < v.n; i0 += U * stride) {
+    if (++trip % 8 == 0) hot.flush(v.pyr);
     uint32_t key[U];
-    int32_t t[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) key[u] = ld_hint(v.pkey + min(i0 + u * stride, v.n - 1), stream);
+    uint32_t flags = 0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) t[u] = ld_hint(v.t8 + key[u], keep);
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < v.n && is_anchor(v, key[u])) flags |= 1u << u;
+    uint32_t tot;
+    const uint32_t x = block_excl_scan<uint32_t, kThreads>((uint32_t)__popc(flags), &tot, wsum);
+    if (tot == 0) continue;  // uniform: tot is the CTA's total
+    if (threadIdx.x == 0) lbase = atomicAdd(&v.st->ext_n, (unsigned long long)tot);
+    __syncthreads();
+    uint64_t pos = lbase + x;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      if (!((flags >> u) & 1)) continue;
       const uint64_t i = i0 + u * stride;
-      const bool ext = i < v.n && t[u] <= -2;
-      Cell16 c{0, 0, 0};
-      if (ext) {
-        if (FIRST) {
-          c = cell16<FMT>(Rec<FMT>::load(v.pts, i), st, bad);
-          v.pc16[i] = (uint64_t)c.x | ((uint64_t)c.y << 16) | ((uint64_t)c.z << 32);
-        } else {
-          c = unpack_c16(__ldg(v.pc16 + i));
-        }
-      }
-      ext_count_point(v, c, t[u], round_first, ext);
+      const Cell16 c = cell16<FMT>(Rec<FMT>::load(v.pts, i), st, bad);
+      const int32_t t = v.t8[key[u]];
+      if (pos < v.elist_cap) v.elist[pos] = make_uint4((uint32_t)i, (uint32_t)(-(t + 2)), c.x | (c.y << 16), c.z);
+      ++pos;
+      ext_count_point(v, hot, c, t, 0);
     }
   }
+  hot.flush(v.pyr);
+  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) raise_err(v.st, ERR_OUTSIDE);
+}
+
+__global__ void __launch_bounds__(kThreads) k_ext_more(SplitView v, uint32_t round_first) {
+  pdl_wait();
+  __shared__ HotCounts<kHotSlots> hot;
+  hot.clear();
+  __syncthreads();
+  const uint64_t n = min((uint64_t)v.st->ext_n, v.elist_cap);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  uint32_t trip = 0;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < n; i0 += U * stride) {
+    if (++trip % 16 == 0) hot.flush(v.pyr);
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = __ldcs(v.elist + min(i0 + u * stride, n - 1));
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n)
+        ext_count_point(v, hot, Cell16{q[u].z & 0xFFFF, q[u].z >> 16, q[u].w}, -(int32_t)q[u].y - 2, round_first);
+  }
+  hot.flush(v.pyr);
 }
 
 int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStream_t s) {
-  uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
-  const bool first = round_first == 0;
-  if (fmt == LOD_POINTS_F32) {
-    if (first) launch_pdl(k_ext_count<LOD_POINTS_F32, true>, blocks, kThreads, 0, s, v, round_first);
-    else launch_pdl(k_ext_count<LOD_POINTS_F32, false>, blocks, kThreads, 0, s, v, round_first);
+  if (round_first == 0) {
+    uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
+    if (fmt == LOD_POINTS_F32) launch_pdl(k_ext_first<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
+    else launch_pdl(k_ext_first<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
   } else {
-    if (first) launch_pdl(k_ext_count<LOD_POINTS_F64, true>, blocks, kThreads, 0, s, v, round_first);
-    else launch_pdl(k_ext_count<LOD_POINTS_F64, false>, blocks, kThreads, 0, s, v, round_first);
+    launch_pdl(k_ext_more, 148 * 8, kThreads, 0, s, v, round_first);
   }
+  return 1;
+}
+
+__global__ void k_anchor_sum(SplitView v, const uint64_t* list, uint32_t n) {
+  pdl_wait();
+  const uint32_t* grid = v.pyr + level_off(v.D);
+  unsigned long long s = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s += grid[list[i]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(&v.st->ext_n, s);
+}
+
+int launch_anchor_sum(const SplitView& v, const uint64_t* list, uint32_t n, cudaStream_t s) {
+  launch_pdl(k_anchor_sum, std::max<uint32_t>(1, std::min<uint32_t>(ceil_div_u32(n, kThreads), 148)), kThreads, 0,
+             s, v, list, n);
+  return 1;
+}
+
+// leaf of every extension point, descending from its round-1 grid (partition.py:273-287)
+__global__ void __launch_bounds__(kThreads) k_ext_leaf(SplitView v, uint32_t* leaf_out) {
+  pdl_wait();
+  const uint64_t n = min((uint64_t)v.st->ext_n, v.elist_cap);
+  bool unresolved = false;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 q = __ldcs(v.elist + j);
+    int32_t t = -(int32_t)q.y - 2;
+    uint32_t e, rr;
+    if (ext_descend(v, Cell16{q.z & 0xFFFF, q.z >> 16, q.w}, e, rr, t)) t = v.te[v.meta[e].tgt_off + rr];
+    if (t < 0) unresolved = true, t = 0;
+    leaf_out[q.x] = (uint32_t)t;
+  }
+  if (__any_sync(0xFFFFFFFFu, unresolved) && (threadIdx.x & 31) == 0) raise_err(v.st, ERR_UNRESOLVED);
+}
+
+int launch_ext_leaf(const SplitView& v, uint32_t* leaf_out, cudaStream_t s) {
+  launch_pdl(k_ext_leaf, 148 * 8, kThreads, 0, s, v, leaf_out);
   return 1;
 }
 

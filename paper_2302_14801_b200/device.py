@@ -49,6 +49,46 @@ def unpack_records(raw: np.ndarray, fmt: int):
     return pos, col
 
 
+_STAGE = {}          # device -> (pinned staging buffers, events, copy stream)
+_STAGE_BYTES = 32 << 20
+_POOL = None
+
+
+def host_to_device(arr: np.ndarray, device: int):
+    """Contiguous host array -> uint8 device tensor of its bytes.  Large arrays are copied
+    through two pinned 32-MB staging buffers: the host copy into one (split over 8 threads;
+    numpy copies release the GIL) overlaps the DMA of the other."""
+    global _POOL
+    torch = _torch()
+    src = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
+    nb = src.nbytes
+    out = torch.empty(max(nb, 1), dtype=torch.uint8, device=f"cuda:{device}")
+    if nb <= 2 * _STAGE_BYTES:
+        if nb:
+            out.copy_(torch.from_numpy(src))
+        return out[:nb]
+    if device not in _STAGE:
+        bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        _STAGE[device] = (bufs, [torch.cuda.Event(), torch.cuda.Event()], torch.cuda.Stream(device))
+    bufs, evs, cs = _STAGE[device]
+    if _POOL is None:
+        import concurrent.futures as cf
+        _POOL = cf.ThreadPoolExecutor(8)
+    cs.wait_stream(torch.cuda.current_stream(device))
+    for k, off in enumerate(range(0, nb, _STAGE_BYTES)):
+        m = min(_STAGE_BYTES, nb - off)
+        b = k & 1
+        evs[b].synchronize()                      # the DMA that last read this buffer is done
+        dst = bufs[b].numpy()
+        parts = [(a, min(m, a + (m + 7) // 8)) for a in range(0, m, (m + 7) // 8)]
+        list(_POOL.map(lambda ab: np.copyto(dst[ab[0]:ab[1]], src[off + ab[0]:off + ab[1]]), parts))
+        with torch.cuda.stream(cs):
+            out[off:off + m].copy_(bufs[b][:m], non_blocking=True)
+            evs[b].record(cs)
+    torch.cuda.current_stream(device).wait_stream(cs)
+    return out[:nb]
+
+
 def generate_device(kind: str, n: int, seed: int, start: int = 0, out=None):
     """Rows [start, start+n) of a BASELINE synthetic cloud generated in HBM as 16-B F32 records
     (uint8 torch tensor of n*16 bytes; `lod_generate`, bit-identical to generators.py)."""
@@ -107,10 +147,32 @@ class DeviceTree:
 
     # -- uploads -------------------------------------------------------------
     def upload(self, positions, colors, fmt: int | None = None):
+        """Host (n,3) float32/float64 positions + (n,3) uint8 colours -> device records.
+
+        The arrays go to HBM as they are (host_to_device: pinned staging, parallel host copies)
+        and are packed there (`lod_pack_points`): F32 records when the coordinates are float32
+        or float64 values exact in float32, else F64 records.  No per-point host work."""
         torch = _torch()
-        rec, fmt = pack_records(positions, colors, fmt)
-        buf = torch.from_numpy(rec.view(np.uint8).reshape(-1)).to(f"cuda:{self.device}")
-        return buf, fmt, len(rec)
+        pos = np.asarray(positions)
+        if pos.dtype != np.float32 and pos.dtype != np.float64:
+            pos = pos.astype(np.float64)
+        pos = np.ascontiguousarray(pos).reshape(-1, 3)
+        col = np.ascontiguousarray(np.asarray(colors, np.uint8)).reshape(-1, 3)
+        n = len(pos)
+        if len(col) != n:
+            raise ValueError("positions/colors length mismatch")
+        dev = f"cuda:{self.device}"
+        f64 = pos.dtype == np.float64
+        d_xyz = host_to_device(pos, self.device)
+        d_rgb = host_to_device(col, self.device)
+        out = torch.empty(max(n, 1) * (32 if (f64 and fmt != LOD_POINTS_F32) else 16), dtype=torch.uint8, device=dev)
+        chosen = C.c_int(-1)
+        _abi.check(self.lib.lod_pack_points(C.c_void_p(d_xyz.data_ptr()), 1 if f64 else 0,
+                                            C.c_void_p(d_rgb.data_ptr()), n, -1 if fmt is None else int(fmt),
+                                            C.c_void_p(out.data_ptr()), C.byref(chosen),
+                                            current_stream_ptr(self.device)))
+        fmt = chosen.value
+        return out[: n * (16 if fmt == LOD_POINTS_F32 else 32)], fmt, n
 
     # -- C ABI calls -----------------------------------------------------------
     def split(self, d_records, n: int, fmt: int, config: LodConfig, bounds=None, stream=None):

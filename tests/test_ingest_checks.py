@@ -201,3 +201,80 @@ def test_device_checks_match_host_rules(strategy):
     assert not bad[0].passed and bad[0].detail == "leaf points 120000, expected 5"
     tight = run_checks(tree.__class__(tree.device_tree, BuildConfig(T=10)), expected_points=120_000)
     assert not next(r for r in tight if r.name == "capacity").passed
+
+
+# ---------------------------------------------------------------------------
+# pinned to the REAL reference: tests/golden/ingest_checks.json.gz (make_ingest_golden.py ran
+# lodforge.ingest.read_las / read_ply and lodforge.checks.run_checks on these inputs)
+# ---------------------------------------------------------------------------
+
+def _ingest_golden():
+    from conftest import load_golden
+    return load_golden("ingest_checks")
+
+
+def _golden_files(tmp_path):
+    import ingest_cases as IC
+    out = []
+    for name, data in IC.files().items():
+        p = tmp_path / name
+        p.write_bytes(data)
+        out.append((name, p))
+    return out
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha1(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_host_readers_match_reference_goldens(tmp_path):
+    g = _ingest_golden()["files"]
+    for name, p in _golden_files(tmp_path):
+        c = read_cloud(p)
+        assert [len(c), _sha(c.positions), _sha(c.colors)] == g[name][:3], name
+
+
+@pytest.mark.gpu
+def test_device_decode_matches_reference_goldens(tmp_path):
+    """lod_ingest_las / lod_ingest_ply (via load_points, streamed in double-buffered chunks)
+    decode to exactly the reference's read_las / read_ply arrays (sha1 of f64 positions and
+    u8 colours), for every LAS point format, LAS 1.4 64-bit counts, binary PLY property types
+    and ASCII PLY."""
+    from paper_2302_14801_b200.device import unpack_records
+    from paper_2302_14801_b200.ingest import load_points
+    g = _ingest_golden()["files"]
+    for name, p in _golden_files(tmp_path):
+        dp = load_points(p, chunk_bytes=1 << 18)
+        n = g[name][0]
+        rs = 16 if dp.fmt == 0 else 32
+        pos, col = unpack_records(dp.records.cpu().numpy()[: n * rs], dp.fmt)
+        assert [n, _sha(pos), _sha(col)] == g[name][:3], name
+
+
+@pytest.mark.gpu
+def test_device_checks_match_reference_goldens():
+    """Device run_checks (lod_tree_checks) == the reference's run_checks on the same trees:
+    names, pass/fail and detail text (first offending paths in DFS order)."""
+    import ingest_cases as IC
+    from paper_2302_14801_b200 import BuildConfig, build_lod, partition
+    from paper_2302_14801_b200.checks import run_checks
+    from paper_2302_14801_b200.generators import reference_cloud
+    gold = _ingest_golden()["checks"]
+    for kind, n, seed, T in IC.CHECK_CASES:
+        exp = gold[f"{kind}_{n}_{seed}_T{T}"]
+        c = reference_cloud(kind, n, seed)
+        tree = partition(PointCloud(c.positions, c.colors), BuildConfig(T=T))
+
+        def rec(r):
+            return [[x.name, bool(x.passed), x.detail] for x in r]
+
+        assert rec(run_checks(tree, expected_points=n)) == exp["split"]
+        build_lod(tree, "first-come", 0)
+        assert rec(run_checks(tree, expected_points=n)) == exp["first-come"]
+        build_lod(tree, "average", 0)
+        assert rec(run_checks(tree, expected_points=n)) == exp["average"]
+        assert rec(run_checks(tree, expected_points=5)) == exp["expected5"]
+        tight = tree.__class__(tree.device_tree, BuildConfig(T=10))
+        tight._generation = tree._generation
+        assert rec(run_checks(tight, expected_points=n)) == exp["tightT10"]
