@@ -190,6 +190,20 @@ enum lod_check_bit {
 };
 int lod_tree_checks(const lod_tree* tree, uint32_t T, int32_t max_depth, uint8_t* h_flags, void* stream);
 
+/* Device memory.  By default trees allocate with cudaMalloc (grow-only buffers, freed by
+ * lod_tree_destroy).  lod_set_allocator routes every later allocation through the caller's
+ * pool instead (e.g. torch.cuda.caching_allocator_alloc, so the framework's allocator sees the
+ * HBM the trees hold); both functions or neither; buffers are returned to the allocator that
+ * made them, after a device synchronize.  Process-wide; set it before creating trees. */
+typedef void* (*lod_alloc_fn)(uint64_t bytes, int device, void* ctx);
+typedef void (*lod_free_fn)(void* ptr, uint64_t bytes, int device, void* ctx);
+int lod_set_allocator(lod_alloc_fn alloc, lod_free_fn free_fn, void* ctx);
+
+/* Planning estimate of the device bytes one build of n points needs (tree buffers, not the
+ * input): an upper bound for surface-like clouds (voxels <= 1.5 n, <= 10% of the points in
+ * extension grids); denser volumes grow the voxel arena on demand. */
+int lod_workspace_bytes(uint64_t n, int format, const lod_config* config, int mode, uint64_t* bytes);
+
 /* Device memory currently held by the tree, bytes. */
 uint64_t lod_tree_device_bytes(const lod_tree* tree);
 

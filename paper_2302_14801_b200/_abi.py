@@ -77,6 +77,8 @@ SIGNATURES = [
     ("lod_ingest_ply", C.c_int, [_P, C.c_uint64, C.c_uint32, _P, _P, C.c_int, C.c_int, _P, _P]),
     ("lod_tree_checks", C.c_int, [_P, C.c_uint32, C.c_int32, _P, _P]),
     ("lod_tree_device_bytes", C.c_uint64, [_P]),
+    ("lod_set_allocator", C.c_int, [_P, _P, _P]),
+    ("lod_workspace_bytes", C.c_int, [C.c_uint64, C.c_int, C.POINTER(LodConfig), C.c_int, C.POINTER(C.c_uint64)]),
     ("lod_set_timing", C.c_int, [_P, C.c_int]),
     ("lod_tree_stage_ms", C.c_int, [_P, C.POINTER(C.c_float)]),
     ("lod_tree_kernel_ms", C.c_int, [_P, C.POINTER(C.c_float)]),

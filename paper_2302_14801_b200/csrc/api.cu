@@ -32,14 +32,37 @@ int fail_cuda(cudaError_t e, const char* what) {
   return fail(LOD_ECUDA, "CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
 }
 
+// Device memory: cudaMalloc, or the caller's allocator (lod_set_allocator) so that e.g.
+// torch's caching allocator accounts for the trees' buffers.  A buffer remembers which
+// allocator made it.
+static lod_alloc_fn g_alloc = nullptr;
+static lod_free_fn g_free = nullptr;
+static void* g_alloc_ctx = nullptr;
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool ext = false;  // from the caller's allocator
   template <class T>
   T* as() const {
     return reinterpret_cast<T*>(p);
   }
 };
+
+static void release(DevBuf& b) {
+  if (!b.p) return;
+  if (b.ext) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceSynchronize();  // the library's streams may still use it; the caller's pool reuses at once
+    g_free(b.p, b.cap, d, g_alloc_ctx);
+  } else {
+    cudaFree(b.p);
+  }
+  b.p = nullptr;
+  b.cap = 0;
+  b.ext = false;
+}
 
 static size_t round_up(size_t b) { return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1); }
 
@@ -48,18 +71,27 @@ static cudaError_t ensure(DevBuf& b, size_t bytes, size_t keep_bytes = 0, cudaSt
   if (bytes <= b.cap) return cudaSuccess;
   void* np = nullptr;
   size_t cap = round_up(bytes);
-  cudaError_t e = cudaMalloc(&np, cap);
-  if (e != cudaSuccess) return e;
+  const bool ext = g_alloc != nullptr;
+  if (ext) {
+    int d = 0;
+    cudaGetDevice(&d);
+    np = g_alloc(cap, d, g_alloc_ctx);
+    if (!np) return cudaErrorMemoryAllocation;
+  } else {
+    cudaError_t e = cudaMalloc(&np, cap);
+    if (e != cudaSuccess) return e;
+  }
   if (b.p) {
     if (keep_bytes) {
-      e = cudaMemcpyAsync(np, b.p, keep_bytes, cudaMemcpyDeviceToDevice, s);
+      cudaError_t e = cudaMemcpyAsync(np, b.p, keep_bytes, cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return e;
       cudaStreamSynchronize(s);
     }
-    cudaFree(b.p);
+    release(b);
   }
   b.p = np;
   b.cap = cap;
+  b.ext = ext;
   return cudaSuccess;
 }
 
@@ -1044,8 +1076,7 @@ void lod_tree_destroy(lod_tree* t) {
                    &t->stash, &t->vbits, &t->vpre, &t->vinfo, &t->vblk, &t->vcount, &t->vlevel_start,
                    &t->node_slot, &t->vacc, &t->vchunks, &t->vvchunks, &t->local_main, &t->local_ext, &t->plan_lists, &t->seg,
                    &t->vpos, &t->vout, &t->obits, &t->pkey, &t->elist, &t->abits};
-  for (DevBuf* b : all)
-    if (b->p) cudaFree(b->p);
+  for (DevBuf* b : all) release(*b);
   for (auto& e : t->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : t->kev)
@@ -1296,6 +1327,41 @@ int lod_tree_kernel_ms(const lod_tree* tc, float* out) {
 }
 
 uint64_t lod_tree_launches(const lod_tree* t) { return t ? t->launches : 0; }
+
+int lod_set_allocator(lod_alloc_fn alloc, lod_free_fn free_fn, void* ctx) {
+  if ((alloc == nullptr) != (free_fn == nullptr)) return fail(LOD_EVALUE, "allocator needs both functions");
+  g_alloc = alloc;
+  g_free = free_fn;
+  g_alloc_ctx = ctx;
+  return LOD_OK;
+}
+
+int lod_workspace_bytes(uint64_t n, int format, const lod_config* cfg, int mode, uint64_t* bytes) {
+  if (!cfg || !bytes) return fail(LOD_EVALUE, "null argument");
+  if (format != LOD_POINTS_F32 && format != LOD_POINTS_F64) return fail(LOD_EVALUE, "unknown point format %d", format);
+  const uint64_t rec = format == LOD_POINTS_F32 ? 16 : 32;
+  const int D = cfg->initial_depth;
+  const uint64_t fine = 1ull << (3 * D), main_cells = level_off(D + 1);
+  const uint64_t leaves_max = std::max<uint64_t>(1, n / std::max<uint32_t>(cfg->T, 1) * 8 + 1);
+  uint64_t b = 0;
+  b += main_cells * 4 + fine * 4 + fine / 8;            // pyramid, targets t8, anchor bitmap
+  b += main_cells * 8 * 2;                              // node slots, scan scratch
+  b += n * 4;                                           // pkey
+  b += n * rec;                                         // leaf buffer
+  b += leaves_max >= (1u << kRadixMaxBits) ? n * rec : 0;  // 2-pass distribute record copy
+  b += n * 8;                                           // leaf ids (input + sorted order)
+  b += n / 2;                                           // tile digit counts (11-bit digits)
+  b += n / 10 * 16;                                     // extension-point list (10% in extension grids)
+  const uint64_t vox = n + n / 2;                       // voxel arena (V/N <= 1.5 for surfaces)
+  b += vox * 8;                                         // arena
+  b += n * 8;                                           // leaf stash {key, rgb}
+  b += 2 * std::max<uint64_t>(n / 4, 1ull << 21) * (mode == LOD_MODE_WEIGHTED ? 32 : mode == LOD_MODE_AVERAGE ? 16 : 4);
+  if (mode == LOD_MODE_FIRST_COME) b += vox * 12 + (n + vox) / 4;  // vpos, vout, ordinal bitmaps
+  b += leaves_max * 160;                                // node table
+  b += 2ull * std::min<uint64_t>(leaves_max, 4096) * (1u << 19);  // rank structures of the widest level
+  *bytes = b;
+  return LOD_OK;
+}
 
 int lod_pack_points(const void* d_xyz, int xyz_is_f64, const uint8_t* d_rgb, uint64_t n, int out_format,
                     void* d_records, int* chosen_format, void* stream) {

@@ -483,9 +483,15 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   // staged, coalesced stores whenever the digit starts at bit 0 (pass 1: leaf id; pass 2: pad)
   constexpr bool kStaged = FMT == LOD_POINTS_F32 && (FIRST || TAGIN) && OUT != OUT_LEAF;
   if (kStaged && p.seg_tiles == 1 && shift == 0) {
-    auto st6 = k_dist_scatter_staged<TAGIN, OUT == OUT_TAG, 6>;
-    auto st11 = k_dist_scatter_staged<TAGIN, OUT == OUT_TAG, kRadixMaxBits>;
-    launch_pdl(bits <= 6 ? st6 : st11, p.segs, kRadixThreads, staged_smem(B), s, v, in_rec, leaf_in, out_rec, bits,
+    // one ballot per digit bit in the in-warp multi-split: instantiate the exact width
+    using K = void (*)(SplitView, const void*, const uint32_t*, void*, int, int, const uint32_t*);
+    constexpr bool TO = OUT == OUT_TAG;
+    const K by_bits[kRadixMaxBits + 1] = {
+        k_dist_scatter_staged<TAGIN, TO, 1>, k_dist_scatter_staged<TAGIN, TO, 1>, k_dist_scatter_staged<TAGIN, TO, 2>,
+        k_dist_scatter_staged<TAGIN, TO, 3>, k_dist_scatter_staged<TAGIN, TO, 4>, k_dist_scatter_staged<TAGIN, TO, 5>,
+        k_dist_scatter_staged<TAGIN, TO, 6>, k_dist_scatter_staged<TAGIN, TO, 7>, k_dist_scatter_staged<TAGIN, TO, 8>,
+        k_dist_scatter_staged<TAGIN, TO, 9>, k_dist_scatter_staged<TAGIN, TO, 10>, k_dist_scatter_staged<TAGIN, TO, 11>};
+    launch_pdl(by_bits[bits], p.segs, kRadixThreads, staged_smem(B), s, v, in_rec, leaf_in, out_rec, bits,
                tag_shift, p.counts);
   } else {
     launch_pdl(scat, p.segs, kRadixThreads, ssm, s, v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,

@@ -154,7 +154,7 @@ constexpr int kHotSlots = 1024;     // per-CTA hot-counter cache (common.cuh Hot
 constexpr int kHotReset = 64;       // loop trips between flushes (64 x 1024 points per CTA)
 
 template <int FMT>
-__global__ void __launch_bounds__(kThreads) k_count(SplitView v) {
+__global__ void __launch_bounds__(kThreads, 4) k_count(SplitView v) {
   pdl_wait();
   __shared__ HotCounts<kHotSlots> hot;
   hot.clear();
@@ -325,19 +325,20 @@ __device__ __forceinline__ bool is_anchor(const SplitView& v, uint32_t key) {
 template <int FMT>
 __global__ void __launch_bounds__(kThreads) k_ext_first(SplitView v) {
   pdl_wait();
+  constexpr int U = 8;
   __shared__ HotCounts<kHotSlots> hot;
   __shared__ uint32_t wsum[kThreads / 32 + 1];
   __shared__ unsigned long long lbase;
+  __shared__ uint32_t sidx[kThreads * U], skey[kThreads * U];  // this trip's extension points
   hot.clear();
   __syncthreads();
   const DevState st = *v.st;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  constexpr int U = 8;
   bool bad = false;
-  uint32_t trip = 0;
+  uint32_t since_flush = 0;
   const uint64_t stream = policy_evict_first();
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < v.n; i0 += U * stride) {
-    if (++trip % 8 == 0) hot.flush(v.pyr);
+    // 1: which of this trip's points are extension points (anchor bitmap, no record read)
     uint32_t key[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) key[u] = ld_hint(v.pkey + min(i0 + u * stride, v.n - 1), stream);
@@ -346,20 +347,28 @@ __global__ void __launch_bounds__(kThreads) k_ext_first(SplitView v) {
     for (int u = 0; u < U; ++u)
       if (i0 + u * stride < v.n && is_anchor(v, key[u])) flags |= 1u << u;
     uint32_t tot;
-    const uint32_t x = block_excl_scan<uint32_t, kThreads>((uint32_t)__popc(flags), &tot, wsum);
+    uint32_t x = block_excl_scan<uint32_t, kThreads>((uint32_t)__popc(flags), &tot, wsum);
     if (tot == 0) continue;  // uniform: tot is the CTA's total
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if ((flags >> u) & 1) sidx[x] = (uint32_t)(i0 + u * stride), skey[x] = key[u], ++x;
     if (threadIdx.x == 0) lbase = atomicAdd(&v.st->ext_n, (unsigned long long)tot);
     __syncthreads();
-    uint64_t pos = lbase + x;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!((flags >> u) & 1)) continue;
-      const uint64_t i = i0 + u * stride;
+    // 2: the trip's extension points, densely over the CTA: project once, list, count
+    for (uint32_t j = threadIdx.x; j < tot; j += kThreads) {
+      const uint32_t i = sidx[j];
       const Cell16 c = cell16<FMT>(Rec<FMT>::load(v.pts, i), st, bad);
-      const int32_t t = v.t8[key[u]];
-      if (pos < v.elist_cap) v.elist[pos] = make_uint4((uint32_t)i, (uint32_t)(-(t + 2)), c.x | (c.y << 16), c.z);
-      ++pos;
+      const int32_t t = v.t8[skey[j]];
+      const uint64_t pos = lbase + j;
+      if (pos < v.elist_cap) v.elist[pos] = make_uint4(i, (uint32_t)(-(t + 2)), c.x | (c.y << 16), c.z);
       ext_count_point(v, hot, c, t, 0);
+    }
+    since_flush += tot;
+    if (since_flush >= 16384) {  // uniform
+      hot.flush(v.pyr);
+      since_flush = 0;
+    } else {
+      __syncthreads();  // sidx / skey / lbase are rewritten by the next trip
     }
   }
   hot.flush(v.pyr);

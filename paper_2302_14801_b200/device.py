@@ -123,12 +123,54 @@ def current_stream_ptr(device: int | None = None):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_uint64, C.c_int, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p)
+_ALLOCATOR = None
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the library's device allocations through torch's caching allocator
+    (lod_set_allocator), so torch.cuda.memory_allocated() and the framework's OOM handling see
+    the HBM the trees hold.  On by default for trees made through this package; set
+    LODB200_CUDA_MALLOC=1 to keep plain cudaMalloc."""
+    global _ALLOCATOR
+    torch = _torch()
+    lib = _abi.load()
+    if not enable:
+        _abi.check(lib.lod_set_allocator(None, None, None))
+        _ALLOCATOR = None
+        return
+
+    def alloc(nbytes, device, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), int(device))
+        except Exception:   # out of memory: the library reports a CUDA allocation error
+            return None
+
+    def free(ptr, nbytes, device, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    _ALLOCATOR = (_ALLOC_FN(alloc), _FREE_FN(free))   # keep the thunks alive
+    _abi.check(lib.lod_set_allocator(C.cast(_ALLOCATOR[0], C.c_void_p), C.cast(_ALLOCATOR[1], C.c_void_p), None))
+
+
+def workspace_bytes(n: int, fmt: int = LOD_POINTS_F32, config: LodConfig | None = None, mode: int = 1) -> int:
+    """lod_workspace_bytes: planning estimate of one build's device bytes."""
+    out = C.c_uint64()
+    cfg = config or make_config()
+    _abi.check(_abi.load().lod_workspace_bytes(int(n), int(fmt), C.byref(cfg), int(mode), C.byref(out)))
+    return int(out.value)
+
+
 class DeviceTree:
     """One `lod_tree` handle (grow-only device buffers reused across builds)."""
 
     def __init__(self, device: int | None = None):
+        import os
         torch = _torch()
         self.lib = _abi.load()
+        if _ALLOCATOR is None and os.environ.get("LODB200_CUDA_MALLOC", "0") != "1":
+            use_torch_allocator(True)
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.h = self.lib.lod_tree_create(self.device)
         if not self.h:
@@ -136,7 +178,8 @@ class DeviceTree:
         self._input = None
         self.generation = 0   # bumped by every split: trees built earlier on this handle are stale
 
-    def __del__(self):
+    def close(self):
+        """Free the tree's device buffers now (also done when the handle is collected)."""
         h = getattr(self, "h", None)
         if h:
             try:
@@ -144,6 +187,9 @@ class DeviceTree:
             except Exception:
                 pass
             self.h = None
+
+    def __del__(self):
+        self.close()
 
     # -- uploads -------------------------------------------------------------
     def upload(self, positions, colors, fmt: int | None = None):
