@@ -466,8 +466,9 @@ def main():
     stream = torch.cuda.current_stream()
     sptr = C.c_void_p(stream.cuda_stream)
     if world > 1:
-        from paper_2302_14801_b200.dist import RankBuilder, TorchComm, build_distributed
-        comm = TorchComm()
+        from paper_2302_14801_b200.dist import NcclComm, RankBuilder, TorchComm, build_distributed
+        # NCCL: the library's own communicator on the build stream; gloo: host-staged (tests)
+        comm = NcclComm.from_torch_distributed(local) if args.backend == "nccl" else TorchComm()
         rb = RankBuilder(rank, world, dev=dev)
 
     def step(src=None):
@@ -611,7 +612,8 @@ def main():
             "dtype": "f64-geometry/u32-counts", "data": "synthetic",
             "config": {"workload": args.config, "points": n_total, "points_per_gpu": n, "mode": args.mode,
                        "T": 50_000, "grid": 128, "l2": "input 16 B/pt x points > 126 MB L2, no flush",
-                       "parallelism": f"subtree-sharded x{world} ({args.backend} all-reduce + all-to-all + rank-0 merge)"
+                       "parallelism": f"subtree-sharded x{world} ({'library NCCL' if args.backend == 'nccl' else 'gloo'} "
+                                      f"all-reduce + all-to-all + rank-0 gather)"
                        if world > 1 else "single"},
             "e2e": e2e, "e2e_api": api, "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),

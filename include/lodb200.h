@@ -238,8 +238,9 @@ int lod_generate(const char* kind, uint64_t seed, uint64_t start, uint64_t n, vo
                  const double* table_or_null, void* stream);
 
 /* ---------------------------------------------------------------------------------
- * Multi-GPU stages (one process per GPU; the caller runs the collectives, e.g. NCCL via
- * torch.distributed -- see paper_2302_14801_b200/dist.py).  Subtree sharding per
+ * Multi-GPU stages (one process per GPU; the collectives run through lod_comm_* below --
+ * NCCL on the build's stream -- or any equivalent the caller drives; see
+ * paper_2302_14801_b200/dist.py).  Subtree sharding per
  * world bounds and counting grids are all-reduced, every rank derives the
  * identical node table, leaves are assigned to ranks by top-level subtree, points are
  * exchanged all-to-all (source-rank order keeps the global input order), each rank samples
@@ -273,6 +274,32 @@ int lod_dist_adopt(lod_tree* tree, const void* d_records, uint64_t n, const uint
 int lod_dist_voxelize(lod_tree* tree, int mode, uint64_t seed, const uint8_t* h_mask, int append,
                       const int32_t* h_imp_nodes, const uint32_t* h_imp_counts, uint32_t n_imp,
                       uint32_t imp_slot_base, const void* d_imp_vox, void* stream);
+
+/* the voxel runs of n inner nodes h_nodes[i], concatenated into d_out (8-B voxels, stored
+ * order) in ONE launch; h_counts[i] receives each node's voxel count (the subtree roots a
+ * rank sends to rank 0) */
+int lod_dist_export_roots(lod_tree* tree, const int32_t* h_nodes, uint32_t n, void* d_out, uint32_t* h_counts,
+                          void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * NCCL communicator of the multi-GPU build (NVLink / NVSwitch), issued on the build's stream.
+ * NCCL is loaded on first use (libnccl.so.2).  Bootstrap: rank 0 calls lod_comm_unique_id,
+ * the caller broadcasts the 128 bytes (any host channel), every rank calls lod_comm_init.
+ * dtype: 0 u32, 1 u64, 2 f64, 3 i64; op: 0 sum, 1 min, 2 max.
+ * ------------------------------------------------------------------------------- */
+typedef struct lod_comm lod_comm;
+int lod_comm_unique_id(uint8_t* out128);
+int lod_comm_init(const uint8_t* id128, int nranks, int rank, int device, lod_comm** out);
+int lod_comm_destroy(lod_comm* comm);
+int lod_comm_allreduce(lod_comm* comm, void* d_buf, uint64_t count, int dtype, int op, void* stream);
+int lod_comm_allgather(lod_comm* comm, const void* d_send, void* d_recv, uint64_t bytes, void* stream);
+/* grouped ncclSend / ncclRecv: send_bytes[q] consecutive bytes to rank q, recv_bytes[q] from
+ * rank q, received in source-rank order (keeps each leaf's points in global input order) */
+int lod_comm_alltoallv(lod_comm* comm, const void* d_send, const uint64_t* send_bytes, void* d_recv,
+                       const uint64_t* recv_bytes, void* stream);
+/* every rank sends `bytes`; `root` receives recv_bytes[q] from each q, in rank order */
+int lod_comm_gatherv(lod_comm* comm, const void* d_send, uint64_t bytes, void* d_recv, const uint64_t* recv_bytes,
+                     int root, void* stream);
 
 /* Message of the last failure on the calling thread. */
 const char* lod_last_error(void);

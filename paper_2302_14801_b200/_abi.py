@@ -94,6 +94,14 @@ SIGNATURES = [
     ("lod_dist_adopt", C.c_int, [_P, _P, C.c_uint64, _P, _P]),
     ("lod_dist_voxelize", C.c_int, [_P, C.c_int, C.c_uint64, _P, C.c_int, _P, _P, C.c_uint32, C.c_uint32, _P,
                                     _P]),
+    ("lod_dist_export_roots", C.c_int, [_P, _P, C.c_uint32, _P, _P, _P]),
+    ("lod_comm_unique_id", C.c_int, [_P]),
+    ("lod_comm_init", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("lod_comm_destroy", C.c_int, [_P]),
+    ("lod_comm_allreduce", C.c_int, [_P, _P, C.c_uint64, C.c_int, C.c_int, _P]),
+    ("lod_comm_allgather", C.c_int, [_P, _P, _P, C.c_uint64, _P]),
+    ("lod_comm_alltoallv", C.c_int, [_P, _P, _P, _P, _P, _P]),
+    ("lod_comm_gatherv", C.c_int, [_P, _P, C.c_uint64, _P, _P, C.c_int, _P]),
     ("lod_last_error", C.c_char_p, []),
     ("lod_version", C.c_char_p, []),
 ]

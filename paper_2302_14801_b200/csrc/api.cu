@@ -860,6 +860,8 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         L.list_n = lst_n[d];
         L.chunk = voxelize_chunk(L.list_n);
         L.vchunk = voxelize_vchunk(L.list_n);
+        L.local_max = voxelize_local_max(mode, L.list_n);
+        L.leaf_chunk = L.local_max ? 65536u : L.chunk;
         if (has_back[L.parity]) CK(cudaStreamWaitEvent(t->vfront, e_back[L.parity], 0));
         CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
                            (size_t)L.list_n * kWordsPerNode * 4, t->vfront));
@@ -1427,6 +1429,38 @@ int lod_dist_copy_segments(lod_tree* t, const void* d_src, void* d_dst, const ui
 int lod_dist_adopt(lod_tree* t, const void* d_records, uint64_t n, const uint32_t* h_leaf_counts, void* stream) {
   return dist_adopt(t, d_records, n, h_leaf_counts, (cudaStream_t)stream);
 }
+int lod_dist_export_roots(lod_tree* t, const int32_t* h_nodes, uint32_t n, void* d_out, uint32_t* h_counts,
+                          void* stream) {
+  if (!t || t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");
+  if (n && (!h_nodes || !d_out || !h_counts)) return fail(LOD_EVALUE, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
+  if (!n) return LOD_OK;
+  // counts and destination offsets from the node table (one small copy each way)
+  std::vector<uint32_t> cnt(t->n_nodes);
+  CK(cudaMemcpyAsync(cnt.data(), t->n_count.p, 4ull * t->n_nodes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<uint64_t> off(n);
+  uint64_t total = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (h_nodes[i] < 0 || (uint32_t)h_nodes[i] >= t->n_nodes) return fail(LOD_EVALUE, "node %d out of range", h_nodes[i]);
+    h_counts[i] = cnt[h_nodes[i]];
+    off[i] = total;
+    total += cnt[h_nodes[i]];
+  }
+  CK(ensure(t->seg, (size_t)n * 12 + 16));
+  int32_t* d_nodes = t->seg.as<int32_t>();
+  uint64_t* d_off = reinterpret_cast<uint64_t*>(t->seg.as<char>() + (((size_t)n * 4 + 15) & ~(size_t)15));
+  CK(cudaMemcpyAsync(d_nodes, h_nodes, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_off, off.data(), (size_t)n * 8, cudaMemcpyHostToDevice, s));
+  RUN(launch_export_runs(stored_voxels(t), t->n_first.as<uint64_t>(), t->n_count.as<uint32_t>(), d_nodes, d_off, n,
+                         d_out, s));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));  // the host arrays above are locals
+  return LOD_OK;
+}
+
 int lod_dist_voxelize(lod_tree* t, int mode, uint64_t seed, const uint8_t* h_mask, int append,
                       const int32_t* h_imp_nodes, const uint32_t* h_imp_counts, uint32_t n_imp, uint32_t imp_slot_base,
                       const void* d_imp_vox, void* stream) {

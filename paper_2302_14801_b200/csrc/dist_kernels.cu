@@ -1,5 +1,6 @@
-// Multi-GPU helpers: local per-leaf counts and record segment copies (pack / unpack of
-// the subtree exchange).  The collectives themselves run in torch.distributed (NCCL).
+// Multi-GPU helpers: local per-leaf counts, record segment copies (pack / unpack of the
+// subtree exchange) and the export of subtree-root voxel runs.  The collectives themselves
+// are comm.cu (NCCL).
 #include "kernels.h"
 
 namespace lod {
@@ -45,7 +46,27 @@ __global__ void k_copy_segments(const uint4* src, uint4* dst, const uint64_t* se
   }
 }
 
+// voxel runs (8-B units) of the listed nodes, concatenated: one CTA per run
+__global__ void k_export_runs(const uint2* vox, const uint64_t* n_first, const uint32_t* n_count, const int32_t* nodes,
+                              const uint64_t* dst_off, uint32_t n, uint2* out) {
+  pdl_wait();
+  for (uint32_t g = blockIdx.x; g < n; g += gridDim.x) {
+    const int32_t k = nodes[g];
+    const uint64_t a = n_first[k], b = dst_off[g];
+    const uint32_t c = n_count[k];
+    for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) out[b + i] = __ldg(vox + a + i);
+  }
+}
+
 }  // namespace
+
+int launch_export_runs(const void* vox, const uint64_t* n_first, const uint32_t* n_count, const int32_t* d_nodes,
+                       const uint64_t* d_off, uint32_t n, void* out, cudaStream_t s) {
+  if (!n) return 0;
+  launch_pdl(k_export_runs, std::min<uint32_t>(n, 148 * 16), kT, 0, s, reinterpret_cast<const uint2*>(vox), n_first,
+             n_count, d_nodes, d_off, n, reinterpret_cast<uint2*>(out));
+  return 1;
+}
 
 int launch_local_leaf_counts(const SplitView& v, const uint32_t* local_main, const uint32_t* local_ext,
                              const uint32_t* round_first, const uint32_t* round_count, const int* round_ext,

@@ -20,9 +20,10 @@ Every step is the single-GPU algorithm restricted to a subset, so the distribute
 bit-identical to the single-GPU one (tests/test_dist_gpu.py checks node by node).
 
 `RankBuilder` runs the per-rank stages through the C ABI (`lod_dist_*`); the collectives
-go through a `Comm`: `TorchComm` (torch.distributed; NCCL on device tensors, or gloo with
-host staging) for real runs, `LocalGroup` to drive R ranks in one process (tests on one
-GPU).  `plan_subtrees` is pure numpy (CPU-testable).
+go through a `Comm`: `NcclComm` (the library's own NCCL communicator, lod_comm_*, on the
+build's stream) for real multi-GPU runs, `TorchComm` (torch.distributed, e.g. gloo: several
+processes on one GPU in the tests), `LocalComm` to drive R ranks as threads of one process.
+`plan_subtrees` is pure numpy (CPU-testable).
 """
 from __future__ import annotations
 
@@ -249,45 +250,19 @@ class RankBuilder:
                                               self._stream()))
 
     def export_roots(self, roots):
-        """Voxel runs of the given inner nodes, concatenated (device uint32 pairs) + counts."""
+        """Voxel runs of the given inner nodes, concatenated (device uint32 pairs) + counts:
+        one library launch (lod_dist_export_roots)."""
         import torch
+        roots = np.ascontiguousarray(roots, np.int32)
+        counts = np.zeros(len(roots), np.uint32)
         nd = self.dev.nodes()
-        counts = nd["count"][roots].astype(np.uint32)
-        total = int(counts.sum())
+        total = int(nd["count"][roots].astype(np.int64).sum()) if len(roots) else 0
         out = torch.empty(max(total, 1) * 8, dtype=torch.uint8, device="cuda")
-        if total:
-            _, vp = self.dev.device_ptrs()
-            cudart = _cudart()
-            off = 0
-            for r, c in zip(roots, counts):
-                if c:
-                    cudart.cudaMemcpy(C.c_void_p(out.data_ptr() + off * 8), C.c_void_p(vp + int(nd["first"][r]) * 8),
-                                      C.c_size_t(int(c) * 8), 3)
-                    off += int(c)
+        if len(roots):
+            _abi.check(self.lib.lod_dist_export_roots(self.h, roots.ctypes.data_as(C.c_void_p), len(roots),
+                                                      C.c_void_p(out.data_ptr()), counts.ctypes.data_as(C.c_void_p),
+                                                      self._stream()))
         return out, counts
-
-
-_CUDART = None
-
-
-def _cudart():
-    global _CUDART
-    if _CUDART is None:
-        import glob
-        import os
-        import torch
-        cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib", "libcudart.so*"))
-        cands += glob.glob("/usr/local/cuda/lib64/libcudart.so*")
-        for c in cands:
-            try:
-                _CUDART = C.CDLL(c)
-                break
-            except OSError:
-                continue
-        if _CUDART is None:
-            _CUDART = C.CDLL("libcudart.so")
-        _CUDART.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
-    return _CUDART
 
 
 # ---------------------------------------------------------------------------
@@ -369,6 +344,89 @@ class TorchComm:
         self.dist.all_gather(outs, x, group=self.group)
         return [o[:int(s)].to(self.device) for o, s in zip(outs, sizes)] if self.rank == 0 else None
 
+
+class NcclComm:
+    """Collectives through the library's own NCCL communicator (lod_comm_*, include/lodb200.h),
+    enqueued on the build's stream -- NVLink / NVSwitch, no torch.distributed on the data
+    path.  torch.distributed (any backend) only broadcasts the 128-byte NCCL id at setup."""
+
+    _DT = {"torch.int32": 0, "torch.uint32": 0, "torch.int64": 3, "torch.float64": 2}
+    _OP = {"sum": 0, "min": 1, "max": 2}
+
+    def __init__(self, rank, world, device, uid: bytes):
+        self.lib = _abi.load()
+        self.rank, self.world, self.nccl, self.device = rank, world, True, f"cuda:{device}"
+        self.h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _abi.check(self.lib.lod_comm_init(buf, world, rank, int(device), C.byref(self.h)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _abi.check(_abi.load().lod_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_torch_distributed(cls, device, group=None):
+        import torch.distributed as dist
+        obj = [cls.unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(dist.get_rank(group), dist.get_world_size(group), device, obj[0])
+
+    def close(self):
+        if self.h:
+            self.lib.lod_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stream():
+        return current_stream_ptr()
+
+    def allreduce(self, t, op):
+        _abi.check(self.lib.lod_comm_allreduce(self.h, C.c_void_p(t.data_ptr()), t.numel(), self._DT[str(t.dtype)],
+                                               self._OP[op], self._stream()))
+        return t
+
+    def all_gather_np(self, arr):
+        import torch
+        a = np.ascontiguousarray(arr)
+        x = torch.from_numpy(a.view(np.uint8).reshape(-1).copy()).to(self.device)
+        out = torch.empty(x.numel() * self.world, dtype=torch.uint8, device=self.device)
+        _abi.check(self.lib.lod_comm_allgather(self.h, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()),
+                                               x.numel(), self._stream()))
+        return out.cpu().numpy().view(a.dtype).reshape((self.world,) + a.shape)
+
+    def all_to_all_bytes(self, send, send_splits, recv_splits):
+        import torch
+        sb = np.ascontiguousarray(send_splits, np.uint64)
+        rb = np.ascontiguousarray(recv_splits, np.uint64)
+        recv = torch.empty(max(int(rb.sum()), 1), dtype=torch.uint8, device=self.device)
+        _abi.check(self.lib.lod_comm_alltoallv(self.h, C.c_void_p(send.data_ptr()), sb.ctypes.data_as(C.c_void_p),
+                                               C.c_void_p(recv.data_ptr()), rb.ctypes.data_as(C.c_void_p),
+                                               self._stream()))
+        return recv
+
+    def gather_bytes(self, t, nbytes):
+        """Variable-size gather of device byte tensors to rank 0 (grouped send / recv to the
+        root only; list of per-rank views on rank 0)."""
+        import torch
+        sizes = self.all_gather_np(np.array([nbytes], np.int64))[:, 0].astype(np.uint64)
+        recv = None
+        if self.rank == 0:
+            recv = torch.empty(max(int(sizes.sum()), 1), dtype=torch.uint8, device=self.device)
+        _abi.check(self.lib.lod_comm_gatherv(self.h, C.c_void_p(t.data_ptr()), int(nbytes),
+                                             C.c_void_p(recv.data_ptr() if recv is not None else 0),
+                                             sizes.ctypes.data_as(C.c_void_p), 0, self._stream()))
+        if self.rank != 0:
+            return None
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        return [recv[off[q]:off[q + 1]] for q in range(self.world)]
 
 class LocalComm:
     """R ranks as threads of one process (tests on a single GPU): same interface as
