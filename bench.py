@@ -499,12 +499,12 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             step()
-            stage_sum = [a + b for a, b in zip(stage_sum, dev.stage_ms())]
+            stage_sum = [None if a is None or b is None else a + b for a, b in zip(stage_sum, dev.stage_ms())]
             kernel_sum += dev.kernel_ms()
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    stages = [x / args.steps for x in stage_sum]
+    stages = [None if x is None else x / args.steps for x in stage_sum]
     scatter_ms = kernel_sum / args.steps
     dev.set_timing(False)
     if world > 1:
@@ -586,8 +586,8 @@ def main():
                           f"timed together against one read + one write per record",
                 "algorithmic_bytes": kern_bytes, "ms_per_build": scatter_ms, "peak_source": peak_kind,
                 "stages": {nm: {"ms": st, "algorithmic_bytes": b,
-                                "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st > 0 else None,
-                                "frac": (b / (st / 1000.0) / 1e9 / peak) if b and st > 0 else None,
+                                "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st else None,
+                                "frac": (b / (st / 1000.0) / 1e9 / peak) if b and st else None,
                                 "traffic": measured_traffic(args.config, mode_key, n, nm) if world == 1 else None}
                            for nm, st, b in zip(stage_names, stages, stage_bytes)},
                 "whole_build": {"algorithmic_bytes": whole_bytes, "E": E, "V": V,

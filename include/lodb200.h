@@ -208,7 +208,8 @@ int lod_workspace_bytes(uint64_t n, int format, const lod_config* config, int mo
 uint64_t lod_tree_device_bytes(const lod_tree* tree);
 
 /* Per-stage device times of the last build in milliseconds (CUDA events), for profiling:
- * out[0] bounds+count, [1] extension, [2] merge+nodes+targets, [3] distribute, [4] voxelize.
+ * out[0] bounds+count, [1] extension, [2] merge+nodes+targets, [3] distribute, [4] voxelize;
+ * NaN for a stage the last build did not bracket (the multi-GPU stage calls).
  * Timing is recorded only when enabled (small overhead from event records). */
 int lod_set_timing(lod_tree* tree, int enabled);
 int lod_tree_stage_ms(const lod_tree* tree, float* out5);

@@ -7,6 +7,7 @@
 //   3. after leaf numbering                      -> leaf count, per-depth inner lists
 //   4. end of distribute / end of voxelize       -> error flags
 #include <cstdarg>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -860,8 +861,6 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         L.list_n = lst_n[d];
         L.chunk = voxelize_chunk(L.list_n);
         L.vchunk = voxelize_vchunk(L.list_n);
-        L.local_max = voxelize_local_max(mode, L.list_n);
-        L.leaf_chunk = L.local_max ? 65536u : L.chunk;
         if (has_back[L.parity]) CK(cudaStreamWaitEvent(t->vfront, e_back[L.parity], 0));
         CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
                            (size_t)L.list_n * kWordsPerNode * 4, t->vfront));
@@ -1308,9 +1307,9 @@ int lod_set_timing(lod_tree* t, int enabled) {
 int lod_tree_stage_ms(const lod_tree* tc, float* out) {
   lod_tree* t = const_cast<lod_tree*>(tc);
   if (!t || !t->timing) return fail(LOD_EVALUE, "timing not enabled");
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i < 5; ++i) {  // a stage the last build did not bracket (multi-GPU calls) -> NaN
     out[i] = 0;
-    if (cudaEventElapsedTime(&out[i], t->ev[i], t->ev[i + 1]) != cudaSuccess) out[i] = -1;
+    if (cudaEventElapsedTime(&out[i], t->ev[i], t->ev[i + 1]) != cudaSuccess || out[i] < 0) out[i] = NAN;
   }
   cudaGetLastError();
   return LOD_OK;

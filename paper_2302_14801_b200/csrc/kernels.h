@@ -155,9 +155,6 @@ struct VoxNode {           // per inner node of the level being sampled (by list
   uint32_t ccount[8];
   int32_t cslot[8];        // -2 absent, -1 leaf child, >= 0 slot of an inner child
   uint64_t obase;          // first-come: first word of the node's ordinal bitmap
-  uint32_t lm[8];          // leaf child sampled whole by one K1 chunk: its region's occupied cells
-  uint32_t spill_in;       // octant regions that received boundary spills from other children
-  uint32_t pad_;
 };
 
 struct VoxLevel {
@@ -197,9 +194,6 @@ struct VoxLevel {
                            // with their exclusive popcount prefix: [2 w] bits, [2 w + 1] prefix
   uint64_t ocap;           // bitmap words of obits
   uint32_t chunk;          // samples per K1/K3 chunk
-  uint32_t leaf_chunk;     // samples per K1/K3 chunk of a leaf child (>= chunk)
-  uint32_t local_max;      // regions of <= local_max voxels fed by one leaf child are sampled
-                           // in shared memory by K3L (0: off)
   uint32_t vchunk;         // voxels per K4 chunk
   int mode;
   int exact_sums;          // average: u64 sums (fallback) instead of f32 vector reductions
@@ -207,7 +201,6 @@ struct VoxLevel {
 };
 int launch_voxelize_front(const VoxLevel& L, int sms, cudaStream_t s);
 int launch_voxelize_accumulate(const VoxLevel& L, int sms, cudaStream_t s);
-uint32_t voxelize_local_max(int mode, uint32_t nodes);
 int launch_voxelize_back(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s);
 uint32_t voxelize_acc_bytes(int mode, bool exact_sums);
 int launch_voxelize_import(const VoxLevel& L, uint32_t slot_base, cudaStream_t s);

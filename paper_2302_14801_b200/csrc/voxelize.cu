@@ -86,19 +86,6 @@ __device__ __forceinline__ uint32_t* pre_of(const VoxLevel& L, int parity, uint3
   return L.pre + ((uint64_t)parity * L.slots + slot) * kWords;
 }
 
-// A region (child octant o of a node) fed by ONE leaf child that K1 sampled whole, with no
-// boundary spills from other children and at most local_max occupied cells, is sampled by
-// K3L alone: accumulation in shared memory and the final records written straight away.
-// K3 skips its samples and K4 its voxels.
-__device__ __forceinline__ bool local_region(const VoxLevel& L, const VoxNode& nd, int o) {
-  return L.local_max && !nd.skip && nd.cslot[o] == -1 && nd.lm[o] != 0 && nd.lm[o] <= L.local_max &&
-         !((nd.spill_in >> o) & 1u) && nd.ccount[o] <= L.leaf_chunk;
-}
-
-__device__ __forceinline__ int key_octant(uint32_t key) {
-  return (int)((key >> 20) | (((key >> 13) & 1) << 1) | (((key >> 6) & 1) << 2));
-}
-
 // ---------------------------------------------------------------------------
 // K0: per-node setup; eight lanes per node, one per child octant
 // ---------------------------------------------------------------------------
@@ -137,7 +124,6 @@ __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
   info.ccount[o] = cnt;
   info.cfirst[o] = first;
   info.cslot[o] = cslot;
-  info.lm[o] = 0;
   bool skip = false;
   if (empty) skip = true;
   else if (L.mode == LOD_MODE_RANDOM && S >= (uint32_t)kRandomLimit) skip = true;
@@ -159,13 +145,12 @@ __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
     info.vbase = 0;
     info.m = 0;
     info.skip = skip;
-    info.spill_in = 0;
     L.node_slot[node] = s;
     if (empty) raise_err(L.st, ERR_EMPTY_CHILD, (uint32_t)empty_child);
     else if (skip) raise_err(L.st, ERR_RANDOM_LIMIT, node, S);
   }
   if (skip || cnt == 0) return;
-  const uint32_t chunk = cslot == -1 ? L.leaf_chunk : L.chunk;
+  const uint32_t chunk = L.chunk;
   const uint32_t nch = (cnt + chunk - 1) / chunk;
   uint32_t at = atomicAdd(L.counters + 0, nch);
   for (uint32_t j = 0; j < cnt; j += chunk) {
@@ -220,8 +205,6 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
         if (!(rb[lw] & bit)) atomicOr(rb + lw, bit);
       } else {  // boundary spill of a leaf point into a neighbouring octant
         atomicOr(bits + (key >> 5), bit);
-        const uint32_t to = (key >> 20) | (((key >> 13) & 1) << 1) | (((key >> 6) & 1) << 2);
-        atomicOr(&L.info[ch.x].spill_in, 1u << to);   // that region is no longer one child's alone
       }
     };
     if (nd.cslot[o] == -1) {
@@ -260,17 +243,9 @@ __global__ void __launch_bounds__(kRT, 2) k_occupy(VoxLevel L) {
       }
     }
     __syncthreads();
-    uint32_t occ = 0;
     for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) {
       const uint32_t v = rb[i];
       if (v) atomicOr(bits + region_to_global(i, o), v);
-      occ += __popc(v);
-    }
-    // a leaf child sampled whole by this chunk: its region's own occupancy (K3L eligibility)
-    if (L.local_max && nd.cslot[o] == -1 && ch.z == 0 && ch.w == nd.ccount[o]) {
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) occ += __shfl_xor_sync(0xFFFFFFFFu, occ, d);
-      if ((threadIdx.x & 31) == 0 && occ) atomicAdd(&L.info[ch.x].lm[o], occ);
     }
     __syncthreads();
   }
@@ -471,7 +446,6 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
     const uint32_t* pre = pre_of(L, L.parity, ch.x);
     const uint64_t acc0 = nd.vbase - L.level_start[0];
     const int o = (int)ch.y;
-    if (local_region(L, nd, o)) continue;  // K3L samples this region (uniform per chunk)
     for (uint32_t i = threadIdx.x; i < kRegionWords; i += kRT) {
       const uint32_t gw = region_to_global(i, o);
       const uint32_t w = __ldcg(bits + gw);
@@ -522,125 +496,6 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
           const uint32_t ord = ob + (leafc ? j : __ldg(L.vpos + nd.cfirst[o] + j));
           atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, ~ord);
         }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K3L: a local region (see local_region) in one CTA.  The region's bitmap (32 KB) and its
-// region-local exclusive popcount prefix (u16, 16 KB) sit in shared memory, the voxels'
-// accumulators too (average: u64 {r | g << 32}, {b | n << 32}, exact integer sums since the
-// child has <= 65536 samples; random: max (rand12 | ordinal20); first-come: max ~ordinal).
-// The child's samples (the K1 stash) are read once; a sample spilling out of the region takes
-// K3's global path.  Then one thread per region word writes its voxels' final records at their
-// node-wide ranks (word prefix from K2b): no accumulator round trip through HBM, no K4 pass.
-// ---------------------------------------------------------------------------
-constexpr int kLT = 1024;
-
-__host__ __device__ constexpr size_t local_smem(uint32_t local_max, bool average) {
-  return (size_t)kRegionWords * 6 + (size_t)local_max * (average ? 16 : 4);
-}
-
-__global__ void __launch_bounds__(kLT) k_local(VoxLevel L) {
-  pdl_wait();
-  if (L.st->err & ERR_ARENA) return;
-  extern __shared__ __align__(16) uint32_t lsm[];
-  uint32_t* rbits = lsm;                                                  // [8192]
-  uint16_t* lpre = reinterpret_cast<uint16_t*>(lsm + kRegionWords);      // [8192]
-  uint32_t* acc = lsm + kRegionWords + kRegionWords / 2;                 // accumulators
-  unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(acc);
-  __shared__ uint32_t wsum[kLT / 32 + 1];
-  const bool avg = L.mode == LOD_MODE_AVERAGE;
-  for (uint32_t u = blockIdx.x; u < L.list_n * 8; u += gridDim.x) {
-    const uint32_t s = u >> 3;
-    const int o = (int)(u & 7);
-    const VoxNode& nd = L.info[s];
-    if (!local_region(L, nd, o)) continue;  // uniform
-    const uint32_t* bits = bits_of(L, L.parity, s);
-    const uint32_t* pre = pre_of(L, L.parity, s);
-    constexpr int per = kRegionWords / kLT;
-    uint32_t w[per], c = 0;
-#pragma unroll
-    for (int q = 0; q < per; ++q) c += __popc(w[q] = __ldcg(bits + region_to_global(threadIdx.x * per + q, o)));
-    uint32_t tot;
-    uint32_t x = block_excl_scan<uint32_t, kLT>(c, &tot, wsum);
-#pragma unroll
-    for (int q = 0; q < per; ++q) {
-      rbits[threadIdx.x * per + q] = w[q];
-      lpre[threadIdx.x * per + q] = (uint16_t)x;
-      x += __popc(w[q]);
-    }
-    const uint32_t words = (avg ? 4 : 1) * tot;
-    for (uint32_t i = threadIdx.x; i < words; i += kLT) acc[i] = 0;
-    __syncthreads();
-    const uint2* src = L.stash + nd.cfirst[o];
-    const uint32_t cnt = nd.ccount[o], ob = nd.cbase[o];
-    const uint64_t acc0 = nd.vbase - L.level_start[0];
-    for (uint32_t j = threadIdx.x; j < cnt; j += kLT) {
-      const uint2 r = __ldcs(src + j);
-      const uint32_t key = r.x, rgb = r.y;
-      const uint32_t mask = (1u << (key & 31)) - 1;
-      uint32_t lw;
-      if (region_word(key, o, lw)) {
-        const uint32_t lr = lpre[lw] + __popc(rbits[lw] & mask);
-        if (avg) {
-          atomicAdd(acc64 + 2 * lr, (unsigned long long)(rgb & 0xFF) | ((unsigned long long)((rgb >> 8) & 0xFF) << 32));
-          atomicAdd(acc64 + 2 * lr + 1, (unsigned long long)((rgb >> 16) & 0xFF) | (1ull << 32));
-        } else if (L.mode == LOD_MODE_RANDOM) {
-          atomicMax(acc + lr, rand_enc(nd.hash, ob + j));
-        } else {
-          atomicMax(acc + lr, ~(ob + j));
-        }
-      } else {  // spill into a neighbouring region (never local): K3's global path
-        const uint64_t a = acc0 + __ldcg(pre + (key >> 5)) + __popc(__ldcg(bits + (key >> 5)) & mask);
-        if (avg && !L.exact_sums) {
-          float* p = reinterpret_cast<float*>(L.acc) + 4 * a;
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"((float)(rgb & 0xFF)),
-                       "f"((float)((rgb >> 8) & 0xFF)), "f"((float)((rgb >> 16) & 0xFF)), "f"(1.0f)
-                       : "memory");
-        } else if (avg) {
-          unsigned long long* p = reinterpret_cast<unsigned long long*>(L.acc) + 4 * a;
-          atomicAdd(p, (unsigned long long)(rgb & 0xFF));
-          atomicAdd(p + 1, (unsigned long long)((rgb >> 8) & 0xFF));
-          atomicAdd(p + 2, (unsigned long long)((rgb >> 16) & 0xFF));
-          atomicAdd(p + 3, 1ull);
-        } else if (L.mode == LOD_MODE_RANDOM) {
-          atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, rand_enc(nd.hash, ob + j));
-        } else {
-          atomicMax(reinterpret_cast<uint32_t*>(L.acc) + a, ~(ob + j));
-        }
-      }
-    }
-    __syncthreads();
-    // final records at node-wide ranks: rank = K2b's word prefix + rank inside the word
-    for (uint32_t wi = threadIdx.x; wi < kRegionWords; wi += kLT) {
-      uint32_t b = rbits[wi];
-      if (!b) continue;
-      const uint32_t gw = region_to_global(wi, o);
-      uint32_t r = __ldcg(pre + gw), lr = lpre[wi];
-      while (b) {
-        const uint32_t bit = __ffs(b) - 1;
-        b &= b - 1;
-        const uint32_t key = (gw << 5) | bit;
-        uint32_t rgb;
-        if (avg) {
-          const unsigned long long a0 = acc64[2 * lr], a1 = acc64[2 * lr + 1];
-          const uint64_t n = a1 >> 32;
-          rgb = mean_round(a0 & 0xFFFFFFFFull, n) | (mean_round(a0 >> 32, n) << 8) |
-                (mean_round(a1 & 0xFFFFFFFFull, n) << 16);
-        } else {
-          const uint32_t ord = L.mode == LOD_MODE_RANDOM ? (acc[lr] & 0xFFFFFu) : ~acc[lr];
-          rgb = __ldg(&src[ord - ob].y);  // the winning sample names the colour
-          if (L.mode == LOD_MODE_FIRST_COME) {
-            reinterpret_cast<uint32_t*>(L.acc)[acc0 + r] = ord;  // ranked by K5 like K4's
-            atomicOr(L.obits + 2 * (nd.obase + (ord >> 5)), 1u << (ord & 31));
-          }
-        }
-        L.vox[nd.vbase + r] = make_uint2(key, rgb);
-        ++r;
-        ++lr;
       }
     }
     __syncthreads();
@@ -811,10 +666,7 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
     const VoxNode& nd = L.info[ch.x];
     const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
     const uint64_t acc0 = nd.vbase - L.level_start[0];
-    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) {
-      const uint32_t key = __ldcg(&L.vox[nd.vbase + r].x);
-      if (!local_region(L, nd, key_octant(key))) finalize_voxel(L, nd, acc0, key, r);
-    }
+    for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) finalize_voxel(L, nd, acc0, __ldcg(&L.vox[nd.vbase + r].x), r);
   }
 }
 
@@ -983,22 +835,11 @@ int launch_voxelize_front(const VoxLevel& L, int sms, cudaStream_t s) {
 }
 
 int launch_voxelize_accumulate(const VoxLevel& L, int sms, cudaStream_t s) {
-  if (L.mode == LOD_MODE_WEIGHTED) {
+  if (L.mode == LOD_MODE_WEIGHTED)
     launch_pdl(k_scatter_w, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
-    return 1;
-  }
-  launch_pdl(k_scatter, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
-  if (!L.local_max) return 1;
-  const size_t sm = local_smem(L.local_max, L.mode == LOD_MODE_AVERAGE);
-  launch_pdl(k_local, (uint32_t)std::min<uint64_t>(8ull * L.list_n, (uint64_t)sms), kLT, sm, s, L);  // 1 CTA/SM
-  return 2;
-}
-
-// K3L regions (one 1024-thread CTA per SM): average keeps 16 B per voxel, random and
-// first-come 4 B; levels of few nodes keep the all-SM K3 path
-uint32_t voxelize_local_max(int mode, uint32_t nodes) {
-  if (mode == LOD_MODE_WEIGHTED || nodes < 16) return 0;
-  return mode == LOD_MODE_AVERAGE ? 10240 : 12288;
+  else
+    launch_pdl(k_scatter, sms * 2, kRT, 2 * kRegionWords * 4, s, L);
+  return 1;
 }
 
 int launch_voxelize_back(const VoxLevel& L, int sms, ScanScratch& scr, cudaStream_t s) {

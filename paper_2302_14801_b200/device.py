@@ -294,7 +294,7 @@ class DeviceTree:
     def stage_ms(self):
         out = (C.c_float * 5)()
         _abi.check(self.lib.lod_tree_stage_ms(self.h, out))
-        return list(out)
+        return [None if x != x else float(x) for x in out]   # NaN: stage not bracketed
 
     def kernel_ms(self) -> float:
         """Device ms of the distribute's K_scatter (all passes) in the last timed build."""

@@ -73,3 +73,81 @@ def test_distributed_matches_reference(name, world):
             assert {k: [len(c), sha(c, k2)] for k, (c, k2) in vox.items()} == exp, (name, mode)
         if world > 1 and len(plan.roots) >= world:
             assert len(set(plan.root_owner.tolist())) > 1  # the work really was spread
+
+
+class _Dumped:
+    """A rank's dumped part of the tree (scripts/dist_rank.py) with the RankBuilder surface
+    combined_digests reads."""
+
+    class _Dev:
+        def __init__(self, z):
+            self.z = z
+
+        def nodes(self):
+            return self.z["nodes"]
+
+        def leaf_records(self):
+            return self.z["leaf"]
+
+        def voxels(self):
+            return self.z["vox"]
+
+    def __init__(self, z):
+        self.dev = self._Dev(z)
+
+
+@pytest.mark.parametrize("name,mode,world", [("part_stadium_30000_3_T1500", "average", 2),
+                                             ("cluster1500k_T2000", "random:0", 2),
+                                             ("small_tree_30k", "first-come", 3)])
+def test_multiprocess_gloo_matches_reference(tmp_path, name, mode, world):
+    """`world` PROCESSES on one GPU (torch.distributed.run, gloo collectives through
+    TorchComm), each a RankBuilder with its own lod_tree: the union of their outputs equals
+    the reference's golden digests."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    from types import SimpleNamespace
+    g = load_golden(name)
+    exp = g["modes"][mode]
+    if "error" in exp:
+        pytest.skip("the reference raises for this mode")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    strat, _, seed = mode.partition(":")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "scripts", "dist_rank.py"),
+           "--case", name, "--mode", strat, "--seed", seed or "0", "--out", str(tmp_path)]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    parts = [np.load(os.path.join(tmp_path, f"rank{q}.npz")) for q in range(world)]
+    plan = SimpleNamespace(cut=int(parts[0]["cut"]), node_owner=parts[0]["node_owner"])
+    split, vox = combined_digests([_Dumped(z) for z in parts], plan, int(parts[0]["fmt"]))
+    assert split == g["split"]
+    assert {k: [len(c), sha(c, k2)] for k, (c, k2) in vox.items()} == exp
+
+
+def test_nccl_communicator_single_rank_matches_reference():
+    """The library's own NCCL communicator (lod_comm_*: all-reduce, all-gather, grouped
+    send/recv all-to-all, gather to rank 0) driving build_distributed on one rank -- the code
+    path bench.py --gpus N takes on an NVLink box -- reproduces the golden tree."""
+    import torch
+    from paper_2302_14801_b200.device import pack_records
+    from paper_2302_14801_b200.dist import NcclComm, build_distributed
+    name = "part_uniform-cube_20000_1_T1000"
+    g = load_golden(name)
+    case = by_name(name)
+    pos, col = make_input(case)
+    rec, fmt = pack_records(pos, col)
+    comm = NcclComm(0, 1, torch.cuda.current_device(), NcclComm.unique_id())
+    d = torch.from_numpy(rec.view(np.uint8).reshape(-1).copy()).cuda()
+    for mode in ("average", "random:11", "first-come"):
+        strat, _, seed = mode.partition(":")
+        rb, plan = build_distributed(comm, d, len(rec), fmt, strat, int(seed or 0), T=case["cfg"]["T"])
+        torch.cuda.synchronize()
+        split, vox = combined_digests([rb], plan, fmt)
+        assert split == g["split"], mode
+        assert {k: [len(c), sha(c, k2)] for k, (c, k2) in vox.items()} == g["modes"][mode], mode
+    comm.close()
