@@ -67,11 +67,12 @@ __device__ __forceinline__ void load_items(const SplitView& v, const void* in_re
       }
       leaf[k] = (uint32_t)t;
     }
-  } else if (TAGIN) {  // 2nd pass: the digit rides in the record's pad
+  } else if (TAGIN) {  // 2nd pass: the digit from the byte stream pass 1 wrote (f32), else the record's pad
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const uint64_t i = base + (uint64_t)k * 32 + lane;
-      leaf[k] = Rec<FMT>::tag(Rec<FMT>::load(in_rec, i < last ? i : last));  // re-read at the store
+      leaf[k] = in_leaf ? (uint32_t)__ldcs(reinterpret_cast<const uint8_t*>(in_leaf) + (i < last ? i : last))
+                        : Rec<FMT>::tag(Rec<FMT>::load(in_rec, i < last ? i : last));  // re-read at the store
     }
   } else {
 #pragma unroll
@@ -327,12 +328,14 @@ __host__ __device__ constexpr size_t staged_region(int B) {  // count rows / rec
 }
 __host__ __device__ constexpr size_t staged_smem(int B) { return staged_region(B) + (size_t)kRadixTile * 4 + (size_t)B * 8; }
 
-// TAGIN (2nd pass): the digit is the record's pad byte, read as the record's last word (the
-// sectors stay in L2 for the record loads after the ranking); the pad is cleared on output.
+// TAGOUT (1st of 2 passes): the 2nd digit travels in the record's pad AND in a byte stream in
+// destination order (out_tag, 1 B/pt), so the 2nd pass reads its digits -- histogram and
+// ranks -- from 1 B/pt instead of re-reading the 16-B records.  TAGIN: digits from that
+// stream (in_leaf, as bytes); the pad is cleared on output.
 template <bool TAGIN, bool TAGOUT, int NB>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_dist_scatter_staged(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, int bits,
-                          int tag_shift, const uint32_t* firsts) {
+                          int tag_shift, const uint32_t* firsts, uint8_t* out_tag) {
   pdl_wait();
   extern __shared__ __align__(16) uint32_t sm[];
   const int B = 1 << bits;
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const uint64_t i = min(base + (uint64_t)k * 32 + lane, last);
-    leaf[k] = TAGIN ? __ldg(reinterpret_cast<const uint32_t*>(in_rec) + 4 * i + 3) >> 24 : __ldcs(in_leaf + i);
+    leaf[k] = TAGIN ? (uint32_t)__ldcs(reinterpret_cast<const uint8_t*>(in_leaf) + i) : __ldcs(in_leaf + i);
   }
   __syncthreads();
   // stable in-warp ranks (item-major, lane order)
@@ -439,8 +442,11 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   }
   __syncthreads();
   const uint32_t tile_n = (uint32_t)min((uint64_t)kRadixTile, v.n - (uint64_t)tile * kRadixTile);
-  for (uint32_t j = threadIdx.x; j < tile_n; j += kRadixThreads)
-    reinterpret_cast<uint4*>(out_rec)[sdst[j]] = srec[j];
+  for (uint32_t j = threadIdx.x; j < tile_n; j += kRadixThreads) {
+    const uint4 r = srec[j];
+    reinterpret_cast<uint4*>(out_rec)[sdst[j]] = r;
+    if (TAGOUT) out_tag[sdst[j]] = (uint8_t)(r.w >> 24);
+  }
 }
 
 // Global exclusive prefix per digit, from the leaf counts (leaf ids are the sort keys).
@@ -469,7 +475,7 @@ __global__ void __launch_bounds__(1024) k_digit_scan(uint64_t* hist, int B) {
 template <int FMT, bool FIRST, bool TAGIN, int OUT>
 int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, uint32_t* leaf_tmp, void* out_rec,
              uint32_t* out_leaf, int shift, int bits, int tag_shift, const uint64_t* digit_base, const RadixPlan& p,
-             cudaStream_t s) {
+             cudaStream_t s, uint8_t* out_tag = nullptr) {
   const int B = 1 << bits;
   auto hist = k_dist_hist<FMT, FIRST, TAGIN>;
   auto scat = k_dist_scatter<FMT, TAGIN, OUT>;
@@ -484,7 +490,7 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   constexpr bool kStaged = FMT == LOD_POINTS_F32 && (FIRST || TAGIN) && OUT != OUT_LEAF;
   if (kStaged && p.seg_tiles == 1 && shift == 0) {
     // one ballot per digit bit in the in-warp multi-split: instantiate the exact width
-    using K = void (*)(SplitView, const void*, const uint32_t*, void*, int, int, const uint32_t*);
+    using K = void (*)(SplitView, const void*, const uint32_t*, void*, int, int, const uint32_t*, uint8_t*);
     constexpr bool TO = OUT == OUT_TAG;
     const K by_bits[kRadixMaxBits + 1] = {
         k_dist_scatter_staged<TAGIN, TO, 1>, k_dist_scatter_staged<TAGIN, TO, 1>, k_dist_scatter_staged<TAGIN, TO, 2>,
@@ -492,7 +498,7 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
         k_dist_scatter_staged<TAGIN, TO, 6>, k_dist_scatter_staged<TAGIN, TO, 7>, k_dist_scatter_staged<TAGIN, TO, 8>,
         k_dist_scatter_staged<TAGIN, TO, 9>, k_dist_scatter_staged<TAGIN, TO, 10>, k_dist_scatter_staged<TAGIN, TO, 11>};
     launch_pdl(by_bits[bits], p.segs, kRadixThreads, staged_smem(B), s, v, in_rec, leaf_in, out_rec, bits,
-               tag_shift, p.counts);
+               tag_shift, p.counts, out_tag);
   } else {
     launch_pdl(scat, p.segs, kRadixThreads, ssm, s, v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,
                p.seg_tiles, p.tiles, p.counts);
@@ -535,10 +541,12 @@ int distribute_fmt(const SplitView& v, RadixPlan& p, void* leaf_out, cudaStream_
   if (p.bits[1] <= Rec<FMT>::kTagBits) {
     // the 2nd digit rides in the record pad: no scattered 4-B leaf-id stream (its partial
     // sectors cost read-modify-writes), the 2nd pass reads digits from the records
+    // f32: the 2nd digit also as a byte stream in destination order (after the input-order ids)
+    uint8_t* tags = FMT == LOD_POINTS_F32 ? reinterpret_cast<uint8_t*>(p.tmp_leaf + v.n) : nullptr;
     launches += run_pass<FMT, true, false, OUT_TAG>(v, v.pts, nullptr, p.tmp_leaf, p.tmp_rec, nullptr, 0,
-                                                    p.bits[0], p.bits[0], base0, p, s);
-    launches += run_pass<FMT, false, true, OUT_FINAL>(v, p.tmp_rec, nullptr, nullptr, leaf_out, nullptr, 0,
-                                                      p.bits[1], 0, base1, p, s);
+                                                    p.bits[0], p.bits[0], base0, p, s, tags);
+    launches += run_pass<FMT, false, true, OUT_FINAL>(v, p.tmp_rec, reinterpret_cast<const uint32_t*>(tags), nullptr,
+                                                      leaf_out, nullptr, 0, p.bits[1], 0, base1, p, s);
     return launches;
   }
   uint32_t* sorted_leaf = p.tmp_leaf + v.n;
