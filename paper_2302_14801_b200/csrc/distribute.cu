@@ -449,6 +449,143 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K_scatter, TMA form (f32 records, digits <= 9 bits: the 2-pass distributes of large clouds).
+// The staged kernel loads the tile's records only after ranking it; here one thread starts a
+// 1-D bulk copy (cp.async.bulk, completion on an mbarrier) of the tile's 64 KB of records into
+// shared memory at kernel entry, so the load streams in under the whole ranking.  Per local
+// slot one word {item in tile (12 b), digit (9 b), next pass's tag (8 b)} replaces the slot
+// arrays; the store pass gathers slot j's record from the stage and writes it to
+// run[d] + (j - first local slot of d).  102 KB of shared memory at B = 512: 2 CTAs per SM.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__host__ __device__ constexpr size_t tma_rows(int B) { return ((size_t)B * kRowWords * 4 + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t tma_smem(int B) {
+  return (size_t)kRadixTile * 16 + tma_rows(B) + (size_t)kRadixTile * 4 + (size_t)B * 8;
+}
+
+template <bool TAGIN, bool TAGOUT, int NB>
+__global__ void __launch_bounds__(kRadixThreads, 2)
+    k_dist_scatter_tma(SplitView v, const void* in_rec, const uint32_t* in_leaf, void* out_rec, int bits,
+                       int tag_shift, const uint32_t* firsts, uint8_t* out_tag) {
+  pdl_wait();
+  extern __shared__ __align__(128) uint32_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  const int B = 1 << bits;
+  uint4* srec = reinterpret_cast<uint4*>(sm);                                        // [tile] input order
+  uint32_t* wh = sm + kRadixTile * 4;                                                // [B][kRowWords]
+  uint32_t* sinfo = wh + tma_rows(B) / 4;                                            // [tile] per local slot
+  uint32_t* run = sinfo + kRadixTile;                                                // [B]
+  uint32_t* tf = run + B;                                                            // [B]
+  uint16_t* wh16 = reinterpret_cast<uint16_t*>(wh);
+  const uint32_t tile = gridDim.x - 1 - blockIdx.x;
+  const uint32_t tile_n = (uint32_t)min((uint64_t)kRadixTile, v.n - (uint64_t)tile * kRadixTile);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(tile_n * 16)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(srec)),
+                 "l"(reinterpret_cast<const uint4*>(in_rec) + (uint64_t)tile * kRadixTile), "r"(tile_n * 16),
+                 "r"(smem_u32(&bar))
+                 : "memory");
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const uint32_t n4 = (uint32_t)(((size_t)B * kRowWords + 3) / 4);
+    for (uint32_t i = threadIdx.x; i < n4; i += kRadixThreads) reinterpret_cast<uint4*>(wh)[i] = make_uint4(0, 0, 0, 0);
+    for (int d = threadIdx.x; d < B; d += kRadixThreads) run[d] = __ldcs(firsts + (uint64_t)tile * B + d);
+  }
+  const uint32_t item0 = (uint32_t)warp * 32 * K;
+  const uint64_t base = (uint64_t)tile * kRadixTile + item0;
+  const uint64_t last = v.n - 1;
+  uint32_t leaf[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const uint64_t i = min(base + (uint64_t)k * 32 + lane, last);
+    leaf[k] = TAGIN ? (uint32_t)__ldcs(reinterpret_cast<const uint8_t*>(in_leaf) + i) : __ldcs(in_leaf + i);
+  }
+  __syncthreads();
+  const uint32_t lt_mask = (1u << lane) - 1;
+  uint32_t rk[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const bool valid = base + (uint64_t)k * 32 + lane < v.n;
+    const uint32_t d = leaf[k] & (B - 1);
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, valid);
+    const unsigned peers = digit_peers<NB>(d, act);
+    uint32_t rank = 0;
+    if (valid) {
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (lane == leader) {
+        uint16_t* c = wh16 + (size_t)d * (2 * kRowWords) + warp;
+        old = *c;
+        *c = (uint16_t)(old + __popc(peers));
+      }
+      old = __shfl_sync(act, old, leader);
+      rank = old + __popc(peers & lt_mask);
+    }
+    rk[k] = rank;
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < B; d += kRadixThreads) {
+    uint32_t* row = wh + (size_t)d * kRowWords;
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < kW / 2; ++q) {
+      const uint32_t c = row[q], lo = c & 0xFFFF;
+      row[q] = r | ((r + lo) << 16);
+      r += lo + (c >> 16);
+    }
+    tf[d] = r;
+  }
+  __syncthreads();
+  {
+    __shared__ uint32_t wsum[kW + 1];
+    const int per = (B + kRadixThreads - 1) / kRadixThreads;
+    const int d0 = threadIdx.x * per;
+    uint32_t c = 0;
+    for (int j = 0; j < per; ++j) c += d0 + j < B ? tf[d0 + j] : 0;
+    uint32_t tot;
+    uint32_t x = block_excl_scan<uint32_t, kRadixThreads>(c, &tot, wsum);
+    for (int j = 0; j < per; ++j)
+      if (d0 + j < B) {
+        const uint32_t t = tf[d0 + j];
+        tf[d0 + j] = x;
+        x += t;
+      }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (base + (uint64_t)k * 32 + lane < v.n) {
+      const uint32_t d = leaf[k] & (B - 1);
+      const uint32_t slot = tf[d] + wh16[(size_t)d * (2 * kRowWords) + warp] + rk[k];
+      const uint32_t tag = TAGOUT ? (leaf[k] >> tag_shift) & 0xFF : 0u;
+      sinfo[slot] = (item0 + (uint32_t)k * 32 + lane) | (d << 12) | (tag << 21);
+    }
+  }
+  __syncthreads();
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(&bar))
+      : "memory");
+  for (uint32_t j = threadIdx.x; j < tile_n; j += kRadixThreads) {
+    const uint32_t info = sinfo[j];
+    const uint32_t d = (info >> 12) & 0x1FF;
+    uint4 r = srec[info & 0xFFF];
+    if (TAGOUT) r.w = (r.w & 0xFFFFFFu) | ((info >> 21) << 24);
+    if (TAGIN) r.w &= 0xFFFFFFu;
+    const uint32_t g = run[d] + (j - tf[d]);
+    reinterpret_cast<uint4*>(out_rec)[g] = r;
+    if (TAGOUT) out_tag[g] = (uint8_t)(info >> 21);
+  }
+}
+
 // Global exclusive prefix per digit, from the leaf counts (leaf ids are the sort keys).
 __global__ void k_digit_hist(const uint32_t* leaf_count, uint32_t n_leaves, int shift, int bits,
                              unsigned long long* hist) {
@@ -497,8 +634,17 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
         k_dist_scatter_staged<TAGIN, TO, 3>, k_dist_scatter_staged<TAGIN, TO, 4>, k_dist_scatter_staged<TAGIN, TO, 5>,
         k_dist_scatter_staged<TAGIN, TO, 6>, k_dist_scatter_staged<TAGIN, TO, 7>, k_dist_scatter_staged<TAGIN, TO, 8>,
         k_dist_scatter_staged<TAGIN, TO, 9>, k_dist_scatter_staged<TAGIN, TO, 10>, k_dist_scatter_staged<TAGIN, TO, 11>};
-    launch_pdl(by_bits[bits], p.segs, kRadixThreads, staged_smem(B), s, v, in_rec, leaf_in, out_rec, bits,
-               tag_shift, p.counts, out_tag);
+    const K by_bits_tma[10] = {
+        k_dist_scatter_tma<TAGIN, TO, 1>, k_dist_scatter_tma<TAGIN, TO, 1>, k_dist_scatter_tma<TAGIN, TO, 2>,
+        k_dist_scatter_tma<TAGIN, TO, 3>, k_dist_scatter_tma<TAGIN, TO, 4>, k_dist_scatter_tma<TAGIN, TO, 5>,
+        k_dist_scatter_tma<TAGIN, TO, 6>, k_dist_scatter_tma<TAGIN, TO, 7>, k_dist_scatter_tma<TAGIN, TO, 8>,
+        k_dist_scatter_tma<TAGIN, TO, 9>};
+    if (bits <= 9 && (reinterpret_cast<uintptr_t>(in_rec) & 15) == 0)  // records in flight under the ranking
+      launch_pdl(by_bits_tma[bits], p.segs, kRadixThreads, tma_smem(B), s, v, in_rec, leaf_in, out_rec, bits, tag_shift,
+                 p.counts, out_tag);
+    else
+      launch_pdl(by_bits[bits], p.segs, kRadixThreads, staged_smem(B), s, v, in_rec, leaf_in, out_rec, bits,
+                 tag_shift, p.counts, out_tag);
   } else {
     launch_pdl(scat, p.segs, kRadixThreads, ssm, s, v, in_rec, leaf_in, out_rec, out_leaf, shift, bits, tag_shift,
                p.seg_tiles, p.tiles, p.counts);
