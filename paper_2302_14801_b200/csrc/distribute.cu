@@ -152,8 +152,10 @@ __global__ void __launch_bounds__(1024) k_dist_scan_part(const uint32_t* counts,
   uint32_t g0, g1;
   rows_of(rows, seg_rows, blockIdx.y, warp, g0, g1);
   uint32_t sum = 0;
-  if (d < B)
+  if (d < B) {
+#pragma unroll 8
     for (uint32_t g = g0; g < g1; ++g) sum += __ldcg(counts + (uint64_t)g * B + d);
+  }
   sm[warp][lane] = sum;
   __syncthreads();
   if (warp == 0 && d < B) {
@@ -173,8 +175,10 @@ __global__ void __launch_bounds__(1024) k_dist_scan_apply(uint32_t* a, uint32_t 
   uint32_t g0, g1;
   rows_of(rows, seg_rows, blockIdx.y, warp, g0, g1);
   uint32_t sum = 0;
-  if (d < B)
+  if (d < B) {
+#pragma unroll 8
     for (uint32_t g = g0; g < g1; ++g) sum += a[(uint64_t)g * B + d];
+  }
   part[warp][lane] = sum;
   __syncthreads();
   if (warp == 0) {
@@ -186,9 +190,20 @@ __global__ void __launch_bounds__(1024) k_dist_scan_apply(uint32_t* a, uint32_t 
     }
   }
   __syncthreads();
-  if (d < B) {
+  if (d < B) {  // the loads run ahead of the dependent stores
     uint32_t run = part[warp][lane];
-    for (uint32_t g = g0; g < g1; ++g) {
+    uint32_t g = g0;
+    for (; g + 8 <= g1; g += 8) {
+      uint32_t c[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q] = a[(uint64_t)(g + q) * B + d];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        a[(uint64_t)(g + q) * B + d] = run;
+        run += c[q];
+      }
+    }
+    for (; g < g1; ++g) {
       const uint32_t c = a[(uint64_t)g * B + d];
       a[(uint64_t)g * B + d] = run;
       run += c;
