@@ -94,7 +94,7 @@ _add("many_leaves_stadium_300k_T60", ("ref", "stadium", 300_000, 8), dict(T=60),
 # BASELINE configs; float32 coordinates
 _add("sphere1M", ("syn", "sphere", 1_000_000, 1), dict(), ["random:0", "average"], quick=False)
 _add("terrain2M", ("syn", "terrain", 2_000_000, 2), dict(), ["average", "random:0"], quick=False)
-_add("terrain20M", ("syn", "terrain", 20_000_000, 2), dict(), ["average"], quick=False)
+_add("terrain20M", ("syn", "terrain", 20_000_000, 2), dict(), ["average", "random:0"], quick=False)
 _add("cluster1500k_T2000", ("syn", "cluster", 1_500_000, 4), dict(T=2000), ["average", "random:0"],
      quick=False)
 _add("scene2M", ("syn", "scene", 2_000_000, 3), dict(), ["average", "random:0"], quick=False)
