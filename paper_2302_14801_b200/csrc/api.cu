@@ -861,7 +861,6 @@ int do_voxelize(lod_tree* t, int mode, uint64_t seed, cudaStream_t s, const VoxP
         L.list_n = lst_n[d];
         L.chunk = voxelize_chunk(L.list_n);
         L.vchunk = voxelize_vchunk(L.list_n);
-        L.fuse = (mode == LOD_MODE_AVERAGE || mode == LOD_MODE_RANDOM) ? 1 : 0;
         if (has_back[L.parity]) CK(cudaStreamWaitEvent(t->vfront, e_back[L.parity], 0));
         CK(cudaMemsetAsync(L.bits + (size_t)L.parity * widest * kWordsPerNode, 0,
                            (size_t)L.list_n * kWordsPerNode * 4, t->vfront));

@@ -155,10 +155,6 @@ struct VoxNode {           // per inner node of the level being sampled (by list
   uint32_t ccount[8];
   int32_t cslot[8];        // -2 absent, -1 leaf child, >= 0 slot of an inner child
   uint64_t obase;          // first-come: first word of the node's ordinal bitmap
-  uint32_t nchunks;        // K3 chunks of the node's samples
-  uint32_t done;           // K3 chunks finished (the last one finalizes small nodes, L.fuse)
-  uint32_t fused;          // finalized by K3 (K4 skips it)
-  uint32_t pad_;
 };
 
 struct VoxLevel {
@@ -198,7 +194,6 @@ struct VoxLevel {
                            // with their exclusive popcount prefix: [2 w] bits, [2 w + 1] prefix
   uint64_t ocap;           // bitmap words of obits
   uint32_t chunk;          // samples per K1/K3 chunk
-  int fuse;                // K3's last chunk of a node finalizes it (average, random)
   uint32_t vchunk;         // voxels per K4 chunk
   int mode;
   int exact_sums;          // average: u64 sums (fallback) instead of f32 vector reductions

@@ -322,20 +322,23 @@ __device__ __forceinline__ bool is_anchor(const SplitView& v, uint32_t key) {
   return v.abits ? (__ldg(v.abits + (key >> 5)) >> (key & 31)) & 1 : v.t8[key] <= -2;
 }
 
-// Round 1 in two streaming kernels: k_ext_mark tests every point's main key (pkey, 4 B/pt)
-// against the anchor bitmap and appends the extension points {index, key} to the list (one
-// atomic per CTA trip, no record read); k_ext_project then takes the listed points one per
-// thread -- every record load independent and in flight at once -- projects each record to
-// its exact depth-16 cell, rewrites the entry in place {index, round-1 grid, x | y << 16, z}
-// and counts it (hot-counter cache).
-__global__ void __launch_bounds__(kThreads) k_ext_mark(SplitView v) {
+template <int FMT>
+__global__ void __launch_bounds__(kThreads) k_ext_first(SplitView v) {
   pdl_wait();
-  constexpr int U = 16;
+  constexpr int U = 8;   // 16 measured slower (registers: 3 CTAs/SM either way, +10% time)
+  __shared__ HotCounts<kHotSlots> hot;
   __shared__ uint32_t wsum[kThreads / 32 + 1];
   __shared__ unsigned long long lbase;
+  __shared__ uint32_t sidx[kThreads * U], skey[kThreads * U];  // this trip's extension points
+  hot.clear();
+  __syncthreads();
+  const DevState st = *v.st;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  uint32_t since_flush = 0;
   const uint64_t stream = policy_evict_first();
   for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < v.n; i0 += U * stride) {
+    // 1: which of this trip's points are extension points (anchor bitmap, no record read)
     uint32_t key[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) key[u] = ld_hint(v.pkey + min(i0 + u * stride, v.n - 1), stream);
@@ -344,39 +347,28 @@ __global__ void __launch_bounds__(kThreads) k_ext_mark(SplitView v) {
     for (int u = 0; u < U; ++u)
       if (i0 + u * stride < v.n && is_anchor(v, key[u])) flags |= 1u << u;
     uint32_t tot;
-    const uint32_t x = block_excl_scan<uint32_t, kThreads>((uint32_t)__popc(flags), &tot, wsum);
-    if (tot == 0) continue;  // uniform
-    if (threadIdx.x == 0) lbase = atomicAdd(&v.st->ext_n, (unsigned long long)tot);
-    __syncthreads();
-    uint64_t pos = lbase + x;
+    uint32_t x = block_excl_scan<uint32_t, kThreads>((uint32_t)__popc(flags), &tot, wsum);
+    if (tot == 0) continue;  // uniform: tot is the CTA's total
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if ((flags >> u) & 1) {
-        if (pos < v.elist_cap) v.elist[pos] = make_uint4((uint32_t)(i0 + u * stride), key[u], 0u, 0u);
-        ++pos;
-      }
-  }
-}
-
-template <int FMT>
-__global__ void __launch_bounds__(kThreads) k_ext_project(SplitView v) {
-  pdl_wait();
-  __shared__ HotCounts<kHotSlots> hot;
-  hot.clear();
-  __syncthreads();
-  const DevState st = *v.st;
-  const uint64_t n = min((uint64_t)st.ext_n, v.elist_cap);
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  bool bad = false;
-  uint32_t trip = 0;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j - threadIdx.x < n; j += stride) {
-    if (++trip % 64 == 0) hot.flush(v.pyr);  // uniform
-    if (j < n) {
-      const uint4 q = v.elist[j];
-      const Cell16 c = cell16<FMT>(Rec<FMT>::load(v.pts, q.x), st, bad);
-      const int32_t t = v.t8[q.y];
-      v.elist[j] = make_uint4(q.x, (uint32_t)(-(t + 2)), c.x | (c.y << 16), c.z);
+      if ((flags >> u) & 1) sidx[x] = (uint32_t)(i0 + u * stride), skey[x] = key[u], ++x;
+    if (threadIdx.x == 0) lbase = atomicAdd(&v.st->ext_n, (unsigned long long)tot);
+    __syncthreads();
+    // 2: the trip's extension points, densely over the CTA: project once, list, count
+    for (uint32_t j = threadIdx.x; j < tot; j += kThreads) {
+      const uint32_t i = sidx[j];
+      const Cell16 c = cell16<FMT>(Rec<FMT>::load(v.pts, i), st, bad);
+      const int32_t t = v.t8[skey[j]];
+      const uint64_t pos = lbase + j;
+      if (pos < v.elist_cap) v.elist[pos] = make_uint4(i, (uint32_t)(-(t + 2)), c.x | (c.y << 16), c.z);
       ext_count_point(v, hot, c, t, 0);
+    }
+    since_flush += tot;
+    if (since_flush >= 16384) {  // uniform
+      hot.flush(v.pyr);
+      since_flush = 0;
+    } else {
+      __syncthreads();  // sidx / skey / lbase are rewritten by the next trip
     }
   }
   hot.flush(v.pyr);
@@ -408,12 +400,11 @@ __global__ void __launch_bounds__(kThreads) k_ext_more(SplitView v, uint32_t rou
 int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStream_t s) {
   if (round_first == 0) {
     uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
-    launch_pdl(k_ext_mark, blocks, kThreads, 0, s, v);
-    if (fmt == LOD_POINTS_F32) launch_pdl(k_ext_project<LOD_POINTS_F32>, 148 * 8, kThreads, 0, s, v);
-    else launch_pdl(k_ext_project<LOD_POINTS_F64>, 148 * 8, kThreads, 0, s, v);
-    return 2;
+    if (fmt == LOD_POINTS_F32) launch_pdl(k_ext_first<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
+    else launch_pdl(k_ext_first<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
+  } else {
+    launch_pdl(k_ext_more, 148 * 8, kThreads, 0, s, v, round_first);
   }
-  launch_pdl(k_ext_more, 148 * 8, kThreads, 0, s, v, round_first);
   return 1;
 }
 

@@ -50,7 +50,6 @@ constexpr uint32_t kBlkWords = 4096;         // words per K2 block
 constexpr uint32_t kBlksPerNode = kWords / kBlkWords;
 constexpr uint32_t kVoxChunk = 2048;         // voxels per K4 chunk
 constexpr int kT = 256;
-constexpr uint32_t kFuseMax = 1u << 16;       // nodes K3 finalizes in one CTA (larger: K4)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -119,9 +118,6 @@ __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
   const bool empty = emask != 0;
   // the reference raises on the first empty child in octant order (sampling.py:33-35)
   const int32_t empty_child = __shfl_sync(0xFFFFFFFFu, c, (threadIdx.x & 24) + (empty ? __ffs(emask) - 1 : 0));
-  uint32_t nch_all = (cnt + L.chunk - 1) / L.chunk;  // the node's K3 chunks (all octants)
-#pragma unroll
-  for (int d = 1; d < 8; d <<= 1) nch_all += __shfl_xor_sync(0xFFFFFFFFu, nch_all, d, 8);
   if (!live) return;
   VoxNode& info = L.info[s];
   info.cbase[o] = incl - cnt;
@@ -149,9 +145,6 @@ __global__ void __launch_bounds__(kT) k_setup(VoxLevel L) {
     info.vbase = 0;
     info.m = 0;
     info.skip = skip;
-    info.nchunks = skip ? 0u : nch_all;
-    info.done = 0;
-    info.fused = 0;
     L.node_slot[node] = s;
     if (empty) raise_err(L.st, ERR_EMPTY_CHILD, (uint32_t)empty_child);
     else if (skip) raise_err(L.st, ERR_RANDOM_LIMIT, node, S);
@@ -435,9 +428,6 @@ __device__ __forceinline__ uint32_t rank_of(const uint32_t* bits, const uint32_t
 // bits + prefixes are staged in shared memory, so a sample's rank costs two shared loads;
 // only the accumulator atomics reach L2.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void finalize_voxel(const VoxLevel& L, const VoxNode& nd, uint64_t acc0, uint32_t key,
-                                               uint32_t r);
-
 __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
   pdl_wait();
   if (L.st->err & ERR_ARENA) return;
@@ -509,28 +499,6 @@ __global__ void __launch_bounds__(kRT, 2) k_scatter(VoxLevel L) {
       }
     }
     __syncthreads();
-    if (L.fuse) {
-      // the CTA finishing a node's last chunk finalizes it while its accumulators are still in
-      // L2 (K4 skips it), then drops the node's accumulator lines from L2 without writing them
-      // back (discard.global.L2: they are dead; the next user zeroes them first)
-      __shared__ uint32_t s_last;
-      if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&L.info[ch.x].done, 1u) + 1 == nd.nchunks && nd.m <= kFuseMax;
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        for (uint32_t r = threadIdx.x; r < nd.m; r += kRT) finalize_voxel(L, nd, acc0, __ldcg(&L.vox[nd.vbase + r].x), r);
-        if (threadIdx.x == 0) L.info[ch.x].fused = 1;
-        __syncthreads();
-        const uint32_t stride = L.mode == LOD_MODE_AVERAGE ? (L.exact_sums ? 32u : 16u) : 4u;  // voxelize_acc_bytes
-        const uint64_t b0 = (reinterpret_cast<uint64_t>(L.acc) + acc0 * stride + 127) & ~127ull;
-        const uint64_t b1 = (reinterpret_cast<uint64_t>(L.acc) + (acc0 + nd.m) * stride) & ~127ull;
-        for (uint64_t b = b0 + 128ull * threadIdx.x; b < b1; b += 128ull * kRT)
-          asm volatile("discard.global.L2 [%0], 128;" ::"l"(b) : "memory");
-      }
-    }
   }
 }
 
@@ -696,7 +664,6 @@ __global__ void __launch_bounds__(kT) k_finalize(VoxLevel L) {
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
     const uint2 ch = L.vchunks[c];
     const VoxNode& nd = L.info[ch.x];
-    if (nd.fused) continue;  // finalized by K3
     const uint32_t r1 = min(nd.m, ch.y + L.vchunk);
     const uint64_t acc0 = nd.vbase - L.level_start[0];
     for (uint32_t r = ch.y + threadIdx.x; r < r1; r += kT) finalize_voxel(L, nd, acc0, __ldcg(&L.vox[nd.vbase + r].x), r);

@@ -49,9 +49,10 @@ def unpack_records(raw: np.ndarray, fmt: int):
     return pos, col
 
 
-_STAGE = {}          # device -> (pinned staging buffers, events, copy stream)
+_STAGE = {}          # device -> (pinned staging buffers, events, copy stream, lock)
 _STAGE_BYTES = 32 << 20
 _POOL = None
+_STAGE_LOCK = None
 
 
 def host_to_device(arr: np.ndarray, device: int):
@@ -67,25 +68,32 @@ def host_to_device(arr: np.ndarray, device: int):
         if nb:
             out.copy_(torch.from_numpy(src))
         return out[:nb]
-    if device not in _STAGE:
-        bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-        _STAGE[device] = (bufs, [torch.cuda.Event(), torch.cuda.Event()], torch.cuda.Stream(device))
-    bufs, evs, cs = _STAGE[device]
-    if _POOL is None:
-        import concurrent.futures as cf
-        _POOL = cf.ThreadPoolExecutor(8)
-    cs.wait_stream(torch.cuda.current_stream(device))
-    for k, off in enumerate(range(0, nb, _STAGE_BYTES)):
-        m = min(_STAGE_BYTES, nb - off)
-        b = k & 1
-        evs[b].synchronize()                      # the DMA that last read this buffer is done
-        dst = bufs[b].numpy()
-        parts = [(a, min(m, a + (m + 7) // 8)) for a in range(0, m, (m + 7) // 8)]
-        list(_POOL.map(lambda ab: np.copyto(dst[ab[0]:ab[1]], src[off + ab[0]:off + ab[1]]), parts))
-        with torch.cuda.stream(cs):
-            out[off:off + m].copy_(bufs[b][:m], non_blocking=True)
-            evs[b].record(cs)
-    torch.cuda.current_stream(device).wait_stream(cs)
+    global _STAGE_LOCK
+    import threading
+    if _STAGE_LOCK is None:
+        _STAGE_LOCK = threading.Lock()
+    with _STAGE_LOCK:   # one staging ring per device, shared by every caller thread
+        if device not in _STAGE:
+            bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            _STAGE[device] = (bufs, [torch.cuda.Event(), torch.cuda.Event()], torch.cuda.Stream(device),
+                              threading.Lock())
+        if _POOL is None:
+            import concurrent.futures as cf
+            _POOL = cf.ThreadPoolExecutor(8)
+    bufs, evs, cs, lock = _STAGE[device]
+    with lock:
+        cs.wait_stream(torch.cuda.current_stream(device))
+        for k, off in enumerate(range(0, nb, _STAGE_BYTES)):
+            m = min(_STAGE_BYTES, nb - off)
+            b = k & 1
+            evs[b].synchronize()                      # the DMA that last read this buffer is done
+            dst = bufs[b].numpy()
+            parts = [(a, min(m, a + (m + 7) // 8)) for a in range(0, m, (m + 7) // 8)]
+            list(_POOL.map(lambda ab: np.copyto(dst[ab[0]:ab[1]], src[off + ab[0]:off + ab[1]]), parts))
+            with torch.cuda.stream(cs):
+                out[off:off + m].copy_(bufs[b][:m], non_blocking=True)
+                evs[b].record(cs)
+        torch.cuda.current_stream(device).wait_stream(cs)
     return out[:nb]
 
 
@@ -148,7 +156,10 @@ def use_torch_allocator(enable: bool = True):
             return None
 
     def free(ptr, nbytes, device, ctx):
-        torch.cuda.caching_allocator_delete(int(ptr))
+        try:
+            torch.cuda.caching_allocator_delete(int(ptr))
+        except Exception:   # interpreter shutdown: torch may already be gone
+            pass
 
     _ALLOCATOR = (_ALLOC_FN(alloc), _FREE_FN(free))   # keep the thunks alive
     _abi.check(lib.lod_set_allocator(C.cast(_ALLOCATOR[0], C.c_void_p), C.cast(_ALLOCATOR[1], C.c_void_p), None))
