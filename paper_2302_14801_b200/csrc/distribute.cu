@@ -94,13 +94,12 @@ __global__ void __launch_bounds__(kRadixThreads, 3)
   pdl_wait();
   extern __shared__ __align__(16) uint32_t hist[];
   const int B = 1 << bits;
+  for (int d = threadIdx.x; d < B; d += kRadixThreads) hist[d] = 0;
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   bool unresolved = false;
-  // persistent CTAs: one 4096-point tile (one row of counts) per trip
-  (void)seg_tiles;
-  for (uint32_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    for (int d = threadIdx.x; d < B; d += kRadixThreads) hist[d] = 0;
-    __syncthreads();
+  const uint32_t t0 = blockIdx.x * seg_tiles, t1 = min(t0 + seg_tiles, tiles);
+  for (uint32_t tile = t0; tile < t1; ++tile) {
     const uint64_t base = (uint64_t)tile * kRadixTile + (uint64_t)warp * 32 * K;
     uint32_t leaf[K];
     load_items<FMT, FIRST, TAGIN>(v, in_rec, in_leaf, leaf_out, base, lane, leaf, unresolved);
@@ -119,10 +118,9 @@ __global__ void __launch_bounds__(kRadixThreads, 3)
         atomicAdd(hist + d, 1u);
       }
     }
-    __syncthreads();
-    for (int d = threadIdx.x; d < B; d += kRadixThreads) counts[(uint64_t)tile * B + d] = hist[d];
-    __syncthreads();
   }
+  __syncthreads();
+  for (int d = threadIdx.x; d < B; d += kRadixThreads) counts[(uint64_t)blockIdx.x * B + d] = hist[d];
   if (FIRST) {
     if (__any_sync(0xFFFFFFFFu, unresolved) && lane == 0) raise_err(v.st, ERR_UNRESOLVED);
   }
@@ -635,11 +633,7 @@ int run_pass(const SplitView& v, const void* in_rec, const uint32_t* in_leaf, ui
   auto scat = k_dist_scatter<FMT, TAGIN, OUT>;
   const size_t hsm = (size_t)B * 4, ssm = (size_t)B * 8 + (size_t)kW * B * 2 + 4 * kW;
   const uint32_t* leaf_in = FIRST ? leaf_tmp : in_leaf;
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  launch_pdl(hist, std::min<uint32_t>(p.tiles, (uint32_t)sms * 3), kRadixThreads, hsm, s, v, in_rec, in_leaf, leaf_tmp,
-             shift, bits, p.seg_tiles, p.tiles, p.counts);
+  launch_pdl(hist, p.segs, kRadixThreads, hsm, s, v, in_rec, in_leaf, leaf_tmp, shift, bits, p.seg_tiles, p.tiles, p.counts);
   if (FIRST && p.aux) cudaStreamWaitEvent(s, p.aux_ev[1], 0);  // the digit bases
   const int nscan = launch_dist_scan(p.counts, p.segs, B, digit_base, p.scan_part, s);
   const cudaEvent_t* ev = p.scatter_ev + (FIRST ? 0 : 2);
