@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(kRadixThreads, 3)
       const bool valid = base + (uint64_t)k * 32 + lane < v.n;
       if (FIRST && valid) leaf_out[base + (uint64_t)k * 32 + lane] = leaf[k];  // the scatter reuses it
       const uint32_t d = (leaf[k] >> shift) & (B - 1);
+      if (TAGIN) {  // 2nd pass: the records are sorted by the 1st digit, the 2nd is scattered
+        if (valid) atomicAdd(hist + d, 1u);
+        continue;
+      }
       // warp-uniform digit (coherent scans): one add; otherwise plain shared atomics
       // (MATCH.ANY would saturate the MIO pipe: it was the top stall here)
       const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);

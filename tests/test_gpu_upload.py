@@ -54,3 +54,21 @@ def test_partition_of_float64_cloud_uses_f32_records_when_exact():
     pos[5] += 1e-12   # no longer exact in float32
     tree = partition(PointCloud(pos, col), BuildConfig(T=5000))
     assert tree.device_tree.info().point_format == 1
+
+
+def test_trees_allocate_through_torch_and_workspace_estimate():
+    """lod_set_allocator routes the trees' buffers through torch's caching allocator (so torch
+    sees the HBM they hold); lod_workspace_bytes bounds a surface-like build's need."""
+    import torch
+    from paper_2302_14801_b200 import BuildConfig, PointCloud, partition, build_lod
+    from paper_2302_14801_b200.device import workspace_bytes
+    from paper_2302_14801_b200.generators import synthetic_cloud
+    pos, col = synthetic_cloud("sphere", 1_000_000, 1)
+    before = torch.cuda.memory_allocated()
+    tree = partition(PointCloud(pos.astype(np.float64), col), BuildConfig())
+    build_lod(tree, "average", 0)
+    held = tree.device_tree.device_bytes()
+    assert held > 0 and torch.cuda.memory_allocated() - before >= held
+    assert workspace_bytes(len(pos)) >= held
+    tree.device_tree.close()
+    assert torch.cuda.memory_allocated() - before < held
