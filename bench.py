@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--cpu-runs", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-target", action="store_true", help="skip the north-star 1B-point scene measurement")
     ap.add_argument("--e2e-api-config", default="terrain20M",
                     help="config of the Python-API e2e leg ('' to skip)")
     ap.add_argument("--stages", action="store_true", help="also print per-stage device times to stderr")
@@ -434,6 +435,35 @@ def e2e_api(torch, config, mode, steps, warmup):
     return out
 
 
+def north_star_target(torch, mode, n, steps):
+    """BASELINE north star: >= 4 G pts/s with color filtering on 1 B200 for a 1B-point cloud
+    (scene generator, first 1e9 rows; parity: tests/test_gpu_large.py test_full_cloud[scene1B])."""
+    from paper_2302_14801_b200 import _abi
+    from paper_2302_14801_b200.device import DeviceTree, generate_device, make_config
+    from paper_2302_14801_b200.sampling import _mode_code
+    d = generate_device("scene", n, 3)
+    dev = DeviceTree()
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    cfg = make_config(50_000)
+    for _ in range(2):
+        dev.build(d, n, _abi.LOD_POINTS_F32, cfg, _mode_code(mode), 0, stream=sp)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        dev.build(d, n, _abi.LOD_POINTS_F32, cfg, _mode_code(mode), 0, stream=sp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    dev.close()
+    del d
+    torch.cuda.empty_cache()
+    return {"workload": "scene, first 1e9 rows (north-star target >= 4 G pts/s)", "points": n, "mode": mode,
+            "value": n / (ms / 1000.0), "unit": "points/s", "ms_per_step": ms, "steps": steps,
+            "vs_target": n / (ms / 1000.0) / 4e9}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -565,6 +595,16 @@ def main():
     if world == 1 and not args.no_e2e and args.e2e_api_config:
         api = e2e_api(torch, args.e2e_api_config, args.mode, max(3, min(args.steps, 10)), 2)
 
+    device_bytes = dev.device_bytes()
+    target = None
+    if world == 1 and not args.no_target and args.config != "scene1B":
+        # the north star's own target (>= 4 G pts/s color filtering on a 1B-point cloud): the
+        # first 1e9 rows of the scene generator, device time of `target_steps` builds
+        del d_in
+        dev.close()
+        torch.cuda.empty_cache()
+        target = north_star_target(torch, args.mode, 1_000_000_000, 3)
+
     # ---- roofline (SURVEY 8(d) algorithmic bytes: B = 80 N + 16 E + 12 V) ----
     # Dominant single kernel: the distribute's K_scatter (stable counting-sort scatter), the
     # longest kernel of a build (ncu launch lists in profiles/).  Algorithmic bytes: each
@@ -582,8 +622,9 @@ def main():
     traffic = measured_traffic(args.config, mode_key, n, "k_dist_scatter") if world == 1 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
-                "kernel": f"K_scatter (distribute.cu k_dist_scatter_staged, f32 records), {passes} radix pass(es) "
-                          f"timed together against one read + one write per record",
+                "kernel": f"K_scatter (distribute.cu: k_dist_scatter_tma for the <= 9-bit digits of a 2-pass sort, "
+                          f"k_dist_scatter_staged for one pass), {passes} radix pass(es) timed together against one "
+                          f"read + one write per record",
                 "algorithmic_bytes": kern_bytes, "ms_per_build": scatter_ms, "peak_source": peak_kind,
                 "stages": {nm: {"ms": st, "algorithmic_bytes": b,
                                 "achieved_gbs": (b / (st / 1000.0) / 1e9) if b and st else None,
@@ -620,7 +661,8 @@ def main():
             "stages_ms": dict(zip(stage_names, stages)),
             "tree": {"nodes": info.n_nodes, "leaves": info.n_leaves, "depth": info.depth, "voxels": V,
                      "ext_grids": info.n_ext_grids, "ext_points": E, "radix_passes": info.radix_passes,
-                     "device_bytes": dev.device_bytes()},
+                     "device_bytes": device_bytes},
+            "north_star_target": target,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
