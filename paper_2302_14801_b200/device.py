@@ -113,10 +113,11 @@ def generate_device(kind: str, n: int, seed: int, start: int = 0, out=None):
     stream = C.c_void_p(torch.cuda.current_stream(buf.device).cuda_stream)
     tptr = C.cast(C.c_void_p(table.data_ptr()), C.POINTER(C.c_double)) if table is not None else None
     chunk = 1 << 28
-    for s in range(0, n, chunk):
-        m = min(chunk, n - s)
-        _abi.check(lib.lod_generate(kind.encode(), seed, start + s, m, C.c_void_p(buf.data_ptr() + s * 16), tptr,
-                                    stream))
+    with torch.cuda.device(buf.device):   # lod_generate launches on the current device
+        for s in range(0, n, chunk):
+            m = min(chunk, n - s)
+            _abi.check(lib.lod_generate(kind.encode(), seed, start + s, m, C.c_void_p(buf.data_ptr() + s * 16), tptr,
+                                        stream))
     torch.cuda.current_stream(buf.device).synchronize()
     return buf
 
@@ -224,10 +225,11 @@ class DeviceTree:
         d_rgb = host_to_device(col, self.device)
         out = torch.empty(max(n, 1) * (32 if (f64 and fmt != LOD_POINTS_F32) else 16), dtype=torch.uint8, device=dev)
         chosen = C.c_int(-1)
-        _abi.check(self.lib.lod_pack_points(C.c_void_p(d_xyz.data_ptr()), 1 if f64 else 0,
-                                            C.c_void_p(d_rgb.data_ptr()), n, -1 if fmt is None else int(fmt),
-                                            C.c_void_p(out.data_ptr()), C.byref(chosen),
-                                            current_stream_ptr(self.device)))
+        with torch.cuda.device(self.device):   # lod_pack_points runs on the current device
+            _abi.check(self.lib.lod_pack_points(C.c_void_p(d_xyz.data_ptr()), 1 if f64 else 0,
+                                                C.c_void_p(d_rgb.data_ptr()), n, -1 if fmt is None else int(fmt),
+                                                C.c_void_p(out.data_ptr()), C.byref(chosen),
+                                                current_stream_ptr(self.device)))
         fmt = chosen.value
         return out[: n * (16 if fmt == LOD_POINTS_F32 else 32)], fmt, n
 
