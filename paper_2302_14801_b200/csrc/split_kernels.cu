@@ -375,66 +375,6 @@ __global__ void __launch_bounds__(kThreads) k_ext_first(SplitView v) {
   if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) raise_err(v.st, ERR_OUTSIDE);
 }
 
-// Dense extension points (more than 1 in 32 points): the scattered record loads of the
-// listed points would fetch most of the record array anyway at a fraction of its bandwidth
-// (1 in 10 points at cluster2B: 34 GB of DRAM reads, 12 ms), so this variant streams every
-// record once, coalesced, next to its key, and projects only the extension points; each
-// thread appends its own points (one atomic per CTA trip for the list cursor).
-template <int FMT>
-__global__ void __launch_bounds__(kThreads) k_ext_first_dense(SplitView v) {
-  pdl_wait();
-  constexpr int U = 4;
-  __shared__ HotCounts<kHotSlots> hot;
-  __shared__ uint32_t wsum[kThreads / 32 + 1];
-  __shared__ unsigned long long lbase;
-  hot.clear();
-  __syncthreads();
-  const DevState st = *v.st;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  bool bad = false;
-  uint32_t since_flush = 0;
-  const uint64_t stream = policy_evict_first();
-  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < v.n; i0 += U * stride) {
-    typename Rec<FMT>::Raw r[U];
-    uint32_t key[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t i = min(i0 + u * stride, v.n - 1);
-      key[u] = ld_hint(v.pkey + i, stream);
-      r[u] = Rec<FMT>::load_cs(v.pts, i);
-    }
-    uint32_t flags = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (i0 + u * stride < v.n && is_anchor(v, key[u])) flags |= 1u << u;
-    uint32_t tot;
-    const uint32_t x = block_excl_scan<uint32_t, kThreads>((uint32_t)__popc(flags), &tot, wsum);
-    if (tot == 0) continue;  // uniform
-    if (threadIdx.x == 0) lbase = atomicAdd(&v.st->ext_n, (unsigned long long)tot);
-    __syncthreads();
-    uint64_t pos = lbase + x;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!((flags >> u) & 1)) continue;
-      const Cell16 c = cell16<FMT>(r[u], st, bad);
-      const int32_t t = v.t8[key[u]];
-      if (pos < v.elist_cap)
-        v.elist[pos] = make_uint4((uint32_t)(i0 + u * stride), (uint32_t)(-(t + 2)), c.x | (c.y << 16), c.z);
-      ++pos;
-      ext_count_point(v, hot, c, t, 0);
-    }
-    since_flush += tot;
-    if (since_flush >= 16384) {  // uniform
-      hot.flush(v.pyr);
-      since_flush = 0;
-    } else {
-      __syncthreads();  // lbase is rewritten by the next trip
-    }
-  }
-  hot.flush(v.pyr);
-  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) raise_err(v.st, ERR_OUTSIDE);
-}
-
 __global__ void __launch_bounds__(kThreads) k_ext_more(SplitView v, uint32_t round_first) {
   pdl_wait();
   __shared__ HotCounts<kHotSlots> hot;
@@ -460,11 +400,8 @@ __global__ void __launch_bounds__(kThreads) k_ext_more(SplitView v, uint32_t rou
 int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStream_t s) {
   if (round_first == 0) {
     uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
-    const bool dense = v.elist_cap > v.n / 32;  // extension points among the records
-    if (fmt == LOD_POINTS_F32)
-      launch_pdl(dense ? k_ext_first_dense<LOD_POINTS_F32> : k_ext_first<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
-    else
-      launch_pdl(dense ? k_ext_first_dense<LOD_POINTS_F64> : k_ext_first<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
+    if (fmt == LOD_POINTS_F32) launch_pdl(k_ext_first<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
+    else launch_pdl(k_ext_first<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
   } else {
     launch_pdl(k_ext_more, 148 * 8, kThreads, 0, s, v, round_first);
   }
