@@ -491,6 +491,18 @@ def main():
     mode_code = _mode_code(args.mode)
     cfg = make_config(50_000)
 
+    from paper_2302_14801_b200.device import workspace_bytes
+    need = n * 16 + workspace_bytes(n, _abi.LOD_POINTS_F32, cfg, mode_code)
+    free, _ = torch.cuda.mem_get_info()
+    if need > free:   # e.g. surface4B (4e9 points) on one GPU: run it with --gpus >= 2
+        if rank == 0:
+            print(json.dumps({"metric": f"LOD construction points/sec ({args.mode})", "value": None,
+                              "unit": "points/s", "n_gpus": world,
+                              "config": {"workload": args.config, "points": n_total, "points_per_gpu": n},
+                              "unavailable": f"{n} points per GPU need ~{need / 1e9:.0f} GB "
+                                             f"(input + lod_workspace_bytes), {free / 1e9:.0f} GB free: use more GPUs"}),
+                  flush=True)
+        return
     d_in = make_input_device(torch, kind, n, seed, start=start)
     dev = DeviceTree(local)
     stream = torch.cuda.current_stream()
