@@ -231,6 +231,45 @@ uint64_t lod_tree_launches(const lod_tree* tree);
 int lod_pack_points(const void* d_xyz, int xyz_is_f64, const uint8_t* d_rgb, uint64_t n, int out_format,
                     void* d_records, int* chosen_format, void* stream);
 
+/* ---------------------------------------------------------------------------------
+ * Stage-level access (the reference's Partitioner stages and module functions,
+ * partition.py:36-287), for callers that drive count / extend / merge / targets / insert
+ * one at a time: the single-GPU build runs through the lod_dist_* stages with one rank.
+ * ------------------------------------------------------------------------------- */
+/* merge_pyramid(finest, T) (partition.py:36-61): d_pyr holds the levels of one pyramid, level l
+ * at (8^l - 1) / 7 u32 cells, x-major; the finest level L is the input (counts or 0xFFFFFFFF =
+ * UNMERGEABLE); levels L-1..0 are computed in place and merged children zeroed. */
+int lod_merge_pyramid(uint32_t* d_pyr, int L, uint32_t T, void* stream);
+/* the main finest-grid key of every point (pkey: (cx * dim + cy) * dim + cz), n entries */
+int lod_tree_copy_point_keys(const lod_tree* tree, uint32_t* h_keys, void* stream);
+/* every counting pyramid of the last split (main pyramid at 0, extension pyramids at their
+ * pyr_off), u32 per cell after the merge; h_cells NULL: *n_out = the number of cells */
+int lod_tree_copy_pyramids(const lod_tree* tree, uint32_t* h_cells, uint64_t* n_out, void* stream);
+typedef struct lod_ext_grid {
+  uint64_t pyr_off;        /* its pyramid in the pyramid buffer (levels 0..ext) */
+  uint16_t ax, ay, az;     /* anchor cell, absolute coordinates at depth base */
+  uint8_t base, ext;       /* anchor depth, levels below it */
+} lod_ext_grid;
+/* the extension grids (partition.py:64-76 ExtendedPyramid), h NULL: *n_out = their number */
+int lod_tree_ext_grids(const lod_tree* tree, lod_ext_grid* h, uint32_t* n_out, void* stream);
+/* the extension points: input index and depth-16 cell (x | y << 16 | z << 32); h NULL: count */
+int lod_tree_ext_points(const lod_tree* tree, uint32_t* h_index, uint64_t* h_cell16, uint64_t* n_out,
+                        void* stream);
+
+/* The reference's per-node sampling helpers on ONE node's sample list (sampling.py:21-133), for
+ * callers driving the stages themselves:
+ * lod_project_samples: one child's samples into the parent's 128^3 grid -- kind 0: n leaf points
+ *   (f64 xyz) -> clip((p - min) / size * 128, 0, nextafter(128, 0)); kind 1: n child voxels
+ *   (u8 xyz) in octant `octant` -> off + (c + 0.5) / 2; d_gpos: n x 3 f64 (sampling.py:29-44).
+ * lod_extract: extract_first_come / _random / _average / _weighted (mode = lod_mode) on S grid
+ *   positions (f64 x 3) + colours (u8 x 3); writes the m voxels' u8 coordinates and colours
+ *   (buffers of S x 3 bytes) in the reference's stored order and *m_out.  random: seed and the
+ *   node's path_hash (rng.py:48-53); raises the reference's 2^20 ConsistencyError. */
+int lod_project_samples(int kind, const void* d_in, uint64_t n, const double* node_min3, double node_size,
+                        int octant, double* d_gpos, void* stream);
+int lod_extract(int mode, const double* d_gpos, const uint8_t* d_rgb, uint64_t S, uint64_t seed,
+                uint64_t node_hash, uint8_t* d_coords, uint8_t* d_colors, uint64_t* m_out, void* stream);
+
 /* Deterministic synthetic generators on the device, rows
  * [start, start+n) of cloud `kind` ("sphere", "terrain", "scene", "cluster", "surface")
  * written as LOD_POINTS_F32 records.  `table`: scene object table from the host

@@ -136,6 +136,7 @@ class Split:
     world: tuple                   # (lo xyz, size)
     config: dict
     nodes: dict                    # path -> Node
+    top: object = None             # the main _Tier (stage values: counts, subs, levels, refs)
 
 
 def split(pos, T=50_000, initial_depth=8, extension_depth=4, max_depth=16, bounds=None) -> Split:
@@ -249,7 +250,7 @@ def split(pos, T=50_000, initial_depth=8, extension_depth=4, max_depth=16, bound
             raise ConsistencyError("leaf received a different count than allocated")
         nodes[path].idx = sel
     cfg = dict(T=T, initial_depth=initial_depth, extension_depth=extension_depth, max_depth=max_depth)
-    return Split(((float(lo[0]), float(lo[1]), float(lo[2])), float(size)), cfg, nodes)
+    return Split(((float(lo[0]), float(lo[1]), float(lo[2])), float(size)), cfg, nodes, top)
 
 
 # ---------------------------------------------------------------------------

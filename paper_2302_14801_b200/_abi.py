@@ -37,6 +37,11 @@ class LodNode(C.Structure):
                 ("child", C.c_int32 * 8)]
 
 
+class LodExtGrid(C.Structure):
+    _fields_ = [("pyr_off", C.c_uint64), ("ax", C.c_uint16), ("ay", C.c_uint16), ("az", C.c_uint16),
+                ("base", C.c_uint8), ("ext", C.c_uint8)]
+
+
 class LodSpan(C.Structure):
     _fields_ = [("ptr", C.c_void_p), ("n", C.c_uint64)]
 
@@ -84,6 +89,14 @@ SIGNATURES = [
     ("lod_tree_kernel_ms", C.c_int, [_P, C.POINTER(C.c_float)]),
     ("lod_tree_launches", C.c_uint64, [_P]),
     ("lod_pack_points", C.c_int, [_P, C.c_int, _P, C.c_uint64, C.c_int, _P, C.POINTER(C.c_int), _P]),
+    ("lod_merge_pyramid", C.c_int, [_P, C.c_int, C.c_uint32, _P]),
+    ("lod_tree_copy_point_keys", C.c_int, [_P, _P, _P]),
+    ("lod_tree_copy_pyramids", C.c_int, [_P, _P, C.POINTER(C.c_uint64), _P]),
+    ("lod_tree_ext_grids", C.c_int, [_P, _P, C.POINTER(C.c_uint32), _P]),
+    ("lod_tree_ext_points", C.c_int, [_P, _P, _P, C.POINTER(C.c_uint64), _P]),
+    ("lod_project_samples", C.c_int, [C.c_int, _P, C.c_uint64, C.POINTER(C.c_double), C.c_double, C.c_int, _P, _P]),
+    ("lod_extract", C.c_int, [C.c_int, _P, _P, C.c_uint64, C.c_uint64, C.c_uint64, _P, _P, C.POINTER(C.c_uint64),
+                              _P]),
     ("lod_generate", C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint64, _P, C.POINTER(C.c_double), _P]),
     ("lod_dist_begin", C.c_int, [_P, _P, C.c_uint64, C.c_int, C.POINTER(LodConfig), _P, _P]),
     ("lod_dist_count", C.c_int, [_P, C.c_uint64, _P, C.POINTER(LodSpan), _P]),

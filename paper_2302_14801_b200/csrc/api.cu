@@ -330,6 +330,11 @@ int ceil_log2(uint64_t x) {
     t->launches += _r;       \
   } while (0)
 
+#define RUN_NOTREE(expr)     \
+  do {                       \
+    if ((expr) < 0) return fail(LOD_ECUDA, "internal scratch too small: %s", #expr); \
+  } while (0)
+
 void mark(lod_tree* t, int i, cudaStream_t s) {
   if (t->timing) cudaEventRecord(t->ev[i], s);
 }
@@ -948,6 +953,7 @@ int dist_count(lod_tree* t, uint64_t n_global, const double* world, lod_span* ou
   RUN(launch_bounds(t->fmt, t->pts, t->n, v.st, world, s));  // forced (global) cube
   int r = phase_count(t, s);
   if (r) return r;
+  if ((r = read_state(t, s)) || (r = check_errors(t, s))) return r;  // points outside the cube
   const uint64_t fine = 1ull << (3 * t->cfg.initial_depth);
   CK(ensure(t->local_main, fine * 4));
   CK(cudaMemcpyAsync(t->local_main.p, t->pyr.as<uint32_t>() + level_off(t->cfg.initial_depth), fine * 4,
@@ -1428,6 +1434,69 @@ int lod_dist_copy_segments(lod_tree* t, const void* d_src, void* d_dst, const ui
 int lod_dist_adopt(lod_tree* t, const void* d_records, uint64_t n, const uint32_t* h_leaf_counts, void* stream) {
   return dist_adopt(t, d_records, n, h_leaf_counts, (cudaStream_t)stream);
 }
+int lod_merge_pyramid(uint32_t* d_pyr, int L, uint32_t T, void* stream) {
+  if (!d_pyr || L < 0 || L > 10) return fail(LOD_EVALUE, "bad pyramid (levels 0..10)");
+  if (T < 1) return fail(LOD_EVALUE, "T must be >= 1");
+  RUN_NOTREE(launch_merge_standalone(d_pyr, L, T, (cudaStream_t)stream));
+  CK(cudaGetLastError());
+  return LOD_OK;
+}
+
+// the stage exports are readable from the count stage on (lod_dist_count / lod_split)
+static bool counted(const lod_tree* t) { return t && (t->split_done || t->dist_stage >= 2); }
+
+int lod_tree_copy_point_keys(const lod_tree* t, uint32_t* h, void* stream) {
+  if (!counted(t)) return fail(LOD_EVALUE, "no counted tree");
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
+  if (t->n) CK(cudaMemcpyAsync(h, t->pkey.p, t->n * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return LOD_OK;
+}
+
+int lod_tree_copy_pyramids(const lod_tree* t, uint32_t* h, uint64_t* n_out, void* stream) {
+  if (!counted(t) || !n_out) return fail(LOD_EVALUE, "no counted tree");
+  const uint64_t n = level_off(t->cfg.initial_depth + 1) + t->ext_pyr_used;
+  *n_out = n;
+  if (!h) return LOD_OK;
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
+  CK(cudaMemcpyAsync(h, t->pyr.p, n * 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return LOD_OK;
+}
+
+int lod_tree_ext_grids(const lod_tree* t, lod_ext_grid* h, uint32_t* n_out, void* stream) {
+  if (!counted(t) || !n_out) return fail(LOD_EVALUE, "no counted tree");
+  *n_out = t->n_ext;
+  if (!h || !t->n_ext) return LOD_OK;
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
+  std::vector<ExtMeta> m(t->n_ext);
+  CK(cudaMemcpyAsync(m.data(), t->meta.p, t->n_ext * sizeof(ExtMeta), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  for (uint32_t e = 0; e < t->n_ext; ++e)
+    h[e] = lod_ext_grid{m[e].pyr_off, m[e].ax, m[e].ay, m[e].az, m[e].base, m[e].ext};
+  return LOD_OK;
+}
+
+int lod_tree_ext_points(const lod_tree* t, uint32_t* h_index, uint64_t* h_cell16, uint64_t* n_out, void* stream) {
+  if (!counted(t) || !n_out) return fail(LOD_EVALUE, "no counted tree");
+  const uint64_t n = t->elist_cap ? std::min<uint64_t>(t->host_state->ext_n, t->elist_cap) : 0;
+  *n_out = n;
+  if (!h_index || !h_cell16 || !n) return LOD_OK;
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
+  std::vector<uint4> q(n);
+  CK(cudaMemcpyAsync(q.data(), t->elist.p, n * 16, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  for (uint64_t j = 0; j < n; ++j) {
+    h_index[j] = q[j].x;
+    h_cell16[j] = (uint64_t)q[j].z | ((uint64_t)q[j].w << 32);  // x | y << 16, z
+  }
+  return LOD_OK;
+}
+
 int lod_dist_export_roots(lod_tree* t, const int32_t* h_nodes, uint32_t n, void* d_out, uint32_t* h_counts,
                           void* stream) {
   if (!t || t->voxel_mode < 0) return fail(LOD_EVALUE, "no voxels built");

@@ -106,6 +106,7 @@ __device__ __forceinline__ Cell16 unpack_c16(uint64_t p) {
 }
 int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint32_t* round_count,
                      const int* round_ext, const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s);
+int launch_merge_standalone(uint32_t* pyr, int L, uint32_t T, cudaStream_t s);
 int launch_count_nodes(const SplitView& v, uint64_t total_slots, uint64_t* slots_out, ScanScratch& scr,
                        cudaStream_t s);
 int launch_build_nodes(const SplitView& v, const uint64_t* slots, cudaStream_t s);

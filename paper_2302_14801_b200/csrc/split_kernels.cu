@@ -521,6 +521,14 @@ static uint32_t merge_blocks(uint64_t total) {
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + kThreads - 1) / kThreads, 148ull * 16));
 }
 
+// merge_pyramid on a standalone pyramid (the reference's module function, partition.py:36-61):
+// the finest level L at level_off(L) in, levels L-1..0 computed in place
+int launch_merge_standalone(uint32_t* pyr, int L, uint32_t T, cudaStream_t s) {
+  for (int lp = L - 1; lp >= 0; --lp)
+    launch_pdl(k_merge, merge_blocks(1ull << (3 * lp)), kThreads, 0, s, pyr, (uint64_t)0, (uint64_t)0, 1u, lp, T);
+  return L;
+}
+
 int launch_merge_all(const SplitView& v, const uint32_t* round_first, const uint32_t* round_count,
                      const int* round_ext, const uint64_t* round_pyr_base, int n_rounds, cudaStream_t s) {
   int launches = 0;

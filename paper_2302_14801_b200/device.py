@@ -279,6 +279,47 @@ class DeviceTree:
             _abi.check(self.lib.lod_tree_copy_voxels(self.h, raw.ctypes.data_as(C.c_void_p), current_stream_ptr(self.device)))
         return raw
 
+    # -- stage exports (the reference Partitioner's intermediate arrays) ------------------
+
+    def point_keys(self, n: int) -> np.ndarray:
+        """Finest main-grid key (cx * dim + cy) * dim + cz of each input point (count stage)."""
+        out = np.empty(n, np.uint32)
+        _abi.check(self.lib.lod_tree_copy_point_keys(self.h, out.ctypes.data_as(C.c_void_p),
+                                                     current_stream_ptr(self.device)))
+        return out
+
+    def pyramids(self) -> np.ndarray:
+        """Every counting pyramid of the build, u32 per cell (main at 0, extensions after)."""
+        n = C.c_uint64()
+        _abi.check(self.lib.lod_tree_copy_pyramids(self.h, None, C.byref(n), None))
+        out = np.empty(n.value, np.uint32)
+        _abi.check(self.lib.lod_tree_copy_pyramids(self.h, out.ctypes.data_as(C.c_void_p), C.byref(n),
+                                                   current_stream_ptr(self.device)))
+        return out
+
+    def ext_grids(self):
+        """The extension grids in creation order: list of LodExtGrid."""
+        n = C.c_uint32()
+        _abi.check(self.lib.lod_tree_ext_grids(self.h, None, C.byref(n), None))
+        arr = (_abi.LodExtGrid * max(n.value, 1))()
+        if n.value:
+            _abi.check(self.lib.lod_tree_ext_grids(self.h, C.cast(arr, C.c_void_p), C.byref(n),
+                                                   current_stream_ptr(self.device)))
+        return list(arr[:n.value])
+
+    def ext_points(self):
+        """(input index, depth-16 cell (n, 3)) of every point inside an extension grid."""
+        n = C.c_uint64()
+        _abi.check(self.lib.lod_tree_ext_points(self.h, None, None, C.byref(n), None))
+        idx = np.empty(n.value, np.uint32)
+        packed = np.empty(n.value, np.uint64)
+        if n.value:
+            _abi.check(self.lib.lod_tree_ext_points(self.h, idx.ctypes.data_as(C.c_void_p),
+                                                    packed.ctypes.data_as(C.c_void_p), C.byref(n),
+                                                    current_stream_ptr(self.device)))
+        cells = np.stack([packed & 0xFFFF, (packed >> 16) & 0xFFFF, packed >> 32], axis=1).astype(np.int64)
+        return idx.astype(np.int64), cells
+
     def leaf_range(self, first: int, count: int) -> np.ndarray:
         """Raw records [first, first+count) of the leaf buffer (one node's points)."""
         size = 16 if self.info().point_format == LOD_POINTS_F32 else 32

@@ -175,7 +175,7 @@ class RankBuilder:
         self.h = self.dev.h
 
     def _stream(self):
-        return current_stream_ptr()
+        return current_stream_ptr(self.dev.device)
 
     def begin(self, d_records, n_local, fmt, T=50_000, initial_depth=8, extension_depth=4, max_depth=16):
         self.d_in, self.n_local, self.fmt = d_records, n_local, fmt

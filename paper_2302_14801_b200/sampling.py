@@ -82,3 +82,121 @@ def build_lod_points(points, colors, T: int = 50_000, grid: int = GRID_SIZE, mod
     tree = GpuOctree(dev, cfg)
     tree.strategy_built = MODE_ALIASES[mode]
     return tree
+
+
+# ---------------------------------------------------------------------------
+# The reference's per-node helpers (sampling.py:21-162) on the device, for callers driving
+# the stages themselves: lod_project_samples / lod_extract (csrc/extract.cu).
+# ---------------------------------------------------------------------------
+
+def _torch_dev():
+    from .device import _torch
+    return _torch()
+
+
+def _stream():
+    from .device import current_stream_ptr
+    return current_stream_ptr()
+
+
+def project_child_samples(node):
+    """All child samples of an inner node in its 128^3 grid, canonical ordinal order
+    (children in octant order, each child's samples in stored order): (S,3) float64 grid
+    positions and (S,3) uint8 colours (reference sampling.py:21-47)."""
+    import ctypes as C
+    from . import _abi
+    from .errors import ConsistencyError
+    torch = _torch_dev()
+    if node.is_leaf:
+        raise ValueError("cannot project samples for a leaf node")
+    lib = _abi.load()
+    mn = (C.c_double * 3)(*[float(v) for v in node.bounds.min])
+    parts, cols = [], []
+    for octant, child in node.existing_children():
+        if child.sample_count == 0:
+            raise ConsistencyError(f"child {child.path} has no samples")
+        if child.is_leaf:
+            src = torch.from_numpy(np.ascontiguousarray(child.point_positions, np.float64)).cuda()
+            kind, col = 0, child.point_colors
+        else:
+            src = torch.from_numpy(np.ascontiguousarray(child.voxel_coords, np.uint8)).cuda()
+            kind, col = 1, child.voxel_colors
+        n = len(col)
+        out = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        _abi.check(lib.lod_project_samples(kind, C.c_void_p(src.data_ptr()), n, mn, float(node.bounds.size), octant,
+                                           C.c_void_p(out.data_ptr()), _stream()))
+        parts.append(out)
+        cols.append(np.asarray(col, np.uint8))
+    return torch.cat(parts).cpu().numpy(), np.concatenate(cols)
+
+
+def _extract(code, gpos, colors, seed=0, node_hash=0):
+    import ctypes as C
+    from . import _abi
+    torch = _torch_dev()
+    g = np.ascontiguousarray(gpos, np.float64).reshape(-1, 3)
+    c = np.ascontiguousarray(colors, np.uint8).reshape(-1, 3)
+    if len(g) != len(c):
+        raise ValueError("positions/colors length mismatch")
+    S = len(g)
+    dg = torch.from_numpy(g).cuda()
+    dc = torch.from_numpy(c).cuda()
+    oc = torch.empty((max(S, 1), 3), dtype=torch.uint8, device="cuda")
+    ok = torch.empty((max(S, 1), 3), dtype=torch.uint8, device="cuda")
+    m = C.c_uint64(0)
+    _abi.check(_abi.load().lod_extract(code, C.c_void_p(dg.data_ptr()), C.c_void_p(dc.data_ptr()), S,
+                                       int(seed) & ((1 << 64) - 1), int(node_hash) & ((1 << 64) - 1),
+                                       C.c_void_p(oc.data_ptr()), C.c_void_p(ok.data_ptr()), C.byref(m), _stream()))
+    m = int(m.value)
+    return oc[:m].cpu().numpy(), ok[:m].cpu().numpy()
+
+
+def extract_first_come(gpos, colors):
+    """Per cell the smallest ordinal wins; voxels listed by winning ordinal (sampling.py:61-66)."""
+    return _extract(LOD_MODE_FIRST_COME, gpos, colors)
+
+
+def extract_random(gpos, colors, seed: int, node_hash: int):
+    """Per cell the largest (rand12 | ordinal20) wins; ascending cell key (sampling.py:69-85)."""
+    return _extract(LOD_MODE_RANDOM, gpos, colors, seed, node_hash)
+
+
+def extract_average(gpos, colors):
+    """Per cell the rounded mean colour (half away from zero); ascending key (sampling.py:88-97)."""
+    return _extract(LOD_MODE_AVERAGE, gpos, colors)
+
+
+def extract_weighted(gpos, colors):
+    """Distance-weighted 2x2x2 mean, occupied cells only (sampling.py:100-133); colours within
+    +-1 of the reference's sequential fp64 sums (exact 2^-24 fixed point here)."""
+    return _extract(LOD_MODE_WEIGHTED, gpos, colors)
+
+
+def _sample_node(node, strategy: str, seed: int):
+    from . import rng
+    gpos, colors = project_child_samples(node)
+    if strategy == "first-come":
+        return extract_first_come(gpos, colors)
+    if strategy == "random":
+        return extract_random(gpos, colors, seed, rng.path_hash(seed, node.path))
+    if strategy == "average":
+        return extract_average(gpos, colors)
+    if strategy == "weighted":
+        return extract_weighted(gpos, colors)
+    raise ValueError(f"unknown sampling strategy: {strategy}")
+
+
+def sample_first_come(node):
+    return _sample_node(node, "first-come", 0)
+
+
+def sample_random(node, seed: int):
+    return _sample_node(node, "random", seed)
+
+
+def sample_average(node):
+    return _sample_node(node, "average", 0)
+
+
+def sample_weighted(node):
+    return _sample_node(node, "weighted", 0)
