@@ -176,6 +176,8 @@ class Partitioner:
             return self.extended
         pyr = self._dev.pyramids()
         idx, c16 = self._dev.ext_points()
+        o = np.argsort(idx)   # the device lists them in compaction order; the reference's are input order
+        idx, c16 = idx[o], c16[o]
         cfg = self.config
         by_anchor = {}
         sorted_by_base = {}

@@ -135,6 +135,16 @@ def _ep_digest(ep):
     }
 
 
+def _same(got, exp, where):
+    """Recursive equality naming the first differing field."""
+    if isinstance(exp, dict):
+        assert isinstance(got, dict) and set(got) == set(exp), f"{where}: keys {sorted(got)} != {sorted(exp)}"
+        for k in exp:
+            _same(got[k], exp[k], f"{where}.{k}")
+    else:
+        assert got == exp, f"{where}: {got} != {exp}"
+
+
 def _cloud(kind, n, seed):
     from paper_2302_14801_b200 import PointCloud
     from test_stage_golden import cloud_arrays
@@ -161,7 +171,7 @@ def test_stages_equal_reference(case):
     ext = p.extend_overfull_cells()
     levels = p.merge()
     assert [sha(l) for l in levels] == g["levels"]
-    assert {",".join(map(str, k)): _ep_digest(ep) for k, ep in ext.items()} == g["extended"]
+    _same({",".join(map(str, k)): _ep_digest(ep) for k, ep in ext.items()}, g["extended"], "extended")
     assert list(g["extended"]) == [",".join(map(str, k)) for k in ext]     # reference dict order
     tree = p.build_targets()
     assert [[list(nd.path), c] for nd, c in zip(p.leaf_nodes, p.leaf_counts)] == g["leaves"]
