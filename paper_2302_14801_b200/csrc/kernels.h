@@ -53,8 +53,9 @@ struct SplitView {
 
 // Descend the extension chain of a point; returns the finest-cell index inside extension
 // `e_out` (the deepest one containing the point), or false if the point is in none.
+// `tgt_out` (optional) receives that cell's target, `pyr_out` its counting slot.
 __device__ __forceinline__ bool ext_descend(const SplitView& v, const Cell16& c, uint32_t& e_out, uint32_t& r_out,
-                                            int32_t t) {
+                                            int32_t t, int32_t* tgt_out = nullptr, uint64_t* pyr_out = nullptr) {
   if (t > -2) return false;
   uint32_t e = (uint32_t)(-(t + 2));
   while (true) {
@@ -68,6 +69,8 @@ __device__ __forceinline__ bool ext_descend(const SplitView& v, const Cell16& c,
     if (nt > -2) {
       e_out = e;
       r_out = r;
+      if (tgt_out) *tgt_out = nt;
+      if (pyr_out) *pyr_out = m.pyr_off + level_off(m.ext) + r;
       return true;
     }
     e = (uint32_t)(-(nt + 2));
@@ -80,7 +83,8 @@ __device__ __forceinline__ bool ext_descend(const SplitView& v, const Cell16& c,
 __device__ __forceinline__ int32_t leaf_of_point(const SplitView& v, const Cell16& c) {
   int32_t t = v.t8[level_key(c, v.D)];
   uint32_t e, r;
-  if (ext_descend(v, c, e, r, t)) t = v.te[v.meta[e].tgt_off + r];
+  int32_t nt;
+  if (ext_descend(v, c, e, r, t, &nt)) t = nt;
   return t;
 }
 

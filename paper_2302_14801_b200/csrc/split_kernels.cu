@@ -310,9 +310,8 @@ int launch_ext_create(const SplitView& v, int round, uint32_t first_ext, uint32_
 __device__ __forceinline__ void ext_count_point(const SplitView& v, HotCounts<kHotSlots>& hot, const Cell16& c,
                                                 int32_t t, uint32_t round_first) {
   uint32_t e, rr;
-  if (ext_descend(v, c, e, rr, t) && e >= round_first) {
-    const ExtMeta& m = v.meta[e];
-    const uint64_t slot = m.pyr_off + level_off(m.ext) + rr;
+  uint64_t slot;
+  if (ext_descend(v, c, e, rr, t, nullptr, &slot) && e >= round_first) {
     if (slot < 0xFFFFFFFFull) hot.add(v.pyr, (uint32_t)slot, 1u);
     else atomicAdd(v.pyr + slot, 1u);
   }
@@ -429,13 +428,20 @@ __global__ void __launch_bounds__(kThreads) k_ext_leaf(SplitView v, uint32_t* le
   pdl_wait();
   const uint64_t n = min((uint64_t)v.st->ext_n, v.elist_cap);
   bool unresolved = false;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint4 q = __ldcs(v.elist + j);
-    int32_t t = -(int32_t)q.y - 2;
-    uint32_t e, rr;
-    if (ext_descend(v, Cell16{q.z & 0xFFFF, q.z >> 16, q.w}, e, rr, t)) t = v.te[v.meta[e].tgt_off + rr];
-    if (t < 0) unresolved = true, t = 0;
-    leaf_out[q.x] = (uint32_t)t;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int U = 4;  // independent descents in flight per thread (each is a chain of loads)
+  for (uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < n; j0 += U * stride) {
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = __ldcs(v.elist + min(j0 + u * stride, n - 1));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int32_t t = -(int32_t)q[u].y - 2, nt;
+      uint32_t e, rr;
+      if (ext_descend(v, Cell16{q[u].z & 0xFFFF, q[u].z >> 16, q[u].w}, e, rr, t, &nt)) t = nt;
+      if (t < 0) unresolved = true, t = 0;
+      if (j0 + u * stride < n) leaf_out[q[u].x] = (uint32_t)t;
+    }
   }
   if (__any_sync(0xFFFFFFFFu, unresolved) && (threadIdx.x & 31) == 0) raise_err(v.st, ERR_UNRESOLVED);
 }
