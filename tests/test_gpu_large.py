@@ -115,6 +115,40 @@ def _oracle_node(dev, nodes, k, strat, seed):
     return O.extract_first_come(cells, cols)
 
 
+def _structure_properties(nodes, n, T, max_depth):
+    """Acceptance criteria 01/02 (test_acceptance.py:71-95) on the full node table:
+    conservation, capacity (oversized only at max depth), merging maximality, and every inner
+    node linked to its existing children."""
+    leaf = (nodes["flags"] & 1) == 1
+    over = (nodes["flags"] & 2) == 2
+    cnt = nodes["count"].astype(np.int64)
+    assert int(cnt[leaf].sum()) == n, "conservation"
+    assert (cnt[leaf & ~over] <= T).all(), "capacity"
+    assert (nodes["depth"][over] == max_depth).all(), "oversized leaf away from max depth"
+    ch = nodes["child"]
+    inner = np.flatnonzero(~leaf)
+    kids = ch[inner]
+    assert ((kids >= 0).any(axis=1)).all(), "inner node without children"
+    all_leaf = np.array([all(leaf[c] for c in row if c >= 0) for row in kids])
+    sums = np.array([int(cnt[[c for c in row if c >= 0]].sum()) for row in kids])
+    assert (sums[all_leaf] >= T).all(), "merging maximality"
+
+
+def _occupancy_sums(dev, nodes):
+    """Per inner node: (voxel count, sum of keys, sum of squared keys mod 2^64) -- order-
+    independent, so first-come's ordinal order compares with the others' key order
+    (criterion 05, test_acceptance.py:154-166)."""
+    inner = np.flatnonzero((nodes["flags"] & 1) == 0)
+    keys = dev.voxels()[:, 0].astype(np.uint64)
+    with np.errstate(over="ignore"):
+        c1 = np.concatenate([np.zeros(1, np.uint64), np.cumsum(keys, dtype=np.uint64)])
+        c2 = np.concatenate([np.zeros(1, np.uint64), np.cumsum(keys * keys, dtype=np.uint64)])
+        f = nodes["first"][inner].astype(np.int64)
+        e = f + nodes["count"][inner].astype(np.int64)
+        s1, s2 = c1[e] - c1[f], c2[e] - c2[f]
+    return {int(i): (int(e[j] - f[j]), int(s1[j]), int(s2[j])) for j, i in enumerate(inner)}
+
+
 @pytest.mark.parametrize("name", FULL)
 def test_full_cloud(name):
     import torch
@@ -143,6 +177,7 @@ def test_full_cloud(name):
         gc.collect()
         torch.cuda.empty_cache()
         nodes = dev.nodes()
+        _structure_properties(nodes, n, full["T"], 16)
 
         # skeleton at depths <= 4 (node set, kind, points in the node's cube, fp64 bounds)
         dmax = full["skeleton_depth"]
@@ -168,6 +203,7 @@ def test_full_cloud(name):
 
         # sampling: subtrees vs goldens, shallow inner nodes by induction from their children
         offender = None
+        occupancy = None
         for mode in MODES:
             strat, code, seed = _mode(mode)
             errs = [g for g in subs if "error" in g["modes"][mode]]
@@ -186,6 +222,10 @@ def test_full_cloud(name):
                     continue
             dev.voxelize(code, seed)
             nodes = dev.nodes()
+            occ = _occupancy_sums(dev, nodes)   # criterion 05: occupancy is strategy-independent
+            if occupancy is not None:
+                assert occ == occupancy, f"{name} {mode}: occupancy differs from the other strategies"
+            occupancy = occ
             if strat == "average":
                 offender = _expected_offender(nodes)
             for g in subs:
