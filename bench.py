@@ -511,7 +511,16 @@ def main():
     if world > 1:
         from paper_2302_14801_b200.dist import NcclComm, RankBuilder, TorchComm, build_distributed
         # NCCL: the library's own communicator on the build stream; gloo: host-staged (tests)
-        comm = NcclComm.from_torch_distributed(local) if args.backend == "nccl" else TorchComm()
+        comm = None
+        if args.backend == "nccl":
+            try:
+                comm = NcclComm.from_torch_distributed(local)
+            except Exception as e:  # e.g. libnccl.so.2 not loadable by the library
+                print(f"library NCCL communicator unavailable ({e}); using torch.distributed's NCCL "
+                      "collectives", file=sys.stderr, flush=True)
+        comm_kind = "library NCCL" if comm is not None else args.backend
+        if comm is None:
+            comm = TorchComm()
         rb = RankBuilder(rank, world, dev=dev)
 
     def step(src=None):
@@ -666,7 +675,7 @@ def main():
             "dtype": "f64-geometry/u32-counts", "data": "synthetic",
             "config": {"workload": args.config, "points": n_total, "points_per_gpu": n, "mode": args.mode,
                        "T": 50_000, "grid": 128, "l2": "input 16 B/pt x points > 126 MB L2, no flush",
-                       "parallelism": f"subtree-sharded x{world} ({'library NCCL' if args.backend == 'nccl' else 'gloo'} "
+                       "parallelism": f"subtree-sharded x{world} ({comm_kind} "
                                       f"all-reduce + all-to-all + rank-0 gather)"
                        if world > 1 else "single"},
             "e2e": e2e, "e2e_api": api, "gpu_launches": launches_per_step * args.steps,
