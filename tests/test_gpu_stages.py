@@ -206,3 +206,11 @@ def test_stages_order_and_run_completion():
     a = sorted((lf.path, lf.point_count) for lf in tree.leaves())
     b = sorted((lf.path, lf.point_count) for lf in ref.leaves())
     assert a == b
+    # a tree built stage by stage samples like the fused build
+    from paper_2302_14801_b200 import build_lod
+    for strategy, seed in (("average", 0), ("random", 5)):
+        build_lod(tree, strategy, seed)
+        build_lod(ref, strategy, seed)
+        va = {n.path: (n.voxel_coords.tobytes(), n.voxel_colors.tobytes()) for n in tree.inner_nodes()}
+        vb = {n.path: (n.voxel_coords.tobytes(), n.voxel_colors.tobytes()) for n in ref.inner_nodes()}
+        assert va == vb, strategy
