@@ -54,9 +54,12 @@ def subtree_points(depth, parent, leaf_node, leaf_counts):
     """Points under every node (bottom-up sums of the leaf counts)."""
     pts = np.zeros(len(depth), np.int64)
     pts[leaf_node] = leaf_counts
+    by_depth = np.argsort(depth, kind="stable")
+    bounds = np.searchsorted(depth[by_depth], np.arange(int(depth.max()) + 2))
     for d in range(int(depth.max()), 0, -1):
-        sel = np.flatnonzero(depth == d)
-        np.add.at(pts, parent[sel], pts[sel])
+        sel = by_depth[bounds[d]:bounds[d + 1]]
+        # float64 bincount is exact here (point counts < 2^53)
+        pts += np.bincount(parent[sel], weights=pts[sel], minlength=len(pts)).astype(np.int64)
     return pts
 
 
@@ -102,52 +105,50 @@ def plan_subtrees(depth, parent, is_leaf, leaf_node, leaf_counts, world: int, mi
     return SubtreePlan(cut, node_owner, leaf_owner, roots, root_owner, load)
 
 
-def exchange_layout(leaf_owner, all_counts, world):
+def exchange_layout(leaf_owner, all_counts, world, rank=None):
     """Send/receive layouts of the point exchange.
 
-    all_counts: (R, L) points of rank r in leaf l.  Returns per rank r:
-      send segments (src offset in r's local leaf buffer, dst offset in r's send buffer,
-      count), send_splits[q]; and for the receiving rank q: recv segments (src offset in
-      q's receive buffer, dst offset in q's final leaf buffer, count), recv_splits[r],
-      q's per-leaf counts.
+    all_counts: (R, L) points of rank r in leaf l.  For rank r: send segments (src offset in
+    r's local leaf buffer, dst offset in r's send buffer, count) and send_splits[q]; recv
+    segments (src offset in r's receive buffer, dst offset in r's final leaf buffer, count),
+    recv_splits[q] and r's per-leaf counts.  `rank` given: that rank's layout only (what a
+    rank needs: O(R L) vectorised); else the list for every rank.
     """
     all_counts = np.asarray(all_counts, np.int64)
-    R, L = all_counts.shape
     leaf_owner = np.asarray(leaf_owner)
-    local_first = np.zeros((R, L), np.int64)
-    local_first[:, 1:] = np.cumsum(all_counts[:, :-1], axis=1)
-    order = np.lexsort((np.arange(L), leaf_owner))   # leaves grouped by owner, leaf order within
-    out = []
-    for r in range(R):
-        c = all_counts[r, order]
-        dst = np.zeros(L, np.int64)
-        dst[1:] = np.cumsum(c[:-1])
-        nz = c > 0
-        send = (local_first[r, order][nz], dst[nz], c[nz])
-        splits = np.array([int(all_counts[r, leaf_owner == q].sum()) for q in range(world)], np.int64)
-        out.append({"send": send, "send_splits": splits})
-    for q in range(R):
-        mine = np.flatnonzero(leaf_owner == q)
-        tot = all_counts[:, mine].sum(axis=0)                  # global count per owned leaf
-        final_first = np.zeros(len(mine), np.int64)
-        final_first[1:] = np.cumsum(tot[:-1])
-        recv_splits = all_counts[:, mine].sum(axis=1)
-        recv_base = np.zeros(R, np.int64)
-        recv_base[1:] = np.cumsum(recv_splits[:-1])
-        src, dst, cnt = [], [], []
-        for r in range(R):
-            c = all_counts[r, mine]
-            within = np.zeros(len(mine), np.int64)
-            within[1:] = np.cumsum(c[:-1])
-            before = all_counts[:r, mine].sum(axis=0)
-            nz = c > 0
-            src.append(recv_base[r] + within[nz])
-            dst.append(final_first[nz] + before[nz])
-            cnt.append(c[nz])
-        counts = np.zeros(L, np.uint32)
-        counts[mine] = tot
-        out[q].update({"recv": (np.concatenate(src), np.concatenate(dst), np.concatenate(cnt)),
-                       "recv_splits": recv_splits, "counts": counts})
+    if rank is None:
+        return [exchange_layout(leaf_owner, all_counts, world, r) for r in range(all_counts.shape[0])]
+    R, L = all_counts.shape
+    r = rank
+    # send: r's leaves grouped by owner (leaf order within an owner), from r's leaf-major buffer
+    order = np.argsort(leaf_owner, kind="stable")
+    mine_r = all_counts[r]
+    local_first = np.zeros(L, np.int64)
+    local_first[1:] = np.cumsum(mine_r[:-1])
+    c = mine_r[order]
+    dst = np.zeros(L, np.int64)
+    dst[1:] = np.cumsum(c[:-1])
+    nz = c > 0
+    out = {"send": (local_first[order][nz], dst[nz], c[nz]),
+           "send_splits": np.bincount(leaf_owner, weights=mine_r, minlength=world).astype(np.int64)[:world]}
+    # receive: the leaves r owns, every source rank's run in source-rank order (input order, H3)
+    mine = np.flatnonzero(leaf_owner == r)
+    A = all_counts[:, mine]                                   # (R, M)
+    tot = A.sum(axis=0)
+    final_first = np.zeros(len(mine), np.int64)
+    final_first[1:] = np.cumsum(tot[:-1])
+    recv_splits = A.sum(axis=1)
+    recv_base = np.zeros(R, np.int64)
+    recv_base[1:] = np.cumsum(recv_splits[:-1])
+    within = np.cumsum(A, axis=1) - A                         # offset inside the source's run
+    before = np.cumsum(A, axis=0) - A                         # points of lower source ranks
+    nzA = A > 0
+    src = (recv_base[:, None] + within)[nzA]
+    dstv = (final_first[None, :] + before)[nzA]
+    cnt = A[nzA]
+    counts = np.zeros(L, np.uint32)
+    counts[mine] = tot
+    out.update({"recv": (src, dstv, cnt), "recv_splits": recv_splits, "counts": counts})
     return out
 
 
@@ -550,7 +551,7 @@ def build_distributed(comm: TorchComm, d_records, n_local, fmt, mode, seed=0, T=
     all_counts = comm.all_gather_np(local_counts.astype(np.int64))
     depth, parent, is_leaf, leaf_node = rb.node_arrays()
     plan = plan_subtrees(depth, parent, is_leaf, leaf_node, all_counts.sum(axis=0), comm.world)
-    lay = exchange_layout(plan.leaf_owner, all_counts, comm.world)[comm.rank]
+    lay = exchange_layout(plan.leaf_owner, all_counts, comm.world, comm.rank)
     send = rb.pack(lay)
     recv = comm.all_to_all_bytes(send, lay["send_splits"] * rb.rec_bytes, lay["recv_splits"] * rb.rec_bytes)
     rb.unpack_adopt(recv, lay)
