@@ -1,7 +1,7 @@
 # A/B of voxelize variants (env knobs) on bench configs -> gpurun_out/ab.txt
 mkdir -p gpurun_out
 for c in ${CONFIGS:-cluster2B terrain20M scene500M}; do
- for v in ${VARIANTS:-"X=0" "LODB200_NO_LOCAL_VOX=1"}; do
+ for v in ${VARIANTS:-"X=0" "LODB200_NO_K3ZERO=1"}; do
   env $v timeout 600 python bench.py --config $c --steps 5 --warmup 3 --stages --no-cpu-baseline --no-e2e > gpurun_out/ab.json 2> gpurun_out/ab.err
   LABEL="$c $v" python - <<'PY'
 import json, os
