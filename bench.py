@@ -336,7 +336,9 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     """Clouds that fit once (cluster2B: ~100 GB working set): one tree, split and voxelize as
     separate ABI calls so the copies overlap the work that no longer needs their buffers --
     the next upload starts when the split has consumed the input, the leaf download runs under
-    the voxelize, the voxel/node download under the next upload."""
+    the voxelize and under the NEXT split's bounds / count / extension rounds (the split waits
+    for the previous downloads only before it rewrites the node table and leaf buffer:
+    lod_tree_set_output_wait), the voxel download under the next split."""
     from paper_2302_14801_b200 import _abi
     info = dev.info()
     rec_bytes = n * 16
@@ -347,20 +349,21 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     h_vox = torch.empty(max(info.n_voxels * 8, 8), dtype=torch.uint8, pin_memory=True)
     h_nodes = torch.empty(max(info.n_nodes * _abi.node_dtype().itemsize, 88), dtype=torch.uint8, pin_memory=True)
     d_stage = d_in            # the device input buffer is the staging buffer
-    up, dl = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_up, ev_split, ev_vox, ev_dl = (torch.cuda.Event() for _ in range(4))
+    up, dl, dl2, jn = (torch.cuda.Stream() for _ in range(4))
+    ev_up, ev_split, ev_vox, ev_leaf, ev_voxdl, ev_out = (torch.cuda.Event() for _ in range(6))
     sp = C.c_void_p(stream.cuda_stream)
-    dlp = C.c_void_p(dl.cuda_stream)
+    dlp, dl2p = C.c_void_p(dl.cuda_stream), C.c_void_p(dl2.cuda_stream)
 
     def run(k_steps):
         up.wait_stream(stream)
         with torch.cuda.stream(up):
             d_stage.copy_(h_in, non_blocking=True)
             ev_up.record(up)
-        ev_dl.record(dl)
+        ev_voxdl.record(dl2)
         for k in range(k_steps):
             stream.wait_event(ev_up)
-            stream.wait_event(ev_dl)        # the previous tree's downloads are done
+            if k > 0:   # the previous tree's node + leaf downloads, before the skeleton
+                _abi.check(lib.lod_tree_set_output_wait(dev.h, C.c_void_p(ev_out.cuda_event)))
             dev.split(d_stage, n, _abi.LOD_POINTS_F32, cfg, stream=sp)
             ev_split.record(stream)
             if k + 1 < k_steps:             # the split consumed the input: upload the next one
@@ -370,14 +373,19 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
                     ev_up.record(up)
             dl.wait_event(ev_split)         # leaf points are final after the distribute
             _abi.check(lib.lod_tree_copy_async(dev.h, C.c_void_p(h_leaf.data_ptr()), None, None, dlp))
+            ev_leaf.record(dl)
+            stream.wait_event(ev_voxdl)     # the previous voxels are downloaded: the arena is free
             dev.voxelize(mode_code, seed, stream=sp)
             ev_vox.record(stream)
-            dl.wait_event(ev_vox)
+            dl2.wait_event(ev_vox)
             _abi.check(lib.lod_tree_copy_async(dev.h, None, C.c_void_p(h_vox.data_ptr()),
-                                               C.c_void_p(h_nodes.data_ptr()), dlp))
-            ev_dl.record(dl)
-        stream.wait_stream(dl)
-        stream.wait_stream(up)
+                                               C.c_void_p(h_nodes.data_ptr()), dl2p))
+            ev_voxdl.record(dl2)
+            jn.wait_event(ev_leaf)
+            jn.wait_event(ev_voxdl)
+            ev_out.record(jn)
+        for st in (dl, dl2, up, jn):
+            stream.wait_stream(st)
 
     run(1)
     torch.cuda.synchronize()
@@ -387,7 +395,8 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     return (e0.elapsed_time(e1) / steps,
-            "1 tree, 3 streams: split k -> (voxelize k || leaf download k || upload k+1) -> voxel+node download k",
+            "1 tree, 5 streams: split k+1's bounds/count/extension || leaf download k; "
+            "voxelize k || upload k+1; voxel+node download k || split k+1",
             rec_bytes, _tree_bytes(dev, n))
 
 

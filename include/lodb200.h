@@ -138,6 +138,13 @@ int lod_tree_voxels(const lod_tree* tree, const void** d_ptr);
  * overlap the copies of build k with the upload / build of build k+1 (PCIe is duplex). */
 int lod_tree_copy_async(const lod_tree* tree, void* h_leaf_points, void* h_voxels, lod_node* h_nodes,
                         void* stream);
+/* The NEXT lod_split (or lod_dist_skeleton) on this tree makes its stream wait on `event` (a
+ * cudaEvent_t) right before it rewrites the node table and the leaf buffer -- i.e. after its
+ * bounds, count and extension rounds -- so a caller still downloading the previous build's
+ * outputs (lod_tree_copy_async on another stream) overlaps that download with the next
+ * build's first stages.  Voxels are rewritten by lod_voxelize, which the caller orders itself.
+ * NULL clears it. */
+int lod_tree_set_output_wait(lod_tree* tree, void* event);
 
 /* Host copies of the outputs (sizes from lod_tree_get_info). */
 int lod_tree_copy_leaf_points(const lod_tree* tree, void* host, void* stream);

@@ -129,6 +129,7 @@ struct lod_tree {
   DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
   DevBuf leaf_pts, status, digit_base, tmp_rec, tmp_leaf, pkey, elist, abits;
   uint64_t elist_cap = 0;
+  cudaEvent_t out_wait = nullptr;  // lod_tree_set_output_wait (next split only)
   bool use_abits = false;
   DevBuf vox, export_buf, stash;
   DevBuf vbits, vpre, vinfo, vblk, vcount, vlevel_start, node_slot, vacc, vchunks, vvchunks;
@@ -651,6 +652,15 @@ int phase_distribute(lod_tree* t, cudaStream_t s, bool sync = true) {
   return LOD_OK;
 }
 
+// lod_tree_set_output_wait: the node table and the leaf buffer are rewritten from the skeleton on
+int wait_outputs(lod_tree* t, cudaStream_t s) {
+  if (t->out_wait) {
+    CK(cudaStreamWaitEvent(s, t->out_wait, 0));
+    t->out_wait = nullptr;  // one split only
+  }
+  return LOD_OK;
+}
+
 int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub, const lod_config* cfg,
              cudaStream_t s, bool final_sync = true) {
   if (t) t->dist = false;
@@ -663,7 +673,7 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   while (cur > 0) {
     if ((r = phase_round(t, s)) || (r = phase_subanchors(t, &cur, s))) return r;
   }
-  if ((r = phase_skeleton(t, s)) || (r = phase_distribute(t, s, final_sync))) return r;
+  if ((r = wait_outputs(t, s)) || (r = phase_skeleton(t, s)) || (r = phase_distribute(t, s, final_sync))) return r;
   t->split_done = true;
   return LOD_OK;
 }
@@ -990,8 +1000,8 @@ int dist_extend(lod_tree* t, lod_span* out, cudaStream_t s) {
 
 int dist_skeleton(lod_tree* t, uint32_t* h_counts, cudaStream_t s) {
   if (!t || t->dist_stage != 4) return fail(LOD_EVALUE, "lod_dist_skeleton out of order");
-  int r = phase_skeleton(t, s);
-  if (r) return r;
+  int r = wait_outputs(t, s);
+  if (r || (r = phase_skeleton(t, s))) return r;
   std::vector<uint32_t> rf, rc;
   std::vector<int> re;
   std::vector<uint64_t> rb;
@@ -1146,6 +1156,12 @@ int lod_tree_copy_nodes(const lod_tree* tc, lod_node* host, void* stream) {
   launch_export_nodes(v, t->export_buf.as<lod_node>(), s);
   CK(cudaMemcpyAsync(host, t->export_buf.p, (size_t)t->n_nodes * sizeof(lod_node), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return LOD_OK;
+}
+
+int lod_tree_set_output_wait(lod_tree* t, void* event) {
+  if (!t) return fail(LOD_EVALUE, "null tree");
+  t->out_wait = (cudaEvent_t)event;
   return LOD_OK;
 }
 

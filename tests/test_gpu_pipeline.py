@@ -112,3 +112,79 @@ def test_pipelined_builds_match_solo_builds(mode):
         n_nodes, n_vox, canon0 = solo[k % 3]
         assert (info.n_nodes, info.n_voxels) == (n_nodes, n_vox), k
         assert _canonical(info.n_nodes, leaf.numpy(), vox.numpy(), nodes.numpy()) == canon0, k
+
+
+def test_one_tree_pipeline_with_output_wait():
+    """The bench's one-tree e2e pattern: split k+1 runs its first stages while the leaf / node /
+    voxel downloads of build k are still in flight (lod_tree_set_output_wait holds back only its
+    skeleton and distribute; the caller orders voxelize k+1 after the voxel download).  Every
+    download must equal the same cloud built alone."""
+    import torch
+    from paper_2302_14801_b200 import _abi
+    from paper_2302_14801_b200.device import DeviceTree, make_config
+
+    code = 2  # average
+    cfg = make_config(2_000)
+    clouds = [_records(400_000 + 30_000 * k, seed=10 + k) for k in range(3)]
+    lib = _abi.load()
+    solo = []
+    ref_tree = DeviceTree(0)
+    cur = torch.cuda.current_stream()
+    for rec in clouds:
+        d = torch.from_numpy(rec).cuda()
+        ref_tree.build(d, len(rec) // 16, _abi.LOD_POINTS_F32, cfg, code, 0, stream=C.c_void_p(cur.cuda_stream))
+        info, leaf, vox, nodes = _download(torch, ref_tree, lib, cur)
+        torch.cuda.synchronize()
+        solo.append((info.n_nodes, info.n_voxels,
+                     _canonical(info.n_nodes, leaf.numpy().copy(), vox.numpy().copy(), nodes.numpy().copy())))
+
+    tree = DeviceTree(0)
+    s, up, dl, dl2, jn = (torch.cuda.Stream() for _ in range(5))
+    sp = C.c_void_p(s.cuda_stream)
+    ev_split, ev_vox, ev_leaf, ev_voxdl, ev_out, ev_up = (torch.cuda.Event() for _ in range(6))
+    h_in = [torch.from_numpy(c).pin_memory() for c in clouds]
+    size = max(len(c) for c in clouds)
+    d_stage = torch.empty(size, dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(up):
+        d_stage[: len(clouds[0])].copy_(h_in[0], non_blocking=True)
+        ev_up.record(up)
+    ev_voxdl.record(dl2)
+    outs = []
+    steps = 6
+    for k in range(steps):
+        n = len(clouds[k % 3]) // 16
+        s.wait_event(ev_up)
+        if k > 0:
+            _abi.check(lib.lod_tree_set_output_wait(tree.h, C.c_void_p(ev_out.cuda_event)))
+        tree.split(d_stage, n, _abi.LOD_POINTS_F32, cfg, stream=sp)
+        ev_split.record(s)
+        if k + 1 < steps:
+            nxt = (k + 1) % 3
+            up.wait_event(ev_split)
+            with torch.cuda.stream(up):
+                d_stage[: len(clouds[nxt])].copy_(h_in[nxt], non_blocking=True)
+                ev_up.record(up)
+        info = tree.info()
+        leaf = torch.empty(info.n_points * 16, dtype=torch.uint8, pin_memory=True)
+        dl.wait_event(ev_split)
+        _abi.check(lib.lod_tree_copy_async(tree.h, C.c_void_p(leaf.data_ptr()), None, None, C.c_void_p(dl.cuda_stream)))
+        ev_leaf.record(dl)
+        s.wait_event(ev_voxdl)
+        tree.voxelize(code, 0, stream=sp)
+        ev_vox.record(s)
+        info = tree.info()
+        vox = torch.empty(max(info.n_voxels * 8, 8), dtype=torch.uint8, pin_memory=True)
+        nodes = torch.empty(max(info.n_nodes * _abi.node_dtype().itemsize, 8), dtype=torch.uint8, pin_memory=True)
+        dl2.wait_event(ev_vox)
+        _abi.check(lib.lod_tree_copy_async(tree.h, None, C.c_void_p(vox.data_ptr()), C.c_void_p(nodes.data_ptr()),
+                                           C.c_void_p(dl2.cuda_stream)))
+        ev_voxdl.record(dl2)
+        jn.wait_event(ev_leaf)
+        jn.wait_event(ev_voxdl)
+        ev_out.record(jn)
+        outs.append((info, leaf, vox, nodes))
+    torch.cuda.synchronize()
+    for k, (info, leaf, vox, nodes) in enumerate(outs):
+        n_nodes, n_vox, canon0 = solo[k % 3]
+        assert (info.n_nodes, info.n_voxels) == (n_nodes, n_vox), k
+        assert _canonical(info.n_nodes, leaf.numpy(), vox.numpy(), nodes.numpy()) == canon0, k
