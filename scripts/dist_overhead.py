@@ -33,11 +33,11 @@ def main():
     dev = DeviceTree()
     cfg = make_config(50_000)
     for _ in range(2):
-        dev.build(buf, n, _abi.LOD_POINTS_F32, cfg, 2, 0)
+        dev.build(buf, n, _abi.LOD_POINTS_F32, cfg, _abi.LOD_MODE_AVERAGE, 0)
     torch.cuda.synchronize()
     t = time.perf_counter()
     for _ in range(a.reps):
-        dev.build(buf, n, _abi.LOD_POINTS_F32, cfg, 2, 0)
+        dev.build(buf, n, _abi.LOD_POINTS_F32, cfg, _abi.LOD_MODE_AVERAGE, 0)
     torch.cuda.synchronize()
     fused = (time.perf_counter() - t) / a.reps
     dev.close()

@@ -123,7 +123,7 @@ def test_one_tree_pipeline_with_output_wait():
     from paper_2302_14801_b200 import _abi
     from paper_2302_14801_b200.device import DeviceTree, make_config
 
-    code = 2  # average
+    code = _abi.LOD_MODE_AVERAGE
     cfg = make_config(2_000)
     clouds = [_records(400_000 + 30_000 * k, seed=10 + k) for k in range(3)]
     lib = _abi.load()
