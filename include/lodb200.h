@@ -312,7 +312,12 @@ int lod_dist_leaf_counts(const lod_tree* tree, uint32_t* h_counts);
 /* copy record segments (in records) from d_src to d_dst; NULL = the tree's leaf buffer */
 int lod_dist_copy_segments(lod_tree* tree, const void* d_src, void* d_dst, const uint64_t* h_src,
                            const uint64_t* h_dst, const uint32_t* h_cnt, uint64_t nseg, void* stream);
-/* make d_records (leaf-major, per-leaf counts h_leaf_counts) this rank's leaf buffer */
+/* the tree's leaf buffer grown to n records (contents undefined): receive the exchanged
+ * records straight into it, then lod_dist_adopt(tree, that pointer, ...) adopts them in place
+ * (call after the send buffer was packed from the old leaf buffer) */
+int lod_dist_leaf_buffer(lod_tree* tree, uint64_t n, void** d_out);
+/* make d_records (leaf-major, per-leaf counts h_leaf_counts) this rank's leaf buffer (copied,
+ * or adopted in place when d_records is the pointer lod_dist_leaf_buffer returned) */
 int lod_dist_adopt(lod_tree* tree, const void* d_records, uint64_t n, const uint32_t* h_leaf_counts,
                    void* stream);
 /* voxelize the inner nodes with h_mask[node] = 1; append = keep earlier results; the

@@ -90,6 +90,7 @@ SIGNATURES = [
     ("lod_tree_launches", C.c_uint64, [_P]),
     ("lod_pack_points", C.c_int, [_P, C.c_int, _P, C.c_uint64, C.c_int, _P, C.POINTER(C.c_int), _P]),
     ("lod_tree_set_output_wait", C.c_int, [_P, _P]),
+    ("lod_dist_leaf_buffer", C.c_int, [_P, C.c_uint64, C.POINTER(C.c_void_p)]),
     ("lod_merge_pyramid", C.c_int, [_P, C.c_int, C.c_uint32, _P]),
     ("lod_tree_copy_point_keys", C.c_int, [_P, _P, _P]),
     ("lod_tree_copy_pyramids", C.c_int, [_P, _P, C.POINTER(C.c_uint64), _P]),

@@ -1038,8 +1038,12 @@ int dist_copy_segments(lod_tree* t, const void* src, void* dst, const uint64_t* 
 int dist_adopt(lod_tree* t, const void* recs, uint64_t n, const uint32_t* h_counts, cudaStream_t s) {
   if (!t || t->dist_stage != 5) return fail(LOD_EVALUE, "lod_dist_adopt out of order");
   const size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
-  CK(ensure(t->leaf_pts, std::max<uint64_t>(n, 1) * rec));
-  if (n) CK(cudaMemcpyAsync(t->leaf_pts.p, recs, n * rec, cudaMemcpyDeviceToDevice, s));
+  if (recs != t->leaf_pts.p) {  // else: already received in place (lod_dist_leaf_buffer)
+    CK(ensure(t->leaf_pts, std::max<uint64_t>(n, 1) * rec));
+    if (n) CK(cudaMemcpyAsync(t->leaf_pts.p, recs, n * rec, cudaMemcpyDeviceToDevice, s));
+  } else if (t->leaf_pts.cap < n * rec) {
+    return fail(LOD_EVALUE, "leaf buffer smaller than the adopted records");
+  }
   CK(cudaMemcpyAsync(t->leaf_count.p, h_counts, 4ull * t->n_leaves, cudaMemcpyHostToDevice, s));
   ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
   SplitView v = make_view(t, t->pts);
@@ -1446,6 +1450,14 @@ int lod_dist_leaf_counts(const lod_tree* tc, uint32_t* h) {
 int lod_dist_copy_segments(lod_tree* t, const void* d_src, void* d_dst, const uint64_t* h_src, const uint64_t* h_dst,
                            const uint32_t* h_cnt, uint64_t nseg, void* stream) {
   return dist_copy_segments(t, d_src, d_dst, h_src, h_dst, h_cnt, nseg, (cudaStream_t)stream);
+}
+int lod_dist_leaf_buffer(lod_tree* t, uint64_t n, void** d_out) {
+  if (!t || t->dist_stage != 5 || !d_out) return fail(LOD_EVALUE, "lod_dist_leaf_buffer out of order");
+  DeviceGuard dg_(t->device);
+  CK(dg_.status);
+  CK(ensure(t->leaf_pts, std::max<uint64_t>(n, 1) * (t->fmt == LOD_POINTS_F32 ? 16 : 32)));
+  *d_out = t->leaf_pts.p;
+  return LOD_OK;
 }
 int lod_dist_adopt(lod_tree* t, const void* d_records, uint64_t n, const uint32_t* h_leaf_counts, void* stream) {
   return dist_adopt(t, d_records, n, h_leaf_counts, (cudaStream_t)stream);

@@ -227,14 +227,17 @@ class RankBuilder:
         return send
 
     def unpack_adopt(self, recv, layout):
-        import torch
+        """Received segments straight into the tree's leaf buffer (grown first; the send buffer
+        was already packed from it), adopted in place: no extra device copy."""
         n_mine = int(layout["counts"].sum())
-        final = torch.empty(max(n_mine, 1) * self.rec_bytes, dtype=torch.uint8, device="cuda")
-        self.copy_segments(recv, final, layout["recv"])
+        ptr = C.c_void_p()
+        _abi.check(self.lib.lod_dist_leaf_buffer(self.h, n_mine, C.byref(ptr)))
+        s, d, c = (_u64(layout["recv"][0]), _u64(layout["recv"][1]), np.ascontiguousarray(layout["recv"][2], np.uint32))
+        _abi.check(self.lib.lod_dist_copy_segments(
+            self.h, C.c_void_p(recv.data_ptr()), ptr, s.ctypes.data_as(C.c_void_p), d.ctypes.data_as(C.c_void_p),
+            c.ctypes.data_as(C.c_void_p), len(c), self._stream()))
         counts = np.ascontiguousarray(layout["counts"], np.uint32)
-        _abi.check(self.lib.lod_dist_adopt(self.h, C.c_void_p(final.data_ptr()), n_mine,
-                                           counts.ctypes.data_as(C.c_void_p), self._stream()))
-        self._final = final
+        _abi.check(self.lib.lod_dist_adopt(self.h, ptr, n_mine, counts.ctypes.data_as(C.c_void_p), self._stream()))
 
     def voxelize(self, mode, seed, mask, append=False, imports=None, imp_slot_base=0):
         mask = np.ascontiguousarray(mask, np.uint8)
