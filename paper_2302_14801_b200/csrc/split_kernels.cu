@@ -150,8 +150,14 @@ int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const doub
 // K2: count into the main finest grid, warp-aggregated atomics
 // ---------------------------------------------------------------------------
 constexpr int kCountUnroll = 4;
-constexpr int kHotSlots = 1024;     // per-CTA hot-counter cache (common.cuh HotCounts)
-constexpr int kHotReset = 64;       // loop trips between flushes (64 x 1024 points per CTA)
+#ifndef LOD_HOT_SLOTS
+#define LOD_HOT_SLOTS 1024
+#endif
+#ifndef LOD_HOT_RESET
+#define LOD_HOT_RESET 64
+#endif
+constexpr int kHotSlots = LOD_HOT_SLOTS;  // per-CTA hot-counter cache (common.cuh HotCounts)
+constexpr int kHotReset = LOD_HOT_RESET;  // loop trips between flushes (64 x 1024 points per CTA)
 
 template <int FMT>
 __global__ void __launch_bounds__(kThreads, 4) k_count(SplitView v) {
