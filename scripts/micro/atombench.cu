@@ -47,7 +47,27 @@ __global__ void f32x4_local(float* a, uint32_t n, uint32_t m) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1.f), "f"(2.f), "f"(3.f), "f"(1.f) : "memory");
   }
 }
-int main() {
+// count-grid pattern (k_count on cluster2B): 4-B REDs to `m` random cells spread over a 64 MB grid
+__global__ void u32x1_grid(unsigned* a, uint32_t n, uint32_t m) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t s = (uint32_t)(((uint64_t)(hsh(i) % m) * 2654435761u) & ((1u << 24) - 1));
+    atomicAdd(a + s, 1u);
+  }
+}
+static void grid_reds() {
+  const uint32_t n = 400000000;
+  void* a; cudaMalloc(&a, (size_t)4 << 24); cudaMemset(a, 0, (size_t)4 << 24);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (uint32_t m : {200000u, 2000000u, 16000000u}) {
+    for (int w = 0; w < 2; ++w) u32x1_grid<<<148 * 8, 256>>>((unsigned*)a, n, m);
+    cudaEventRecord(e0); u32x1_grid<<<148 * 8, 256>>>((unsigned*)a, n, m); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("u32 REDs, %8u random cells of a 64 MB grid: %.2f ms for %u = %.1f G/s\n", m, ms, n, n / ms / 1e6);
+  }
+  cudaFree(a);
+}
+int main(int argc, char**) {
+  if (argc > 1) { grid_reds(); return 0; }
   const uint32_t n = 20000000;
   for (uint32_t m : {5000000u, 1000000u, 100000u}) {
     void* a; cudaMalloc(&a, (size_t)m * 16); cudaMemset(a, 0, (size_t)m * 16);
