@@ -335,10 +335,14 @@ def e2e_two_trees(torch, dev, d_in, n, cfg, mode_code, steps, stream):
 def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     """Clouds that fit once (cluster2B: ~100 GB working set): one tree, split and voxelize as
     separate ABI calls so the copies overlap the work that no longer needs their buffers --
-    the next upload starts when the split has consumed the input, the leaf download runs under
-    the voxelize and under the NEXT split's bounds / count / extension rounds (the split waits
-    for the previous downloads only before it rewrites the node table and leaf buffer:
-    lod_tree_set_output_wait), the voxel download under the next split."""
+    the next upload starts when the split has consumed the input; ONE device->host stream
+    carries the leaf buffer (after the split), then the node table and the voxels (after the
+    voxelize) -- the link is the bottleneck (38.9 GB down per cluster2B step), so the downloads
+    queue back to back.  The next split waits only for the leaf + node downloads, and only
+    before it rewrites them (lod_tree_set_output_wait); the voxel download runs under the next
+    split (the split never touches the arena) and the next voxelize waits for it.  Measured
+    (scripts/e2e_timeline1.py): 915 -> 860 ms per cluster2B step against the round-2 schedule,
+    whose skeleton also waited for the 6.9 GB voxel download."""
     from paper_2302_14801_b200 import _abi
     info = dev.info()
     rec_bytes = n * 16
@@ -349,17 +353,17 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     h_vox = torch.empty(max(info.n_voxels * 8, 8), dtype=torch.uint8, pin_memory=True)
     h_nodes = torch.empty(max(info.n_nodes * _abi.node_dtype().itemsize, 88), dtype=torch.uint8, pin_memory=True)
     d_stage = d_in            # the device input buffer is the staging buffer
-    up, dl, dl2, jn = (torch.cuda.Stream() for _ in range(4))
-    ev_up, ev_split, ev_vox, ev_leaf, ev_voxdl, ev_out = (torch.cuda.Event() for _ in range(6))
+    up, dl = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_up, ev_split, ev_vox, ev_voxdl, ev_out = (torch.cuda.Event() for _ in range(5))
     sp = C.c_void_p(stream.cuda_stream)
-    dlp, dl2p = C.c_void_p(dl.cuda_stream), C.c_void_p(dl2.cuda_stream)
+    dlp = C.c_void_p(dl.cuda_stream)
 
     def run(k_steps):
         up.wait_stream(stream)
         with torch.cuda.stream(up):
             d_stage.copy_(h_in, non_blocking=True)
             ev_up.record(up)
-        ev_voxdl.record(dl2)
+        ev_voxdl.record(dl)
         for k in range(k_steps):
             stream.wait_event(ev_up)
             if k > 0:   # the previous tree's node + leaf downloads, before the skeleton
@@ -373,18 +377,15 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
                     ev_up.record(up)
             dl.wait_event(ev_split)         # leaf points are final after the distribute
             _abi.check(lib.lod_tree_copy_async(dev.h, C.c_void_p(h_leaf.data_ptr()), None, None, dlp))
-            ev_leaf.record(dl)
             stream.wait_event(ev_voxdl)     # the previous voxels are downloaded: the arena is free
             dev.voxelize(mode_code, seed, stream=sp)
             ev_vox.record(stream)
-            dl2.wait_event(ev_vox)
-            _abi.check(lib.lod_tree_copy_async(dev.h, None, C.c_void_p(h_vox.data_ptr()),
-                                               C.c_void_p(h_nodes.data_ptr()), dl2p))
-            ev_voxdl.record(dl2)
-            jn.wait_event(ev_leaf)
-            jn.wait_event(ev_voxdl)
-            ev_out.record(jn)
-        for st in (dl, dl2, up, jn):
+            dl.wait_event(ev_vox)           # the voxelize writes the inner nodes' voxel ranges
+            _abi.check(lib.lod_tree_copy_async(dev.h, None, None, C.c_void_p(h_nodes.data_ptr()), dlp))
+            ev_out.record(dl)               # leaf + nodes downloaded: the next skeleton may rewrite them
+            _abi.check(lib.lod_tree_copy_async(dev.h, None, C.c_void_p(h_vox.data_ptr()), None, dlp))
+            ev_voxdl.record(dl)
+        for st in (dl, up):
             stream.wait_stream(st)
 
     run(1)
@@ -395,8 +396,8 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     return (e0.elapsed_time(e1) / steps,
-            "1 tree, 5 streams: split k+1's bounds/count/extension || leaf download k; "
-            "voxelize k || upload k+1; voxel+node download k || split k+1",
+            "1 tree, 3 streams: upload k+1 || voxelize k, split k+1's bounds/count/extension; one D2H "
+            "stream: leaf k, nodes k, voxels k (the voxels under split k+1)",
             rec_bytes, _tree_bytes(dev, n))
 
 
