@@ -342,7 +342,9 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     before it rewrites them (lod_tree_set_output_wait); the voxel download runs under the next
     split (the split never touches the arena) and the next voxelize waits for it.  Measured
     (scripts/e2e_timeline1.py): 915 -> 860 ms per cluster2B step against the round-2 schedule,
-    whose skeleton also waited for the 6.9 GB voxel download."""
+    whose skeleton also waited for the 6.9 GB voxel download.  Both directions move as 256-MB
+    pieces over two streams (two copy engines; lod_tree_copy_async splits its copies the same
+    way): 45.8 -> 49.2 GB/s per direction under duplex load (scripts/micro/pcie_big.py)."""
     from paper_2302_14801_b200 import _abi
     info = dev.info()
     rec_bytes = n * 16
@@ -353,16 +355,23 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     h_vox = torch.empty(max(info.n_voxels * 8, 8), dtype=torch.uint8, pin_memory=True)
     h_nodes = torch.empty(max(info.n_nodes * _abi.node_dtype().itemsize, 88), dtype=torch.uint8, pin_memory=True)
     d_stage = d_in            # the device input buffer is the staging buffer
-    up, dl = torch.cuda.Stream(), torch.cuda.Stream()
+    up, up2, dl = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    piece = 256 << 20
+
+    def upload():   # 256-MB pieces over two streams: two copy engines (lod_tree_copy_async does the same down)
+        up2.wait_stream(up)
+        for k, o in enumerate(range(0, rec_bytes, piece)):
+            with torch.cuda.stream(up2 if k & 1 else up):
+                d_stage[o:o + piece].copy_(h_in[o:o + piece], non_blocking=True)
+        up.wait_stream(up2)
     ev_up, ev_split, ev_vox, ev_voxdl, ev_out = (torch.cuda.Event() for _ in range(5))
     sp = C.c_void_p(stream.cuda_stream)
     dlp = C.c_void_p(dl.cuda_stream)
 
     def run(k_steps):
         up.wait_stream(stream)
-        with torch.cuda.stream(up):
-            d_stage.copy_(h_in, non_blocking=True)
-            ev_up.record(up)
+        upload()
+        ev_up.record(up)
         ev_voxdl.record(dl)
         for k in range(k_steps):
             stream.wait_event(ev_up)
@@ -372,9 +381,8 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
             ev_split.record(stream)
             if k + 1 < k_steps:             # the split consumed the input: upload the next one
                 up.wait_event(ev_split)
-                with torch.cuda.stream(up):
-                    d_stage.copy_(h_in, non_blocking=True)
-                    ev_up.record(up)
+                upload()
+                ev_up.record(up)
             dl.wait_event(ev_split)         # leaf points are final after the distribute
             _abi.check(lib.lod_tree_copy_async(dev.h, C.c_void_p(h_leaf.data_ptr()), None, None, dlp))
             stream.wait_event(ev_voxdl)     # the previous voxels are downloaded: the arena is free
@@ -385,7 +393,7 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
             ev_out.record(dl)               # leaf + nodes downloaded: the next skeleton may rewrite them
             _abi.check(lib.lod_tree_copy_async(dev.h, None, C.c_void_p(h_vox.data_ptr()), None, dlp))
             ev_voxdl.record(dl)
-        for st in (dl, up):
+        for st in (dl, up, up2):
             stream.wait_stream(st)
 
     run(1)
@@ -396,8 +404,9 @@ def e2e_one_tree(torch, dev, d_in, n, cfg, mode_code, seed, steps, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     return (e0.elapsed_time(e1) / steps,
-            "1 tree, 3 streams: upload k+1 || voxelize k, split k+1's bounds/count/extension; one D2H "
-            "stream: leaf k, nodes k, voxels k (the voxels under split k+1)",
+            "1 tree: upload k+1 || voxelize k, split k+1's bounds/count/extension; one D2H stream: leaf k, "
+            "nodes k, voxels k (the voxels under split k+1); copies as 256-MB pieces over two copy engines "
+            "per direction",
             rec_bytes, _tree_bytes(dev, n))
 
 

@@ -122,6 +122,8 @@ struct lod_tree {
   // stream, back (K4/K5) on vback -- so level L+1's front overlaps level L's K3 and K4
   cudaStream_t vfront = nullptr, vback = nullptr;
   cudaEvent_t vev[6] = {};  // fork/join, front done, K3 done, back done (x2: depth parity), spare
+  cudaStream_t cstream = nullptr;  // second copy engine for large host copies (copy_split)
+  cudaEvent_t cev[2] = {};
   float stage_ms[5] = {};
 
   DevBuf state, pyr, node_idx, t8, te, meta, list, scan, slots;
@@ -1083,6 +1085,8 @@ lod_tree* lod_tree_create(int device) {
   for (auto& e : t->vev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&t->vback, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&t->vfront, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&t->cstream, cudaStreamNonBlocking);
+  for (auto& e : t->cev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   return t;
 }
 
@@ -1106,6 +1110,9 @@ void lod_tree_destroy(lod_tree* t) {
     if (e) cudaEventDestroy(e);
   if (t->vback) cudaStreamDestroy(t->vback);
   if (t->vfront) cudaStreamDestroy(t->vfront);
+  if (t->cstream) cudaStreamDestroy(t->cstream);
+  for (auto& e : t->cev)
+    if (e) cudaEventDestroy(e);
   if (t->host_state) cudaFreeHost(t->host_state);
   delete t;
 }
@@ -1169,6 +1176,27 @@ int lod_tree_set_output_wait(lod_tree* t, void* event) {
   return LOD_OK;
 }
 
+// Large device<->host copies go out as 256-MB pieces alternating between the caller's stream and
+// the tree's copy stream, so two copy engines serve the direction: with the other direction busy
+// (the pipelined e2e: next upload || this download) one engine reached 45.8 GB/s per direction,
+// two 49.2 (scripts/micro/pcie_big.py, 8-GB pinned buffers).  Ordered on `s` like one copy.
+static int copy_split(lod_tree* t, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+  constexpr size_t kPiece = 256ull << 20;
+  if (bytes < 2 * kPiece) {
+    CK(cudaMemcpyAsync(dst, src, bytes, kind, s));
+    return LOD_OK;
+  }
+  CK(cudaEventRecord(t->cev[0], s));
+  CK(cudaStreamWaitEvent(t->cstream, t->cev[0], 0));
+  size_t k = 0;
+  for (size_t o = 0; o < bytes; o += kPiece, ++k)
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kPiece, bytes - o), kind,
+                       (k & 1) ? t->cstream : s));
+  CK(cudaEventRecord(t->cev[1], t->cstream));
+  CK(cudaStreamWaitEvent(s, t->cev[1], 0));
+  return LOD_OK;
+}
+
 int lod_tree_copy_async(const lod_tree* tc, void* h_leaf, void* h_vox, lod_node* h_nodes, void* stream) {
   lod_tree* t = const_cast<lod_tree*>(tc);
   if (!t || !t->split_done) return fail(LOD_EVALUE, "no tree built");
@@ -1183,9 +1211,11 @@ int lod_tree_copy_async(const lod_tree* tc, void* h_leaf, void* h_vox, lod_node*
     CK(cudaMemcpyAsync(h_nodes, t->export_buf.p, (size_t)t->n_nodes * sizeof(lod_node), cudaMemcpyDeviceToHost, s));
   }
   const size_t rec = t->fmt == LOD_POINTS_F32 ? 16 : 32;
-  if (h_leaf && t->n) CK(cudaMemcpyAsync(h_leaf, t->leaf_pts.p, t->n * rec, cudaMemcpyDeviceToHost, s));
-  if (h_vox && t->n_voxels)
-    CK(cudaMemcpyAsync(h_vox, stored_voxels(t), t->n_voxels * 8, cudaMemcpyDeviceToHost, s));
+  int r;
+  if (h_leaf && t->n && (r = copy_split(t, h_leaf, t->leaf_pts.p, t->n * rec, cudaMemcpyDeviceToHost, s))) return r;
+  if (h_vox && t->n_voxels &&
+      (r = copy_split(t, h_vox, stored_voxels(t), t->n_voxels * 8, cudaMemcpyDeviceToHost, s)))
+    return r;
   return LOD_OK;
 }
 
