@@ -51,6 +51,8 @@ def unpack_records(raw: np.ndarray, fmt: int):
 
 _STAGE = {}          # device -> (pinned staging buffers, events, copy stream, lock)
 _STAGE_BYTES = 32 << 20
+_STAGE_THREADS = 8
+_STAGE_MIN = 4 << 20    # smaller arrays: one pageable copy (pageable runs at ~11 GB/s: 60 MB 6.0 -> 2.3 ms staged)
 _POOL = None
 _STAGE_LOCK = None
 
@@ -58,13 +60,16 @@ _STAGE_LOCK = None
 def host_to_device(arr: np.ndarray, device: int):
     """Contiguous host array -> uint8 device tensor of its bytes.  Large arrays are copied
     through two pinned 32-MB staging buffers: the host copy into one (split over 8 threads;
-    numpy copies release the GIL) overlaps the DMA of the other."""
+    numpy copies release the GIL) overlaps the DMA of the other.  Sizes, threads and the
+    threshold come from a sweep on the B200 box (scripts/micro/hoststage.py; 16 threads or
+    64-MB buffers were slower, page-locking the caller's array in place costs more than the
+    copy: scripts/micro/hostreg.py)."""
     global _POOL
     torch = _torch()
     src = np.ascontiguousarray(arr).reshape(-1).view(np.uint8)
     nb = src.nbytes
     out = torch.empty(max(nb, 1), dtype=torch.uint8, device=f"cuda:{device}")
-    if nb <= 2 * _STAGE_BYTES:
+    if nb <= _STAGE_MIN:
         if nb:
             out.copy_(torch.from_numpy(src))
         return out[:nb]
@@ -79,7 +84,7 @@ def host_to_device(arr: np.ndarray, device: int):
                               threading.Lock())
         if _POOL is None:
             import concurrent.futures as cf
-            _POOL = cf.ThreadPoolExecutor(8)
+            _POOL = cf.ThreadPoolExecutor(_STAGE_THREADS)
     bufs, evs, cs, lock = _STAGE[device]
     with lock:
         cs.wait_stream(torch.cuda.current_stream(device))
@@ -88,7 +93,8 @@ def host_to_device(arr: np.ndarray, device: int):
             b = k & 1
             evs[b].synchronize()                      # the DMA that last read this buffer is done
             dst = bufs[b].numpy()
-            parts = [(a, min(m, a + (m + 7) // 8)) for a in range(0, m, (m + 7) // 8)]
+            q = (m + _STAGE_THREADS - 1) // _STAGE_THREADS
+            parts = [(a, min(m, a + q)) for a in range(0, m, q)]
             list(_POOL.map(lambda ab: np.copyto(dst[ab[0]:ab[1]], src[off + ab[0]:off + ab[1]]), parts))
             with torch.cuda.stream(cs):
                 out[off:off + m].copy_(bufs[b][:m], non_blocking=True)
