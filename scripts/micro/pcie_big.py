@@ -10,8 +10,8 @@ h1 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
 h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
 d1 = torch.empty(n, dtype=torch.uint8, device="cuda")
 d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
-up = [torch.cuda.Stream(), torch.cuda.Stream()]
-dn = [torch.cuda.Stream(), torch.cuda.Stream()]
+up = [torch.cuda.Stream() for _ in range(4)]
+dn = [torch.cuda.Stream() for _ in range(4)]
 
 
 def copy(dst, src, streams, chunks):
@@ -35,7 +35,7 @@ def timed(fn, reps=2):
     return e0.elapsed_time(e1) / reps
 
 
-for chunks, ns in ((1, 1), (8, 2), (32, 2)):
+for chunks, ns in ((1, 1), (8, 2), (32, 2), (16 * gb, 2), (16 * gb, 3), (16 * gb, 4)):
     tag = f"{chunks} chunk(s) on {ns} stream(s)"
     ms = timed(lambda: copy(d1, h1, up[:ns], chunks))
     print(f"{gb} GB h2d  {tag:24s} {ms:8.1f} ms {n / ms / 1e6:6.1f} GB/s")
