@@ -135,7 +135,9 @@ int lod_tree_voxels(const lod_tree* tree, const void** d_ptr);
 /* Enqueue the whole tree's device->host copies on `stream` without waiting: leaf points,
  * voxels (stored order) and node table, each skipped when its pointer is NULL.  Host
  * buffers should be pinned; synchronize the stream before reading them.  Lets a caller
- * overlap the copies of build k with the upload / build of build k+1 (PCIe is duplex). */
+ * overlap the copies of build k with the upload / build of build k+1 (PCIe is duplex).
+ * Copies of >= 512 MB go out as 256-MB pieces alternating between `stream` and the tree's
+ * own copy stream (two copy engines), joined back into `stream`: ordered like one copy. */
 int lod_tree_copy_async(const lod_tree* tree, void* h_leaf_points, void* h_voxels, lod_node* h_nodes,
                         void* stream);
 /* The NEXT lod_split (or lod_dist_skeleton) on this tree makes its stream wait on `event` (a
