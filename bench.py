@@ -632,18 +632,25 @@ def main():
         e2e = {"value": n_total / (ems / 1000.0), "unit": "points/s", "h2d_bytes_per_step": hb,
                "d2h_bytes_per_step": db, "ms_per_step": ems, "pipeline": pipeline}
 
-    api = None
-    if world == 1 and not args.no_e2e and args.e2e_api_config:
-        api = e2e_api(torch, args.e2e_api_config, args.mode, max(3, min(args.steps, 10)), 2)
-
     device_bytes = dev.device_bytes()
-    target = None
-    if world == 1 and not args.no_target and args.config != "scene1B":
-        # the north star's own target (>= 4 G pts/s color filtering on a 1B-point cloud): the
-        # first 1e9 rows of the scene generator, device time of `target_steps` builds
+    api = target = None
+    want_api = world == 1 and not args.no_e2e and bool(args.e2e_api_config)
+    want_target = world == 1 and not args.no_target and args.config != "scene1B"
+    if want_api or want_target:
+        # release this build's tree, input and pinned host buffers first: the API legs allocate
+        # through torch's caching allocators, and with ~170 GB of HBM (and ~70 GB of pinned host
+        # memory) still held every call re-maps blocks (measured: the terrain20M API leg at
+        # 1.25 / 0.61 G pts/s inside the cluster2B run against 1.63 / 1.16 G on its own)
         del d_in
         dev.close()
         torch.cuda.empty_cache()
+        if hasattr(torch._C, "_host_emptyCache"):
+            torch._C._host_emptyCache()
+    if want_api:
+        api = e2e_api(torch, args.e2e_api_config, args.mode, max(3, min(args.steps, 10)), 2)
+    if want_target:
+        # the north star's own target (>= 4 G pts/s color filtering on a 1B-point cloud): the
+        # first 1e9 rows of the scene generator, device time of `target_steps` builds
         target = north_star_target(torch, args.mode, 1_000_000_000, 3)
 
     # ---- roofline (SURVEY 8(d) algorithmic bytes: B = 80 N + 16 E + 12 V) ----
