@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -130,6 +131,8 @@ struct lod_tree {
   DevBuf n_cell, n_val, n_parent, n_child, n_slot, n_extid, n_lvl, n_leaf, n_box, n_first, n_count;
   DevBuf leaf_node, leaf_first, leaf_count, leaf_pbox, leaf_pinv, depth_count, depth_off, depth_cursor, depth_lists;
   DevBuf leaf_pts, status, digit_base, tmp_rec, tmp_leaf, pkey, elist, abits;
+  DevBuf sgrid, cand_keys;  // candidate path of the single-GPU split (k_cand_sample)
+  bool cand = false;
   uint64_t elist_cap = 0;
   cudaEvent_t out_wait = nullptr;  // lod_tree_set_output_wait (next split only)
   bool use_abits = false;
@@ -296,6 +299,15 @@ SplitView make_view(lod_tree* t, const void* pts) {
   v.elist_cap = t->elist_cap;
   v.abits = t->use_abits ? t->abits.as<uint32_t>() : nullptr;
   v.te = t->te.as<int32_t>();
+  if (t->cand) {
+    v.sgrid = t->sgrid.as<uint32_t>();
+    v.cand_keys = t->cand_keys.as<uint32_t>();
+    v.cand = t->tmp_rec.as<uint4>();
+    v.cand_cap = t->tmp_rec.cap / 16;
+    // 0.85 of the samples a cell of T points gets (~3 sigma below it at T = 50k): fewer
+    // false candidates; an anchor below it is caught by k_cand_check (full-scan fallback)
+    v.cand_thresh = std::max<uint32_t>(1, (uint32_t)(0.85 * (double)t->cfg.T / kCandStride));
+  }
   v.meta = t->meta.as<ExtMeta>();
   v.n_ext = t->n_ext;
   v.n_cell = t->n_cell.as<uint64_t>();
@@ -337,6 +349,16 @@ int ceil_log2(uint64_t x) {
   do {                       \
     if ((expr) < 0) return fail(LOD_ECUDA, "internal scratch too small: %s", #expr); \
   } while (0)
+
+constexpr uint32_t kThreads_count() { return 256; }  // K_count's block (split_kernels.cu kThreads)
+// LODB200_NO_CAND=1 turns the candidate list off (A/B and a fallback switch)
+bool cand_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LODB200_NO_CAND");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 
 void mark(lod_tree* t, int i, cudaStream_t s) {
   if (t->timing) cudaEventRecord(t->ev[i], s);
@@ -382,6 +404,7 @@ int phase_init(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* 
   t->rounds.clear();
   t->elist_cap = 0;
   t->use_abits = false;
+  t->cand = false;
   t->ext_pyr_used = t->ext_tgt_used = 0;
   t->round_cur = 0;
   const int D = cfg->initial_depth;
@@ -411,6 +434,17 @@ int phase_bounds(lod_tree* t, const double* ub, cudaStream_t s) {
 }
 
 int phase_count(lod_tree* t, cudaStream_t s) {
+  if (t->cand) {  // sampled count -> candidate cells; K_count lists their points (tmp_rec)
+    const uint64_t fine_cells = 1ull << (3 * t->cfg.initial_depth);
+    CK(ensure(t->sgrid, fine_cells * 4));
+    CK(cudaMemsetAsync(t->sgrid.p, 0, fine_cells * 4, s));
+    CK(ensure(t->cand_keys, kCandCap * 4));
+    const uint64_t slack = (uint64_t)count_blocks(t->n) * (kThreads_count() / 32) * kCandChunk + kCandChunk;
+    CK(ensure(t->tmp_rec, (t->n + slack) * 16));
+    SplitView v = make_view(t, t->pts);
+    ScanScratch scr{t->scan.as<uint64_t>(), t->scan.cap / 8};
+    RUN(launch_cand_sample(t->fmt, v, scr, s));
+  }
   SplitView v = make_view(t, t->pts);
   if (t->n) RUN(launch_count(t->fmt, v, s));
   mark(t, 1, s);
@@ -433,6 +467,7 @@ int phase_anchors(lod_tree* t, uint32_t* cur, cudaStream_t s) {
   if ((r = check_errors(t, s))) return r;
   *cur = (uint32_t)t->host_state->count_a;
   if (*cur) RUN(launch_find_anchors(v, t->list.as<uint64_t>(), scr, s, true));  // none: no store pass
+  if (*cur && t->cand) RUN(launch_cand_check(v, t->list.as<uint64_t>(), *cur, s));
   // anchor bitmap for the first extension round's membership test (2 MB at depth 8)
   t->use_abits = *cur && 3 * D <= 27;
   if (t->use_abits) {
@@ -669,6 +704,10 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   int r = phase_init(t, pts, n, fmt, ub, cfg, s);
   if (r) return r;
   t->n_global = n;
+  // candidate list for the first extension round: clouds large enough for the sampled count
+  // to see a cell of T points (and a main grid whose candidate bitmap is small)
+  t->cand = cand_enabled() && cfg->max_depth > cfg->initial_depth && cfg->initial_depth <= 9 &&
+            n >= (1ull << 27) && n / ((uint64_t)cfg->T + 1) >= 1;  // smaller: its fixed ~50 us outweighs
   if ((r = phase_bounds(t, ub, s)) || (r = phase_count(t, s))) return r;
   uint32_t cur = 0;
   if ((r = phase_anchors(t, &cur, s))) return r;

@@ -61,7 +61,10 @@ struct DevState {
   uint64_t count_b;
   unsigned long long vox_cursor;  // voxel arena bump pointer
   uint32_t work[kMaxDepth + 1];   // per-depth node tickets for the voxelizer
-  uint32_t pad;
+  uint32_t cand_miss;             // candidate list unusable (too many candidate cells / an anchor missed)
+  uint64_t cand_cells;            // candidate cells of the sampled count
+  unsigned long long cand_est;    // their sampled points (x kCandStride ~ candidate points)
+  unsigned long long cand_n;      // candidate-list slots handed out (K_count, per-warp chunks)
 };
 
 __device__ __forceinline__ void raise_err(DevState* st, uint32_t bit, uint32_t detail = 0,

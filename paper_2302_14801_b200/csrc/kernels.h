@@ -28,6 +28,13 @@ struct SplitView {
   uint64_t elist_cap;
   uint32_t* abits;        // anchor bitmap over the main finest grid (null: test t8)
   int32_t* te;            // ext finest levels: same encoding
+  // candidate list (single-GPU split, LOD_CAND): points of the cells a sampled count marks as
+  // possibly over T, with their exact depth-16 cells, so the first extension round reads no records
+  uint32_t* sgrid;        // sampled counts over the main finest grid (null: candidate path off)
+  uint32_t* cand_keys;    // candidate cells (ascending), <= kCandCap
+  uint4* cand;            // {index, main finest key, x | y << 16, z}; index ~0u = hole
+  uint64_t cand_cap;
+  uint32_t cand_thresh;   // a cell is a candidate at >= cand_thresh samples
   ExtMeta* meta;
   uint32_t n_ext;
   // node table
@@ -92,6 +99,12 @@ __device__ __forceinline__ int32_t leaf_of_point(const SplitView& v, const Cell1
 int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const double* user_bounds,
                   cudaStream_t s);
 int launch_count(int fmt, const SplitView& v, cudaStream_t s);
+constexpr uint32_t kCandCap = 2048;   // candidate cells the count kernel holds in shared memory
+constexpr uint32_t kCandStride = 128; // every kCandStride-th point is sampled
+constexpr uint32_t kCandChunk = 256;  // list slots a warp reserves at a time (a multiple of 32)
+uint32_t count_blocks(uint64_t n);  // K_count's grid
+int launch_cand_sample(int fmt, const SplitView& v, ScanScratch& scr, cudaStream_t s);
+int launch_cand_check(const SplitView& v, const uint64_t* anchors, uint32_t n_anchors, cudaStream_t s);
 // count pass (store = false; hit count -> st->count_a), then, if any, the store pass
 int launch_find_anchors(const SplitView& v, uint64_t* list, ScanScratch& scr, cudaStream_t s, bool store);
 int launch_find_subanchors(const SplitView& v, uint32_t first_ext, uint32_t n_ext_round, int ext_levels,

@@ -159,20 +159,107 @@ constexpr int kCountUnroll = 4;
 constexpr int kHotSlots = LOD_HOT_SLOTS;  // per-CTA hot-counter cache (common.cuh HotCounts)
 constexpr int kHotReset = LOD_HOT_RESET;  // loop trips between flushes (64 x 1024 points per CTA)
 
+// A point's main finest-level key: certified fp32 cell first, exact fp64 otherwise (H1).
 template <int FMT>
+__device__ __forceinline__ uint32_t point_key(const typename Rec<FMT>::Raw& r, const Frame32& fr, float lim,
+                                              const DevState& st, int D, bool& bad) {
+  uint32_t cx, cy, cz;
+  if (FMT == LOD_POINTS_F32 && fast_cell(Rec<FMT>::xf(r), fr.lo[0], fr.s, fr.band, lim, cx) &&
+      fast_cell(Rec<FMT>::yf(r), fr.lo[1], fr.s, fr.band, lim, cy) &&
+      fast_cell(Rec<FMT>::zf(r), fr.lo[2], fr.s, fr.band, lim, cz))
+    return (cx << (2 * D)) | (cy << D) | cz;
+  return (uint32_t)level_key(cell16<FMT>(r, st, bad), D);
+}
+
+// Candidate cells in shared memory: open addressing over 2 x kCandCap slots.
+constexpr uint32_t kCandSlots = 2 * kCandCap;
+__device__ __forceinline__ uint32_t cand_slot(uint32_t k) { return (k * 0x9E3779B1u) >> (32 - 12); }
+static_assert(kCandSlots == 4096, "cand_slot hashes to 12 bits");
+__device__ __forceinline__ bool cand_probe(const uint32_t* h, uint32_t k) {
+  uint32_t s = cand_slot(k);
+  while (true) {
+    const uint32_t c = h[s];
+    if (c == k) return true;
+    if (c == 0xFFFFFFFFu) return false;
+    s = (s + 1) & (kCandSlots - 1);
+  }
+}
+
+// K_count.  CAND (single-GPU split): points of the candidate cells (sampled count, below) are
+// also appended, with their exact depth-16 cells, to the candidate list -- each warp fills
+// kCandChunk-slot chunks it reserves with one atomic, unused slots become holes -- so the
+// first extension round reads 16 B per candidate instead of gathering records (cluster2B:
+// 1 in 10 records, a 128-B line each, 25.6 GB).
+// The list pays only when candidates are a minority of the points (clustered clouds): at most
+// kCandCap candidate cells, and an estimated (sampled) candidate count <= n / 8 (measured: cluster2B,
+// 10 %, gains; scene500M, 21 %, loses -- K_count's extra work outweighs the gathers it saves).
+__device__ __forceinline__ bool cand_usable(const DevState& st, uint64_t n) {
+  return st.cand_cells > 0 && st.cand_cells <= kCandCap && st.cand_est * (uint64_t)kCandStride <= n / 8;
+}
+
+// One warp writes 32 list slots of its chunk (chunks are kCandChunk slots, a multiple of 32):
+// lane's candidate `it` {index, key} with its depth-16 cell if `have`, else a hole.
+template <int FMT>
+__device__ __forceinline__ void cand_emit(const SplitView& v, const DevState& st, const Frame32& f16, uint2 it,
+                                          bool have, unsigned long long& wbase, uint32_t& wleft, int lane, bool& bad) {
+  if (wleft == 0) {  // uniform
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(&v.st->cand_n, (unsigned long long)kCandChunk);
+    wbase = __shfl_sync(0xFFFFFFFFu, b, 0);
+    wleft = kCandChunk;
+  }
+  uint4 e = make_uint4(~0u, 0, 0, 0);
+  if (have) {
+    const auto r = Rec<FMT>::load(v.pts, it.x);
+    Cell16 cc;  // certified fp32 first (as K_count's main key), exact fp64 otherwise
+    if (!(FMT == LOD_POINTS_F32 && fast_cell(Rec<FMT>::xf(r), f16.lo[0], f16.s, f16.band, 65536.f, cc.x) &&
+          fast_cell(Rec<FMT>::yf(r), f16.lo[1], f16.s, f16.band, 65536.f, cc.y) &&
+          fast_cell(Rec<FMT>::zf(r), f16.lo[2], f16.s, f16.band, 65536.f, cc.z)))
+      cc = cell16<FMT>(r, st, bad);
+    e = make_uint4(it.x, it.y, cc.x | (cc.y << 16), cc.z);
+  }
+  if (wbase + lane < v.cand_cap) v.cand[wbase + lane] = e;
+  wbase += 32;
+  wleft -= 32;
+}
+
+template <int FMT, bool CAND>
 __global__ void __launch_bounds__(kThreads, 4) k_count(SplitView v) {
   pdl_wait();
   __shared__ HotCounts<kHotSlots> hot;
+  __shared__ uint32_t chash[CAND ? kCandSlots : 1];
+  __shared__ Frame32 sf16;
+  // per warp: up to 63 pending candidates {index, key}; their depth-16 cells are taken 32 at a
+  // time, one per lane (record re-read from L2: this warp loaded it a few trips before), so the
+  // projection and the list store run at full warp width -- computing them inline for the ~3
+  // candidate lanes of a clustered cloud's warp-iteration was slower (cluster2B count 21.7 ->
+  // 25.4 ms)
+  __shared__ uint2 cbuf[CAND ? kThreads / 32 : 1][CAND ? 64 : 1];
   hot.clear();
-  __syncthreads();
   const DevState st = *v.st;
+  const bool cand_on = CAND && cand_usable(st, v.n);  // CTA-uniform
+  if (CAND && threadIdx.x == 0) sf16 = make_frame32(st.lo[0], st.lo[1], st.lo[2], st.size, 16);
+  if (CAND && cand_on) {
+    for (uint32_t i = threadIdx.x; i < kCandSlots; i += blockDim.x) chash[i] = 0xFFFFFFFFu;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < (uint32_t)st.cand_cells; i += blockDim.x) {
+      const uint32_t k = __ldg(v.cand_keys + i);
+      uint32_t sl = cand_slot(k);
+      while (atomicCAS(chash + sl, 0xFFFFFFFFu, k) != 0xFFFFFFFFu) sl = (sl + 1) & (kCandSlots - 1);
+    }
+  }
+  __syncthreads();
   const Frame32 fr = make_frame32(st.lo[0], st.lo[1], st.lo[2], st.size, v.D);
   const float lim = (float)(1u << v.D);
   uint32_t* grid = v.pyr + level_off(v.D);
   const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   bool bad = false;
   uint32_t trip = 0;
+  unsigned long long wbase = 0;  // warp-uniform: next free slot of the warp's chunk, slots left,
+  uint32_t wleft = 0;            // finished entries waiting in the warp's buffer
+  uint32_t wpend = 0;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < v.n; base += stride * kCountUnroll) {
     if (++trip % kHotReset == 0) hot.flush(grid);
     typename Rec<FMT>::Raw r[kCountUnroll];
@@ -187,15 +274,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_count(SplitView v) {
       bool valid = i < v.n;
       uint32_t key = 0;
       if (valid) {
-        uint32_t cx, cy, cz;
-        if (FMT == LOD_POINTS_F32 &&
-            fast_cell(Rec<FMT>::xf(r[u]), fr.lo[0], fr.s, fr.band, lim, cx) &&
-            fast_cell(Rec<FMT>::yf(r[u]), fr.lo[1], fr.s, fr.band, lim, cy) &&
-            fast_cell(Rec<FMT>::zf(r[u]), fr.lo[2], fr.s, fr.band, lim, cz))
-          key = (cx << (2 * v.D)) | (cy << v.D) | cz;
-        else
-          key = (uint32_t)level_key(cell16<FMT>(r[u], st, bad), v.D);
+        key = point_key<FMT>(r[u], fr, lim, st, v.D, bad);
         v.pkey[i] = key;  // reused by extension counting and the distribute (no re-projection)
+      }
+      if (CAND && cand_on) {
+        const bool c = valid && cand_probe(chash, key);
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
+        if (m) {
+          uint2* wb = cbuf[threadIdx.x >> 5];
+          if (c) wb[wpend + __popc(m & lt)] = make_uint2((uint32_t)i, key);
+          wpend += __popc(m);
+          if (wpend >= 32) {  // uniform: 32 entries to the warp's chunk
+            __syncwarp();
+            cand_emit<FMT>(v, st, sf16, wb[lane], true, wbase, wleft, lane, bad);
+            const uint2 rest = wb[32 + lane];
+            __syncwarp();
+            wb[lane] = rest;
+            __syncwarp();
+            wpend -= 32;
+          }
+        }
       }
       // warp-uniform cell (coherent scans): one aggregated add; otherwise through the
       // CTA's hot-counter cache (interleaved dense clusters), else one RED per point
@@ -209,16 +307,94 @@ __global__ void __launch_bounds__(kThreads, 4) k_count(SplitView v) {
       }
     }
   }
+  if (CAND && cand_on) {
+    if (wpend) {  // uniform: the last < 32 entries, holes after them
+      __syncwarp();
+      cand_emit<FMT>(v, st, sf16, cbuf[threadIdx.x >> 5][lane], lane < wpend, wbase, wleft, lane, bad);
+    }
+    for (uint32_t q = lane; q < wleft; q += 32)  // the rest of the last chunk: holes
+      if (wbase + q < v.cand_cap) v.cand[wbase + q] = make_uint4(~0u, 0, 0, 0);
+  }
   hot.flush(grid);
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) raise_err(v.st, ERR_OUTSIDE);
 }
 
+uint32_t count_blocks(uint64_t n) { return (uint32_t)std::min<uint64_t>((n + kThreads - 1) / kThreads, 148ull * 8); }
+
 int launch_count(int fmt, const SplitView& v, cudaStream_t s) {
-  uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
-  if (fmt == LOD_POINTS_F32)
-    launch_pdl(k_count<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
-  else
-    launch_pdl(k_count<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
+  const uint32_t blocks = count_blocks(v.n);
+  if (v.sgrid) {
+    if (fmt == LOD_POINTS_F32) launch_pdl(k_count<LOD_POINTS_F32, true>, blocks, kThreads, 0, s, v);
+    else launch_pdl(k_count<LOD_POINTS_F64, true>, blocks, kThreads, 0, s, v);
+  } else {
+    if (fmt == LOD_POINTS_F32) launch_pdl(k_count<LOD_POINTS_F32, false>, blocks, kThreads, 0, s, v);
+    else launch_pdl(k_count<LOD_POINTS_F64, false>, blocks, kThreads, 0, s, v);
+  }
+  return 1;
+}
+
+// Candidate cells: every kCandStride-th point counted into sgrid; a cell with >= cand_thresh
+// samples (half the samples a cell of T points would get) is a candidate.  Any anchor that is
+// not a candidate (adversarial input orders) turns the list off (k_cand_check) and the first
+// extension round falls back to the full scan, so the sample only decides speed, never results.
+template <int FMT>
+__global__ void __launch_bounds__(kThreads) k_cand_sample(SplitView v) {
+  pdl_wait();
+  __shared__ HotCounts<kHotSlots> hot;  // dense clusters: a few cells take most samples
+  hot.clear();
+  __syncthreads();
+  const DevState st = *v.st;
+  const Frame32 fr = make_frame32(st.lo[0], st.lo[1], st.lo[2], st.size, v.D);
+  const float lim = (float)(1u << v.D);
+  const uint64_t ns = (v.n + kCandStride - 1) / kCandStride;
+  bool bad = false;  // points outside the cube are reported by K_count
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += (uint64_t)gridDim.x * blockDim.x) {
+    // one point at a hashed offset inside every block of kCandStride: periodic input orders
+    // (e.g. every 10th point in one cell) cannot dodge a fixed stride
+    const uint64_t i = j * kCandStride + (((uint32_t)j * 0x9E3779B1u) >> 25);
+    if (i >= v.n) continue;
+    const auto r = Rec<FMT>::load(v.pts, i);
+    const uint32_t key = point_key<FMT>(r, fr, lim, st, v.D, bad);
+    if (!bad) hot.add(v.sgrid, key, 1u);
+  }
+  hot.flush(v.sgrid);
+}
+
+struct CandF {
+  const uint32_t* sgrid;
+  uint32_t thresh;
+  uint32_t* out;
+  __device__ bool pred(uint64_t i) const { return __ldg(sgrid + i) >= thresh; }
+  unsigned long long* est;
+  __device__ void emit(uint64_t i, uint64_t pos) const {
+    if (pos < kCandCap) out[pos] = (uint32_t)i;
+    atomicAdd(est, (unsigned long long)__ldg(sgrid + i));
+  }
+};
+
+int launch_cand_sample(int fmt, const SplitView& v, ScanScratch& scr, cudaStream_t s) {
+  const uint64_t ns = (v.n + kCandStride - 1) / kCandStride;
+  const uint32_t blocks = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((ns + kThreads - 1) / kThreads, 148ull * 8));
+  if (fmt == LOD_POINTS_F32) launch_pdl(k_cand_sample<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
+  else launch_pdl(k_cand_sample<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
+  const int r = device_compact(1ull << (3 * v.D), CandF{v.sgrid, v.cand_thresh, v.cand_keys, &v.st->cand_est}, scr, &v.st->cand_cells, s);
+  return r < 0 ? r : r + 1;
+}
+
+__global__ void k_cand_check(SplitView v, const uint64_t* anchors, uint32_t na) {
+  pdl_wait();
+  const DevState* st = v.st;
+  bool miss = false;
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    miss = !cand_usable(*st, v.n) || st->cand_n > v.cand_cap;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < na; j += gridDim.x * blockDim.x)
+    miss |= __ldg(v.sgrid + anchors[j]) < v.cand_thresh;
+  if (miss) atomicOr(&v.st->cand_miss, 1u);
+}
+
+int launch_cand_check(const SplitView& v, const uint64_t* anchors, uint32_t na, cudaStream_t s) {
+  launch_pdl(k_cand_check, std::max<uint32_t>(1, std::min<uint32_t>(ceil_div_u32(na, kThreads), 148)), kThreads, 0, s,
+             v, anchors, na);
   return 1;
 }
 
@@ -330,6 +506,7 @@ __device__ __forceinline__ bool is_anchor(const SplitView& v, uint32_t key) {
 template <int FMT>
 __global__ void __launch_bounds__(kThreads) k_ext_first(SplitView v) {
   pdl_wait();
+  if (v.sgrid && !v.st->cand_miss) return;  // k_ext_first_list did the round from the candidate list
   constexpr int U = 8;   // 16 measured slower (registers: 3 CTAs/SM either way, +10% time)
   __shared__ HotCounts<kHotSlots> hot;
   __shared__ uint32_t wsum[kThreads / 32 + 1];
@@ -380,6 +557,57 @@ __global__ void __launch_bounds__(kThreads) k_ext_first(SplitView v) {
   if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) raise_err(v.st, ERR_OUTSIDE);
 }
 
+// First extension round from the candidate list (K_count): the candidates inside anchor cells
+// are the extension points; their depth-16 cells come with them, so no record is read.
+__global__ void __launch_bounds__(kThreads) k_ext_first_list(SplitView v) {
+  pdl_wait();
+  if (v.st->cand_miss) return;  // k_ext_first scans every point instead
+  constexpr int U = 4;
+  __shared__ HotCounts<kHotSlots> hot;
+  __shared__ uint32_t wsum[kThreads / 32 + 1];
+  __shared__ unsigned long long lbase;
+  hot.clear();
+  __syncthreads();
+  const uint64_t n = min((uint64_t)v.st->cand_n, v.cand_cap);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t since_flush = 0;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - threadIdx.x < n; i0 += U * stride) {
+    uint4 q[U];
+    int32_t t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) q[u] = __ldcs(v.cand + min(i0 + u * stride, n - 1));
+    uint32_t flags = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      t[u] = -1;
+      if (i0 + u * stride < n && q[u].x != ~0u && is_anchor(v, q[u].y)) {
+        t[u] = v.t8[q[u].y];
+        flags |= 1u << u;
+      }
+    }
+    uint32_t tot;
+    uint32_t x = block_excl_scan<uint32_t, kThreads>((uint32_t)__popc(flags), &tot, wsum);
+    if (tot == 0) continue;  // uniform
+    if (threadIdx.x == 0) lbase = atomicAdd(&v.st->ext_n, (unsigned long long)tot);
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if ((flags >> u) & 1) {
+        const uint64_t pos = lbase + x++;
+        if (pos < v.elist_cap) v.elist[pos] = make_uint4(q[u].x, (uint32_t)(-(t[u] + 2)), q[u].z, q[u].w);
+        ext_count_point(v, hot, Cell16{q[u].z & 0xFFFF, q[u].z >> 16, q[u].w}, t[u], 0);
+      }
+    since_flush += tot;
+    if (since_flush >= 16384) {  // uniform
+      hot.flush(v.pyr);
+      since_flush = 0;
+    } else {
+      __syncthreads();  // lbase is rewritten by the next trip
+    }
+  }
+  hot.flush(v.pyr);
+}
+
 __global__ void __launch_bounds__(kThreads) k_ext_more(SplitView v, uint32_t round_first) {
   pdl_wait();
   __shared__ HotCounts<kHotSlots> hot;
@@ -404,9 +632,15 @@ __global__ void __launch_bounds__(kThreads) k_ext_more(SplitView v, uint32_t rou
 
 int launch_ext_count(int fmt, const SplitView& v, uint32_t round_first, cudaStream_t s) {
   if (round_first == 0) {
+    int r = 1;
+    if (v.sgrid) {  // candidate list first; k_ext_first returns at once unless it was unusable
+      launch_pdl(k_ext_first_list, 148 * 8, kThreads, 0, s, v);
+      ++r;
+    }
     uint32_t blocks = (uint32_t)std::min<uint64_t>((v.n + kThreads - 1) / kThreads, 148ull * 8);
     if (fmt == LOD_POINTS_F32) launch_pdl(k_ext_first<LOD_POINTS_F32>, blocks, kThreads, 0, s, v);
     else launch_pdl(k_ext_first<LOD_POINTS_F64>, blocks, kThreads, 0, s, v);
+    return r;
   } else {
     launch_pdl(k_ext_more, 148 * 8, kThreads, 0, s, v, round_first);
   }
