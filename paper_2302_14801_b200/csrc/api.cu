@@ -352,6 +352,12 @@ int ceil_log2(uint64_t x) {
 
 constexpr uint32_t kThreads_count() { return 256; }  // K_count's block (split_kernels.cu kThreads)
 // LODB200_NO_CAND=1 turns the candidate list off (A/B and a fallback switch)
+// below 2^27 points the sample + candidate compaction (~50 us) outweighs what it saves;
+// LODB200_CAND_MIN_N overrides (tests run the golden cases through both extension paths)
+uint64_t cand_min_points() {
+  const char* e = getenv("LODB200_CAND_MIN_N");
+  return e ? strtoull(e, nullptr, 10) : (1ull << 27);
+}
 bool cand_enabled() {
   static const bool on = [] {
     const char* e = getenv("LODB200_NO_CAND");
@@ -707,7 +713,7 @@ int do_split(lod_tree* t, const void* pts, uint64_t n, int fmt, const double* ub
   // candidate list for the first extension round: clouds large enough for the sampled count
   // to see a cell of T points (and a main grid whose candidate bitmap is small)
   t->cand = cand_enabled() && cfg->max_depth > cfg->initial_depth && cfg->initial_depth <= 9 &&
-            n >= (1ull << 27) && n / ((uint64_t)cfg->T + 1) >= 1;  // smaller: its fixed ~50 us outweighs
+            n >= cand_min_points() && n / ((uint64_t)cfg->T + 1) >= 1;
   if ((r = phase_bounds(t, ub, s)) || (r = phase_count(t, s))) return r;
   uint32_t cur = 0;
   if ((r = phase_anchors(t, &cur, s))) return r;

@@ -62,3 +62,17 @@ def test_gpu_matches_reference_large(case):
     if not golden_available(case["name"]):
         pytest.skip("golden not generated")
     run_case(case)
+
+
+EXT_CASES = [c for c in CASES if (c["quick"] or c["name"] == "cluster1500k_T2000") and any(
+    k in c["name"] for k in ("cluster", "stadium", "depth_limit", "initial6", "identical", "many_leaves"))]
+
+
+@pytest.mark.parametrize("case", EXT_CASES, ids=[c["name"] for c in EXT_CASES])
+def test_gpu_candidate_list_path(case, monkeypatch):
+    """The first extension round from K_count's candidate list (on by default from 2^27 points):
+    forced on for the golden cases with extension grids.  At their small T the sampled count
+    misses some anchors, so these runs take the candidate path or its full-scan fallback; both
+    must equal the reference."""
+    monkeypatch.setenv("LODB200_CAND_MIN_N", "0")
+    run_case(case)
