@@ -1450,7 +1450,10 @@ int lod_workspace_bytes(uint64_t n, int format, const lod_config* cfg, int mode,
   b += main_cells * 8 * 2;                              // node slots, scan scratch
   b += n * 4;                                           // pkey
   b += n * rec;                                         // leaf buffer
-  b += leaves_max >= (1u << kRadixMaxBits) ? n * rec : 0;  // 2-pass distribute record copy
+  // 2-pass distribute record copy; the first extension round's candidate list shares it
+  const bool cand = cand_enabled() && cfg->max_depth > D && D <= 9 && n >= cand_min_points();
+  b += std::max<uint64_t>(leaves_max >= (1u << kRadixMaxBits) ? n * rec : 0, cand ? n * 16 + (40ull << 20) : 0);
+  b += cand ? fine * 4 : 0;                             // sampled counts
   b += n * 8;                                           // leaf ids (input + sorted order)
   b += n / 2;                                           // tile digit counts (11-bit digits)
   b += n / 10 * 16;                                     // extension-point list (10% in extension grids)
