@@ -99,7 +99,10 @@ __device__ __forceinline__ int32_t leaf_of_point(const SplitView& v, const Cell1
 int launch_bounds(int fmt, const void* pts, uint64_t n, DevState* st, const double* user_bounds,
                   cudaStream_t s);
 int launch_count(int fmt, const SplitView& v, cudaStream_t s);
-constexpr uint32_t kCandCap = 2048;   // candidate cells the count kernel holds in shared memory
+#ifndef LOD_CAND_CAP
+#define LOD_CAND_CAP 2048
+#endif
+constexpr uint32_t kCandCap = LOD_CAND_CAP;  // candidate cells the count kernel holds in shared memory
 constexpr uint32_t kCandStride = 128; // every kCandStride-th point is sampled
 constexpr uint32_t kCandChunk = 256;  // list slots a warp reserves at a time (a multiple of 32)
 uint32_t count_blocks(uint64_t n);  // K_count's grid

@@ -173,8 +173,9 @@ __device__ __forceinline__ uint32_t point_key(const typename Rec<FMT>::Raw& r, c
 
 // Candidate cells in shared memory: open addressing over 2 x kCandCap slots.
 constexpr uint32_t kCandSlots = 2 * kCandCap;
-__device__ __forceinline__ uint32_t cand_slot(uint32_t k) { return (k * 0x9E3779B1u) >> (32 - 12); }
-static_assert(kCandSlots == 4096, "cand_slot hashes to 12 bits");
+constexpr int kCandBits = __builtin_ctz(kCandSlots);
+static_assert((kCandSlots & (kCandSlots - 1)) == 0, "power-of-two slots");
+__device__ __forceinline__ uint32_t cand_slot(uint32_t k) { return (k * 0x9E3779B1u) >> (32 - kCandBits); }
 __device__ __forceinline__ bool cand_probe(const uint32_t* h, uint32_t k) {
   uint32_t s = cand_slot(k);
   while (true) {
