@@ -26,7 +26,8 @@ stage, out = 0, collections.OrderedDict((s, 0.0) for s in
 names = list(out)
 for d in items[start:]:
     k = d["k"]
-    if stage == 0 and ("k_compact" in k or "k_ext" in k or "k_mark_anchors" in k or "k_merge" in k):
+    # (the candidate-cell compaction, CandF, runs inside the count stage)
+    if stage == 0 and (("k_compact" in k and "CandF" not in k) or "k_ext" in k or "k_mark_anchors" in k or "k_merge" in k):
         stage = 1
     if stage <= 1 and ("k_mark_anchors" in k or "k_merge" in k):
         stage = 2
